@@ -8,6 +8,9 @@
 // `--impl reference` leg.  Each entry point names the reference symbol it
 // wraps.  Reference exceptions (sdpsim::Error, errors.hpp:22-34) are mapped
 // to 1 + Errc ordinal with the message kept in ref_last_error().
+#include <algorithm>
+#include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <random>
@@ -318,6 +321,81 @@ REF_SCHED(ref_alternative_f64, double, 1)
 REF_SCHED(ref_global_sync_i64, int64_t, 2)
 REF_SCHED(ref_global_sync_f32, float, 2)
 REF_SCHED(ref_global_sync_f64, double, 2)
+
+// CPU baseline of one MiCS step over a bounded sample of layers, through the
+// reference's own functions: per micro-step a per-layer parameter all_gather in
+// every partition group (forward and backward pass, simulator.cpp:265-280 order),
+// two_hop_micro_step over the sample's flat gradient, then two_hop_boundary.  The
+// reference has no optimizer; the sharded Adam of the B200 step is
+// added as a plain loop with the documented formula so both sides do the same
+// work.  Inputs are built outside the timed region; returns the best of `reps`
+// wall-clock seconds (std::chrono::steady_clock).
+double ref_step_sample(int threads, int n, int p, int s, int nlayers, const uint64_t* layer_params, int reps) {
+  double best = 1e300;
+  try {
+    GroupLayout layout = build_group_layout(n, p);
+    uint64_t len = 0;
+    for (int l = 0; l < nlayers; ++l) len += layer_params[l];
+    std::mt19937 rng(2205);
+    std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+    // bf16 parameter shards per layer per rank
+    std::vector<std::vector<Bytes>> shards(static_cast<size_t>(nlayers));
+    for (int l = 0; l < nlayers; ++l) {
+      const size_t c = (layer_params[l] + p - 1) / p * 2;
+      shards[size_t(l)].resize(size_t(n));
+      for (auto& b : shards[size_t(l)]) {
+        b.resize(c);
+        for (auto& x : b) x = static_cast<std::byte>(rng() & 0xff);
+      }
+    }
+    std::vector<std::vector<std::vector<float>>> grads(static_cast<size_t>(s),
+                                                       std::vector<std::vector<float>>(static_cast<size_t>(n)));
+    for (auto& st : grads)
+      for (auto& g : st) {
+        g.resize(len);
+        for (auto& v : g) v = dist(rng);
+      }
+    const size_t chunk = owned_chunk_elems(layout, len);
+    std::vector<float> param(chunk, 0.5f), m(chunk, 0.0f), v(chunk, 0.0f);
+    for (int rep = 0; rep < reps; ++rep) {
+      VirtualRankEngine engine(threads);
+      auto states = make_sync_states<float>(layout, len, s);
+      std::vector<std::vector<float>> P(size_t(n), param), M(size_t(n), m), V(size_t(n), v);
+      const auto t0 = std::chrono::steady_clock::now();
+      for (int t = 0; t < s; ++t) {
+        for (int pass = 0; pass < 2; ++pass)
+          for (int li = 0; li < nlayers; ++li) {
+            const int l = pass == 0 ? li : nlayers - 1 - li;
+            for (int g = 0; g < layout.num_partition_groups(); ++g) {
+              CollectiveGroup grp{layout.partition_groups[size_t(g)]};
+              std::vector<Bytes> in(shards[size_t(l)].begin() + g * p, shards[size_t(l)].begin() + (g + 1) * p);
+              auto out = all_gather(engine, grp, in);
+              (void)out;
+            }
+          }
+        two_hop_micro_step(engine, layout, states, grads[size_t(t)]);
+      }
+      two_hop_boundary(engine, layout, states);
+      const float b1 = 0.9f, b2 = 0.999f, omb1 = 0.1f, omb2 = 0.001f, eps = 1e-8f, ss = 1e-4f, bc2 = 0.0316f;
+      const float gs = 1.0f / float(n * s);
+      for (int r = 0; r < n; ++r) {
+        const auto& gsh = states[size_t(r)].shard;
+        for (size_t e = 0; e < chunk; ++e) {
+          const float gg = gsh[e] * gs;
+          M[size_t(r)][e] = b1 * M[size_t(r)][e] + omb1 * gg;
+          V[size_t(r)][e] = b2 * V[size_t(r)][e] + omb2 * (gg * gg);
+          P[size_t(r)][e] = P[size_t(r)][e] - ss * (M[size_t(r)][e] / (std::sqrt(V[size_t(r)][e]) / bc2 + eps));
+        }
+      }
+      const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      best = std::min(best, sec);
+    }
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
+  return best;
+}
 
 // State-machine probe (test_sync_schedule.cpp:117-132): runs `ops`, a string
 // of 'm' (micro-step) / 'b' (boundary); returns per-op status in `codes`.

@@ -1,0 +1,584 @@
+// Collective planners: turn the reference's collective calls into descriptor
+// tables for the sm_100a pull engines (kernels.cu) and enqueue them.
+//
+//   all_gather              collectives.cpp:103-134  -> one k_copy launch
+//   reduce_scatter          collectives.cpp:136-183  -> one k_reduce launch
+//   all_reduce              collectives.cpp:185-190  -> k_reduce (in place) + k_copy
+//   hierarchical_all_gather collectives.cpp:192-291  -> two k_copy launches
+//   batched_*               collectives.cpp:293-321  -> one launch for the whole batch
+//
+// Traffic is recorded with the reference's own per-message accounting
+// (record_traffic calls at collectives.cpp:120, :162 and inside the stages), so
+// mics_traffic_get() equals VirtualRankEngine::traffic() for the same calls.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+
+namespace mics {
+
+void CopyPlan::add(const void* src, const std::vector<void*>& dsts, uint64_t bytes) {
+  if (bytes == 0 || dsts.empty()) return;
+  for (size_t b = 0; b < dsts.size(); b += kMaxDst) {
+    CopySeg s;
+    std::memset(&s, 0, sizeof(s));
+    s.src = static_cast<const uint8_t*>(src);
+    s.bytes = bytes;
+    s.ndst = uint32_t(std::min<size_t>(kMaxDst, dsts.size() - b));
+    for (uint32_t d = 0; d < s.ndst; ++d) s.dst[d] = static_cast<uint8_t*>(dsts[b + d]);
+    s.tile0 = tiles;
+    tiles += uint32_t(ceil_div(bytes, kCopyTile));
+    segs.push_back(s);
+  }
+}
+
+void RedPlan::add(const std::vector<const void*>& src, void* dst, uint64_t elems, uint64_t valid) {
+  if (elems == 0) return;
+  RedJob j;
+  std::memset(&j, 0, sizeof(j));
+  j.dst = static_cast<uint8_t*>(dst);
+  j.elems = elems;
+  j.valid = std::min(valid, elems);
+  j.p = uint32_t(src.size());
+  j.tile0 = tiles;
+  uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+  for (const void* s : src) a |= reinterpret_cast<uintptr_t>(s);
+  j.aligned = (a & 15) == 0;
+  tiles += uint32_t(ceil_div(elems, tile_elems));
+  jobs.push_back(j);
+  srcs.push_back(src);
+}
+
+void AdamPlan::add(const std::vector<const void*>& src, float* param, float* m, float* v, uint16_t* pbf16, float* gout,
+                   uint64_t elems, uint64_t sub) {
+  if (elems == 0) return;
+  AdamJob j;
+  std::memset(&j, 0, sizeof(j));
+  j.param = param;
+  j.m = m;
+  j.v = v;
+  j.pbf16 = pbf16;
+  j.gout = gout;
+  j.elems = elems;
+  j.sub = sub;
+  j.rr = uint32_t(src.size());
+  j.tile0 = tiles;
+  tiles += uint32_t(ceil_div(elems, kAdamTile));
+  jobs.push_back(j);
+  srcs.push_back(src);
+}
+
+void Launch::release() {
+  if (d_desc) cudaFree(d_desc);
+  d_desc = nullptr;
+}
+
+namespace {
+void* table_memory(mics_ctx* ctx, uint64_t bytes, bool persistent) {
+  if (!persistent) return ctx->ring_reserve(bytes);
+  void* d = nullptr;
+  MICS_CUDA(cudaMalloc(&d, bytes ? bytes : 16));
+  return d;
+}
+void table_upload(mics_ctx* ctx, void* d, const void* h, uint64_t bytes, bool persistent) {
+  if (persistent)
+    MICS_CUDA(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice));
+  else
+    ctx->ring_upload(d, h, bytes);
+}
+
+// jobs followed by their source-pointer arrays, pointers patched to device addresses
+template <typename Job>
+void* upload_jobs(mics_ctx* ctx, std::vector<Job> jobs, const std::vector<std::vector<const void*>>& srcs,
+                  bool persistent) {
+  uint64_t nptr = 0;
+  for (const auto& s : srcs) nptr += s.size();
+  const uint64_t jbytes = round_up(sizeof(Job) * jobs.size(), 16);
+  const uint64_t bytes = jbytes + nptr * sizeof(void*);
+  char* d = static_cast<char*>(table_memory(ctx, bytes, persistent));
+  std::vector<char> blob(bytes);
+  const void** ptrs = reinterpret_cast<const void**>(blob.data() + jbytes);
+  uint64_t k = 0;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    using P = decltype(jobs[i].srcs);
+    jobs[i].srcs = reinterpret_cast<P>(d + jbytes + k * sizeof(void*));
+    for (const void* s : srcs[i]) ptrs[k++] = s;
+  }
+  std::memcpy(blob.data(), jobs.data(), sizeof(Job) * jobs.size());
+  table_upload(ctx, d, blob.data(), bytes, persistent);
+  return d;
+}
+}  // namespace
+
+Launch make_copy_launch(mics_ctx* ctx, const CopyPlan& plan, const BarrierArg& bar, bool persistent) {
+  Launch l;
+  l.kind = Launch::COPY;
+  l.ndesc = int(plan.segs.size());
+  l.ntiles = plan.tiles;
+  l.grid = ctx->grid_for(plan.tiles);
+  l.bar = bar;
+  if (l.ndesc) {
+    const uint64_t bytes = sizeof(CopySeg) * plan.segs.size();
+    l.d_desc = table_memory(ctx, bytes, persistent);
+    table_upload(ctx, l.d_desc, plan.segs.data(), bytes, persistent);
+  }
+  return l;
+}
+
+Launch make_reduce_launch(mics_ctx* ctx, const RedPlan& plan, mics_dtype in_t, mics_dtype acc_t, double scale,
+                          int mode, const BarrierArg& bar, bool persistent) {
+  Launch l;
+  l.kind = Launch::REDUCE;
+  l.ndesc = int(plan.jobs.size());
+  l.ntiles = plan.tiles;
+  l.grid = ctx->grid_for(plan.tiles);
+  l.in_t = in_t;
+  l.acc_t = acc_t;
+  l.scale = scale;
+  l.mode = mode;
+  l.bar = bar;
+  if (l.ndesc) l.d_desc = upload_jobs(ctx, plan.jobs, plan.srcs, persistent);
+  return l;
+}
+
+Launch make_adam_launch(mics_ctx* ctx, const AdamPlan& plan, const AdamScalars& sc, const BarrierArg& bar,
+                        bool persistent) {
+  Launch l;
+  l.kind = Launch::ADAM;
+  l.ndesc = int(plan.jobs.size());
+  l.ntiles = plan.tiles;
+  l.grid = ctx->grid_for(plan.tiles);
+  l.adam = sc;
+  l.bar = bar;
+  if (l.ndesc) l.d_desc = upload_jobs(ctx, plan.jobs, plan.srcs, persistent);
+  return l;
+}
+
+void enqueue(mics_ctx* ctx, const Launch& l) {
+  // A launch without local work still runs (one CTA) when it carries a barrier:
+  // the peers count on this process's signals.
+  if (l.ndesc == 0 && l.bar.mask == 0) return;
+  switch (l.kind) {
+    case Launch::COPY:
+      launch_copy(ctx->stream, static_cast<const CopySeg*>(l.d_desc), l.ndesc, l.ntiles, l.grid, l.bar);
+      break;
+    case Launch::REDUCE:
+      launch_reduce(ctx->stream, l.in_t, l.acc_t, static_cast<const RedJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid,
+                    l.scale, l.mode, l.bar);
+      break;
+    case Launch::ADAM:
+      launch_adam(ctx->stream, static_cast<const AdamJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid, l.adam, l.bar);
+      break;
+    case Launch::BARRIER:
+      launch_barrier(ctx->stream, l.bar);
+      break;
+  }
+  ctx->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// collectives on device pointers
+namespace {
+
+void check_ptrs(const void* const* a, int count, const mics_ctx* ctx, const int* ranks, bool only_local,
+                const char* what) {
+  if (count > 0 && !a) raise(MICS_OUT_OF_RANGE, std::string(what) + ": null pointer array");
+  for (int i = 0; i < count; ++i)
+    if (!a[i] && (!only_local || ctx->local(ranks[i])))
+      raise(MICS_OUT_OF_RANGE, std::string(what) + ": null buffer at position " + std::to_string(i));
+}
+
+void check_rs_types(mics_dtype in_t, mics_dtype acc_t) {
+  const bool ok = (in_t == acc_t && in_t != MICS_BF16) || (in_t == MICS_BF16 && acc_t == MICS_F32);
+  if (!ok) raise(MICS_TYPE_MISMATCH, "reduce: accumulate type must equal the input type (or f32 for bf16 input)");
+}
+
+void plan_all_gather(mics_ctx* ctx, CopyPlan& plan, const int* ranks, int p, const void* const* shard, uint64_t chunk,
+                     void* const* out) {
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j)
+      if (j != i) ctx->record(ranks[i], ranks[j], chunk);  // collectives.cpp:116-123
+  std::vector<int> loc;
+  for (int j = 0; j < p; ++j)
+    if (ctx->local(ranks[j])) loc.push_back(j);
+  if (loc.empty()) return;
+  for (int i = 0; i < p; ++i) {  // one read of chunk i feeds every local destination
+    std::vector<void*> dsts;
+    for (int j : loc) dsts.push_back(static_cast<char*>(out[j]) + uint64_t(i) * chunk);
+    plan.add(shard[i], dsts, chunk);
+  }
+}
+
+void plan_reduce_scatter(mics_ctx* ctx, RedPlan& plan, const int* ranks, int p, const void* const* in,
+                         uint64_t in_elems, uint64_t valid, mics_dtype in_t, void* const* out) {
+  const uint64_t chunk = in_elems / uint64_t(p);
+  const uint64_t szi = dtype_size(in_t);
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j)
+      if (j != i) ctx->record(ranks[i], ranks[j], chunk * szi);  // collectives.cpp:157-165
+  for (int j = 0; j < p; ++j) {
+    if (!ctx->local(ranks[j])) continue;
+    std::vector<const void*> srcs(static_cast<size_t>(p));
+    for (int i = 0; i < p; ++i) srcs[size_t(i)] = static_cast<const char*>(in[i]) + uint64_t(j) * chunk * szi;
+    const uint64_t first = uint64_t(j) * chunk;
+    plan.add(srcs, out[j], chunk, valid > first ? valid - first : 0);
+  }
+}
+
+}  // namespace
+
+void all_gather(mics_ctx* ctx, const int* ranks, int p, const void* const* shard, uint64_t chunk, void* const* out) {
+  check_group(ctx, ranks, p);
+  check_ptrs(shard, p, ctx, ranks, false, "all_gather input");
+  check_ptrs(const_cast<const void* const*>(out), p, ctx, ranks, true, "all_gather output");
+  CopyPlan plan;
+  plan_all_gather(ctx, plan, ranks, p, shard, chunk, out);
+  enqueue(ctx, make_copy_launch(ctx, plan, ctx->barrier(ctx->peer_mask(ranks, p), 1, 1), false));
+}
+
+void reduce_scatter(mics_ctx* ctx, const int* ranks, int p, const void* const* in, uint64_t in_elems,
+                    uint64_t valid, mics_dtype in_t, mics_dtype acc_t, double scale, int mode, void* const* out) {
+  check_group(ctx, ranks, p);
+  check_rs_types(in_t, acc_t);
+  if (p == 0) return;
+  if (in_elems % uint64_t(p))
+    raise(MICS_TYPE_MISMATCH, "reduce_scatter: " + std::to_string(in_elems) + " elements are not divisible into " +
+                                  std::to_string(p) + " chunks");  // collectives.cpp:148-153
+  if (in_t == MICS_I64 && scale != 1.0) raise(MICS_TYPE_MISMATCH, "reduce_scatter: scale needs a float type");
+  check_ptrs(in, p, ctx, ranks, false, "reduce_scatter input");
+  check_ptrs(const_cast<const void* const*>(out), p, ctx, ranks, true, "reduce_scatter output");
+  RedPlan plan(in_t);
+  plan_reduce_scatter(ctx, plan, ranks, p, in, in_elems, valid, in_t, out);
+  enqueue(ctx, make_reduce_launch(ctx, plan, in_t, acc_t, scale, mode,
+                                  ctx->barrier(ctx->peer_mask(ranks, p), 1, 1), false));
+}
+
+void all_reduce(mics_ctx* ctx, const int* ranks, int p, void* const* buf, uint64_t elems, mics_dtype dt) {
+  check_group(ctx, ranks, p);
+  check_rs_types(dt, dt);
+  if (p == 0) return;
+  if (elems % uint64_t(p))
+    raise(MICS_TYPE_MISMATCH, "all_reduce: " + std::to_string(elems) + " elements are not divisible into " +
+                                  std::to_string(p) + " chunks");
+  check_ptrs(const_cast<const void* const*>(buf), p, ctx, ranks, false, "all_reduce buffer");
+  const uint64_t chunk = elems / uint64_t(p), sz = dtype_size(dt), cb = chunk * sz;
+  // reduce-scatter in place: position j folds slice j of every buffer into its own slice j
+  RedPlan rs(dt);
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j)
+      if (j != i) ctx->record(ranks[i], ranks[j], cb);
+  for (int j = 0; j < p; ++j) {
+    if (!ctx->local(ranks[j])) continue;
+    std::vector<const void*> srcs(static_cast<size_t>(p));
+    for (int i = 0; i < p; ++i) srcs[size_t(i)] = static_cast<const char*>(buf[i]) + uint64_t(j) * cb;
+    rs.add(srcs, static_cast<char*>(buf[j]) + uint64_t(j) * cb, chunk, chunk);
+  }
+  const uint64_t mask = ctx->peer_mask(ranks, p);
+  enqueue(ctx, make_reduce_launch(ctx, rs, dt, dt, 1.0, MICS_RS_STORE, ctx->barrier(mask, 1, 1), false));
+  // all-gather of the reduced slices
+  CopyPlan ag;
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j)
+      if (j != i) ctx->record(ranks[i], ranks[j], cb);
+  for (int i = 0; i < p; ++i) {
+    std::vector<void*> dsts;
+    for (int j = 0; j < p; ++j)
+      if (j != i && ctx->local(ranks[j])) dsts.push_back(static_cast<char*>(buf[j]) + uint64_t(i) * cb);
+    ag.add(static_cast<const char*>(buf[i]) + uint64_t(i) * cb, dsts, cb);
+  }
+  enqueue(ctx, make_copy_launch(ctx, ag, ctx->barrier(mask, 0, 1), false));
+}
+
+// Hierarchical all-gather.  For partition group g (base = g*p) with q = p/k
+// virtual nodes of k ranks: phase 1 is stage 1 (k channel all-gathers among the
+// q ranks sharing a local index) with stage 2's rearrangement folded into the
+// store address: C_{m'k+j} lands directly at its final position.  Phase 2 is
+// stage 3: every rank pulls from each node peer j' the positions t*k+j'.
+// corrupt_stage2 keeps the raw stage-1 layout [C_j, C_{k+j}, ...] at offset
+// j*q*chunk and gathers those buffers per node (collectives.cpp:243-257).
+// `n` is the cluster's rank count: ctx->n, or (single process) any n <= ctx->n.
+void hier_all_gather(mics_ctx* ctx, int n, int p, int k, const void* const* shard, uint64_t chunk,
+                     void* const* out, int corrupt) {
+  if (n < 1 || n > ctx->n || (ctx->world > 1 && n != ctx->n))
+    raise(MICS_SHAPE_ERROR, "cluster has " + std::to_string(n) + " ranks but the context has " +
+                                std::to_string(ctx->n));  // collectives.cpp:200-202
+  if (p < 1 || p > n)
+    raise(MICS_OUT_OF_RANGE, "partition size p=" + std::to_string(p) + " must satisfy 1 <= p <= n=" +
+                                 std::to_string(n));
+  if (n % p) raise(MICS_NON_DIVISIBLE, "partition size p=" + std::to_string(p) + " does not divide n=" +
+                                           std::to_string(n));
+  if (k < 1 || n % k) raise(MICS_SHAPE_ERROR, "cluster of k=" + std::to_string(k) + " ranks per node does not tile n=" +
+                                                  std::to_string(n));
+  if (!mics_partition_shape_ok(p, k))
+    raise(MICS_SHAPE_ERROR, "partition size p=" + std::to_string(p) + " is not node-aligned for k=" +
+                                std::to_string(k));  // collectives.cpp:208-210
+  std::vector<int> all(static_cast<size_t>(n));
+  for (int r = 0; r < n; ++r) all[size_t(r)] = r;
+  check_ptrs(shard, n, ctx, all.data(), false, "hierarchical_all_gather input");
+  // phase 2 pulls from node peers' outputs: every entry must be valid (peer-mapped)
+  check_ptrs(const_cast<const void* const*>(out), n, ctx, all.data(), p <= k, "hierarchical_all_gather output");
+
+  auto O = [&](int r, uint64_t pos) { return static_cast<char*>(out[r]) + pos * chunk; };
+  uint64_t mask = 0;
+  if (p <= k) {  // single-node partition group: plain all-gather (collectives.cpp:218-225)
+    CopyPlan plan;
+    for (int g = 0; g < n / p; ++g) {
+      plan_all_gather(ctx, plan, all.data() + g * p, p, shard + g * p, chunk, out + g * p);
+      mask |= ctx->peer_mask(all.data() + g * p, p);
+    }
+    enqueue(ctx, make_copy_launch(ctx, plan, ctx->barrier(mask, 1, 1), false));
+    return;
+  }
+  const int q = p / k;
+  CopyPlan ph1, ph2;
+  for (int g = 0; g < n / p; ++g) {
+    const int base = g * p;
+    mask |= ctx->peer_mask(all.data() + base, p);
+    // traffic of the reference's stages (stage 1 :233-241, stage 3 :267-288 / corrupt :246-255)
+    for (int j = 0; j < k; ++j)
+      for (int m = 0; m < q; ++m)
+        for (int m2 = 0; m2 < q; ++m2)
+          if (m2 != m) ctx->record(base + m * k + j, base + m2 * k + j, chunk);
+    for (int m = 0; m < q; ++m)
+      for (int j = 0; j < k; ++j)
+        for (int j2 = 0; j2 < k; ++j2)
+          if (j2 != j) ctx->record(base + m * k + j, base + m * k + j2, uint64_t(q) * chunk);
+    for (int m = 0; m < q; ++m) {
+      for (int j = 0; j < k; ++j) {
+        const int r = base + m * k + j;
+        if (!ctx->local(r)) continue;
+        for (int m2 = 0; m2 < q; ++m2) {  // phase 1: channel j
+          const uint64_t pos = corrupt ? uint64_t(j) * q + m2 : uint64_t(m2) * k + j;
+          ph1.add(shard[base + m2 * k + j], {O(r, pos)}, chunk);
+        }
+        for (int j2 = 0; j2 < k; ++j2) {  // phase 2: node peers
+          if (j2 == j) continue;
+          const int src = base + m * k + j2;
+          for (int t = 0; t < q; ++t) {
+            const uint64_t pos = corrupt ? uint64_t(j2) * q + t : uint64_t(t) * k + j2;
+            ph2.add(O(src, pos), {O(r, pos)}, chunk);
+          }
+        }
+      }
+    }
+  }
+  enqueue(ctx, make_copy_launch(ctx, ph1, ctx->barrier(mask, 1, 1), false));
+  enqueue(ctx, make_copy_launch(ctx, ph2, ctx->barrier(mask, 0, 1), false));
+}
+
+void batched_all_gather(mics_ctx* ctx, const mics_ag_desc* d, int count) {
+  if (count < 0 || (count > 0 && !d)) raise(MICS_OUT_OF_RANGE, "batched_all_gather: bad descriptor list");
+  CopyPlan plan;
+  uint64_t mask = 0;
+  for (int b = 0; b < count; ++b) {
+    check_group(ctx, d[b].ranks, d[b].p);
+    check_ptrs(d[b].d_shard, d[b].p, ctx, d[b].ranks, false, "batched_all_gather input");
+    check_ptrs(const_cast<const void* const*>(d[b].d_out), d[b].p, ctx, d[b].ranks, true, "batched_all_gather output");
+    plan_all_gather(ctx, plan, d[b].ranks, d[b].p, d[b].d_shard, d[b].chunk_bytes, d[b].d_out);
+    mask |= ctx->peer_mask(d[b].ranks, d[b].p);
+  }
+  enqueue(ctx, make_copy_launch(ctx, plan, ctx->barrier(mask, 1, 1), false));
+}
+
+void batched_reduce_scatter(mics_ctx* ctx, const mics_rs_desc* d, int count, mics_dtype in_t, mics_dtype acc_t,
+                            double scale, int mode) {
+  if (count < 0 || (count > 0 && !d)) raise(MICS_OUT_OF_RANGE, "batched_reduce_scatter: bad descriptor list");
+  check_rs_types(in_t, acc_t);
+  RedPlan plan(in_t);
+  uint64_t mask = 0;
+  for (int b = 0; b < count; ++b) {
+    check_group(ctx, d[b].ranks, d[b].p);
+    if (d[b].p == 0) continue;
+    if (d[b].in_elems % uint64_t(d[b].p))
+      raise(MICS_TYPE_MISMATCH, "batched_reduce_scatter: descriptor " + std::to_string(b) +
+                                    " is not divisible into whole chunks");
+    check_ptrs(d[b].d_in, d[b].p, ctx, d[b].ranks, false, "batched_reduce_scatter input");
+    check_ptrs(const_cast<const void* const*>(d[b].d_out), d[b].p, ctx, d[b].ranks, true,
+               "batched_reduce_scatter output");
+    plan_reduce_scatter(ctx, plan, d[b].ranks, d[b].p, d[b].d_in, d[b].in_elems, d[b].valid_elems, in_t, d[b].d_out);
+    mask |= ctx->peer_mask(d[b].ranks, d[b].p);
+  }
+  enqueue(ctx, make_reduce_launch(ctx, plan, in_t, acc_t, scale, mode, ctx->barrier(mask, 1, 1), false));
+}
+
+// ---------------------------------------------------------------------------
+// host-buffer drop-ins (world == 1): stage through the arena, run, copy back.
+namespace {
+struct Scratch {
+  mics_ctx* ctx;
+  uint64_t mark;
+  explicit Scratch(mics_ctx* c) : ctx(c), mark(c->used) {
+    if (c->world != 1) raise(MICS_CONFIG_ERROR, "host-buffer API needs a single-process context (world == 1)");
+  }
+  ~Scratch() { ctx->used = mark; }
+  char* alloc(uint64_t bytes) { return ctx->base + ctx->local_alloc(bytes); }
+};
+constexpr uint64_t kStage = 256;  // keep every staged buffer 16-byte aligned
+}  // namespace
+
+void host_all_gather(mics_ctx* ctx, const int* ranks, int p, const void* const* shards, uint64_t chunk,
+                     void* const* out) {
+  Scratch s(ctx);
+  check_group(ctx, ranks, p);
+  const uint64_t cs = round_up(chunk, kStage), os = round_up(uint64_t(p) * chunk, kStage);
+  char* in = s.alloc(cs * uint64_t(p));
+  char* ob = s.alloc(os * uint64_t(p));
+  std::vector<const void*> ip(static_cast<size_t>(p));
+  std::vector<void*> op(static_cast<size_t>(p));
+  for (int i = 0; i < p; ++i) {
+    ip[size_t(i)] = in + uint64_t(i) * cs;
+    op[size_t(i)] = ob + uint64_t(i) * os;
+    if (chunk) MICS_CUDA(cudaMemcpyAsync(in + uint64_t(i) * cs, shards[i], chunk, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  all_gather(ctx, ranks, p, ip.data(), chunk, op.data());
+  for (int j = 0; j < p; ++j)
+    if (chunk) MICS_CUDA(cudaMemcpyAsync(out[j], op[size_t(j)], uint64_t(p) * chunk, cudaMemcpyDeviceToHost, ctx->stream));
+  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void host_reduce_scatter(mics_ctx* ctx, const int* ranks, int p, const void* const* bufs, uint64_t bytes,
+                         mics_dtype dt, void* const* out) {
+  Scratch s(ctx);
+  check_group(ctx, ranks, p);
+  if (dt == MICS_BF16) raise(MICS_TYPE_MISMATCH, "reduce_scatter: bf16 is not a reduction type");
+  if (p == 0) return;
+  const uint64_t sz = dtype_size(dt);
+  if (bytes % (uint64_t(p) * sz))
+    raise(MICS_TYPE_MISMATCH, "reduce_scatter: buffer of " + std::to_string(bytes) + " bytes is not divisible into " +
+                                  std::to_string(p) + " chunks of whole " + std::to_string(sz) + "-byte elements");
+  const uint64_t bs = round_up(bytes, kStage), cb = bytes / uint64_t(p), cs = round_up(cb, kStage);
+  char* in = s.alloc(bs * uint64_t(p));
+  char* ob = s.alloc(cs * uint64_t(p));
+  std::vector<const void*> ip(static_cast<size_t>(p));
+  std::vector<void*> op(static_cast<size_t>(p));
+  for (int i = 0; i < p; ++i) {
+    ip[size_t(i)] = in + uint64_t(i) * bs;
+    op[size_t(i)] = ob + uint64_t(i) * cs;
+    if (bytes) MICS_CUDA(cudaMemcpyAsync(in + uint64_t(i) * bs, bufs[i], bytes, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  reduce_scatter(ctx, ranks, p, ip.data(), bytes / sz, bytes / sz, dt, dt, 1.0, MICS_RS_STORE, op.data());
+  for (int j = 0; j < p; ++j)
+    if (cb) MICS_CUDA(cudaMemcpyAsync(out[j], op[size_t(j)], cb, cudaMemcpyDeviceToHost, ctx->stream));
+  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void host_all_reduce(mics_ctx* ctx, const int* ranks, int p, const void* const* bufs, uint64_t bytes, mics_dtype dt,
+                     void* const* out) {
+  Scratch s(ctx);
+  check_group(ctx, ranks, p);
+  if (dt == MICS_BF16) raise(MICS_TYPE_MISMATCH, "all_reduce: bf16 is not a reduction type");
+  if (p == 0) return;
+  const uint64_t sz = dtype_size(dt);
+  if (bytes % (uint64_t(p) * sz))
+    raise(MICS_TYPE_MISMATCH, "all_reduce: buffer of " + std::to_string(bytes) + " bytes is not divisible into " +
+                                  std::to_string(p) + " chunks of whole " + std::to_string(sz) + "-byte elements");
+  const uint64_t bs = round_up(bytes, kStage);
+  char* b = s.alloc(bs * uint64_t(p));
+  std::vector<void*> bp(static_cast<size_t>(p));
+  for (int i = 0; i < p; ++i) {
+    bp[size_t(i)] = b + uint64_t(i) * bs;
+    if (bytes) MICS_CUDA(cudaMemcpyAsync(bp[size_t(i)], bufs[i], bytes, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  all_reduce(ctx, ranks, p, bp.data(), bytes / sz, dt);
+  for (int j = 0; j < p; ++j)
+    if (bytes) MICS_CUDA(cudaMemcpyAsync(out[j], bp[size_t(j)], bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void host_hier_all_gather(mics_ctx* ctx, int n, int p, int k, const void* const* shards, uint64_t chunk,
+                          void* const* out, int corrupt) {
+  Scratch s(ctx);
+  if (n < 1 || n > ctx->n)
+    raise(MICS_SHAPE_ERROR, "cluster has " + std::to_string(n) + " ranks but the context has " +
+                                std::to_string(ctx->n));  // collectives.cpp:200-202
+  const uint64_t cs = round_up(chunk, kStage), os = round_up(uint64_t(p) * chunk, kStage);
+  char* in = s.alloc(cs * uint64_t(n));
+  char* ob = s.alloc(os * uint64_t(n));
+  std::vector<const void*> ip(static_cast<size_t>(n));
+  std::vector<void*> op(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    ip[size_t(i)] = in + uint64_t(i) * cs;
+    op[size_t(i)] = ob + uint64_t(i) * os;
+    if (chunk) MICS_CUDA(cudaMemcpyAsync(in + uint64_t(i) * cs, shards[i], chunk, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  hier_all_gather(ctx, n, p, k, ip.data(), chunk, op.data(), corrupt);
+  for (int j = 0; j < n; ++j)
+    if (chunk) MICS_CUDA(cudaMemcpyAsync(out[j], op[size_t(j)], uint64_t(p) * chunk, cudaMemcpyDeviceToHost, ctx->stream));
+  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void host_batched_all_gather(mics_ctx* ctx, int count, const int* sizes, const int* ranks, const uint64_t* chunks,
+                             const void* const* shards, void* const* out) {
+  Scratch s(ctx);
+  std::vector<mics_ag_desc> d(static_cast<size_t>(std::max(count, 0)));
+  std::vector<std::vector<const void*>> ip(d.size());
+  std::vector<std::vector<void*>> op(d.size());
+  uint64_t ro = 0;
+  for (int b = 0; b < count; ++b) {
+    const int p = sizes[b];
+    const uint64_t c = chunks[b], cs = round_up(c, kStage), os = round_up(uint64_t(p) * c, kStage);
+    char* in = s.alloc(cs * uint64_t(p));
+    char* ob = s.alloc(os * uint64_t(p));
+    for (int i = 0; i < p; ++i) {
+      ip[size_t(b)].push_back(in + uint64_t(i) * cs);
+      op[size_t(b)].push_back(ob + uint64_t(i) * os);
+      if (c) MICS_CUDA(cudaMemcpyAsync(in + uint64_t(i) * cs, shards[ro + uint64_t(i)], c, cudaMemcpyHostToDevice,
+                                       ctx->stream));
+    }
+    d[size_t(b)] = mics_ag_desc{ranks + ro, p, ip[size_t(b)].data(), c, op[size_t(b)].data()};
+    ro += uint64_t(p);
+  }
+  batched_all_gather(ctx, d.data(), count);
+  ro = 0;
+  for (int b = 0; b < count; ++b) {
+    for (int j = 0; j < sizes[b]; ++j)
+      if (chunks[b])
+        MICS_CUDA(cudaMemcpyAsync(out[ro + uint64_t(j)], op[size_t(b)][size_t(j)], uint64_t(sizes[b]) * chunks[b],
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+    ro += uint64_t(sizes[b]);
+  }
+  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void host_batched_reduce_scatter(mics_ctx* ctx, int count, const int* sizes, const int* ranks, const uint64_t* bytes,
+                                 const void* const* bufs, mics_dtype dt, void* const* out) {
+  Scratch s(ctx);
+  if (dt == MICS_BF16) raise(MICS_TYPE_MISMATCH, "reduce_scatter: bf16 is not a reduction type");
+  const uint64_t sz = dtype_size(dt);
+  std::vector<mics_rs_desc> d(static_cast<size_t>(std::max(count, 0)));
+  std::vector<std::vector<const void*>> ip(d.size());
+  std::vector<std::vector<void*>> op(d.size());
+  uint64_t ro = 0;
+  for (int b = 0; b < count; ++b) {
+    const int p = sizes[b];
+    if (p > 0 && bytes[b] % (uint64_t(p) * sz))
+      raise(MICS_TYPE_MISMATCH, "batched_reduce_scatter: buffer set " + std::to_string(b) +
+                                    " is not divisible into whole chunks");
+    const uint64_t bs = round_up(bytes[b], kStage), cb = p ? bytes[b] / uint64_t(p) : 0, cs = round_up(cb, kStage);
+    char* in = s.alloc(bs * uint64_t(p));
+    char* ob = s.alloc(cs * uint64_t(p));
+    for (int i = 0; i < p; ++i) {
+      ip[size_t(b)].push_back(in + uint64_t(i) * bs);
+      op[size_t(b)].push_back(ob + uint64_t(i) * cs);
+      if (bytes[b]) MICS_CUDA(cudaMemcpyAsync(in + uint64_t(i) * bs, bufs[ro + uint64_t(i)], bytes[b],
+                                              cudaMemcpyHostToDevice, ctx->stream));
+    }
+    d[size_t(b)] = mics_rs_desc{ranks + ro, p, ip[size_t(b)].data(), bytes[b] / sz, bytes[b] / sz, op[size_t(b)].data()};
+    ro += uint64_t(p);
+  }
+  batched_reduce_scatter(ctx, d.data(), count, dt, dt, 1.0, MICS_RS_STORE);
+  ro = 0;
+  for (int b = 0; b < count; ++b) {
+    const uint64_t cb = sizes[b] ? bytes[b] / uint64_t(sizes[b]) : 0;
+    for (int j = 0; j < sizes[b]; ++j)
+      if (cb) MICS_CUDA(cudaMemcpyAsync(out[ro + uint64_t(j)], op[size_t(b)][size_t(j)], cb, cudaMemcpyDeviceToHost,
+                                        ctx->stream));
+    ro += uint64_t(sizes[b]);
+  }
+  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace mics

@@ -1,0 +1,218 @@
+// Internal declarations of libmics (not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "mics.h"
+
+namespace mics {
+
+// --------------------------------------------------------------------------
+// errors: C++ exceptions inside the library, mapped to mics_status at the
+// C-ABI edge (capi.cpp) with "<Errc>: detail" messages like sdpsim::raise.
+struct Error {
+  mics_status code;
+  std::string what;
+};
+[[noreturn]] void raise(mics_status code, const std::string& what);
+void cuda_check(cudaError_t e, const char* expr, const char* file, int line);
+#define MICS_CUDA(x) ::mics::cuda_check((x), #x, __FILE__, __LINE__)
+
+inline size_t dtype_size(mics_dtype t) {
+  switch (t) {
+    case MICS_I64: return 8;
+    case MICS_F32: return 4;
+    case MICS_F64: return 8;
+    case MICS_BF16: return 2;
+  }
+  return 0;
+}
+inline uint64_t ceil_div(uint64_t a, uint64_t b) { return b ? (a + b - 1) / b : 0; }
+inline uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }
+
+// --------------------------------------------------------------------------
+// device descriptors (shared by host planners and kernels)
+constexpr int kMaxDst = 4;       // destinations written from one source read
+constexpr int kThreads = 256;    // threads per CTA for every data kernel
+constexpr int kCopyUnroll = 4;   // 16 B vectors in flight per thread per tile
+constexpr uint32_t kCopyTile = kThreads * kCopyUnroll * 16;  // 16 KiB
+constexpr int kRedUnroll = 2;    // vectors per thread per tile (per source)
+constexpr int kAdamUnroll = 2;
+
+struct CopySeg {              // 64 B
+  const uint8_t* src;
+  uint8_t* dst[kMaxDst];
+  uint64_t bytes;
+  uint32_t ndst;
+  uint32_t tile0;             // first global tile index of this segment
+};
+
+struct RedJob {               // one output chunk (one destination rank, one segment)
+  const uint8_t* const* srcs; // p source pointers, already offset to this chunk
+  uint8_t* dst;
+  uint64_t elems;             // chunk elements
+  uint64_t valid;             // elements [valid, elems) read as zero
+  uint32_t p;
+  uint32_t tile0;
+  uint32_t aligned;           // all srcs and dst 16-byte aligned
+  uint32_t pad_;
+};
+
+struct AdamJob {              // boundary: all-gather phase fused with Adam, one local rank
+  const float* const* srcs;   // rr shard base pointers (replication positions)
+  float* param;
+  float* m;
+  float* v;
+  uint16_t* pbf16;            // nullable
+  float* gout;                // nullable: write the reduced gradient back
+  uint64_t elems;
+  uint64_t sub;               // slice owned by each replication position (multiple of 4)
+  uint32_t rr;
+  uint32_t tile0;
+};
+
+struct AdamScalars {
+  float b1, omb1, b2, omb2, eps, wd, step_size, bc2_sqrt, grad_scale;
+};
+
+// Flag barrier between processes: remote_flag[w] is the slot on process w's
+// arena reserved for this process; local_flag[w] is the slot process w writes
+// on ours.  Values are monotone barrier counts per process pair.
+struct PeerTab {
+  uint64_t* remote_flag[MICS_MAX_WORLD];
+  uint64_t* local_flag[MICS_MAX_WORLD];
+};
+
+struct BarrierArg {
+  const PeerTab* tab;
+  uint64_t* nbar;             // [MICS_MAX_WORLD] barriers completed with each peer (device, local)
+  unsigned* tickets;          // [2] CTA arrival tickets (entry, exit)
+  uint64_t mask;              // peers taking part (bit w = process w), never includes self
+  int entry;                  // signal + wait before any data access
+  int exit;                   // last CTA signals + waits after all data access
+};
+
+// --------------------------------------------------------------------------
+// kernel launchers (kernels.cu)
+void launch_copy(cudaStream_t s, const CopySeg* segs, int nseg, uint32_t ntiles, int grid, const BarrierArg& bar);
+void launch_reduce(cudaStream_t s, mics_dtype in_t, mics_dtype acc_t, const RedJob* jobs, int njobs, uint32_t ntiles,
+                   int grid, double scale, int mode, const BarrierArg& bar);
+uint32_t reduce_tile_elems(mics_dtype in_t);
+void launch_adam(cudaStream_t s, const AdamJob* jobs, int njobs, uint32_t ntiles, int grid, const AdamScalars& sc,
+                 const BarrierArg& bar);
+constexpr uint32_t kAdamTile = kThreads * kAdamUnroll * 4;
+void launch_generate(cudaStream_t s, void* out, mics_dtype dtype, uint64_t seed, int rank, int step, int layer,
+                     uint64_t start, uint64_t count, int grid);
+void launch_cast_bf16(cudaStream_t s, const float* in, uint16_t* out, uint64_t count, int grid);
+void launch_barrier(cudaStream_t s, const BarrierArg& bar);
+
+AdamScalars make_adam_scalars(double lr, double b1, double b2, double eps, double wd, int step, double grad_scale);
+
+}  // namespace mics
+
+// --------------------------------------------------------------------------
+// the context (VirtualRankEngine's B200 counterpart)
+struct mics_ctx {
+  int n = 0, world = 1, wrank = 0, per = 0, device = 0, nsm = 148;
+  int blocks_per_sm = 4;
+  cudaStream_t stream = nullptr;
+  char* base = nullptr;           // local arena (IPC-exportable)
+  uint64_t cap = 0, used = 0;
+  char* peer_base[MICS_MAX_WORLD] = {};
+  bool ipc_ready = false;
+  mics::PeerTab* d_tab = nullptr;
+  uint64_t* d_nbar = nullptr;
+  unsigned* d_tickets = nullptr;
+  // descriptor ring for ad-hoc calls
+  char* ring = nullptr;
+  uint64_t ring_cap = 0, ring_head = 0;
+  bool traffic_on = true;
+  std::map<std::pair<int, int>, uint64_t> traffic;
+  uint64_t launches = 0;
+
+  int process_of(int rank) const { return rank / per; }
+  bool local(int rank) const { return process_of(rank) == wrank; }
+  char* rank_ptr(mics_buf b, int rank) const {
+    return peer_base[process_of(rank)] + b.offset + uint64_t(rank % per) * b.stride;
+  }
+  void record(int from, int to, uint64_t bytes) {
+    if (!traffic_on) return;
+    if (world > 1 && !local(to)) return;
+    traffic[{from, to}] += bytes;
+  }
+  int grid_for(uint64_t tiles) const {
+    uint64_t g = uint64_t(nsm) * blocks_per_sm;
+    if (tiles < g) g = tiles;
+    return g ? int(g) : 1;
+  }
+  // device memory for descriptor tables of one ad-hoc launch
+  void* ring_put(const void* host, uint64_t bytes);
+  void* ring_reserve(uint64_t bytes);
+  void ring_upload(void* dev, const void* host, uint64_t bytes);
+  mics::BarrierArg barrier(uint64_t mask, int entry, int exit) const {
+    mics::BarrierArg b;
+    b.tab = d_tab;
+    b.nbar = d_nbar;
+    b.tickets = d_tickets;
+    b.mask = ipc_ready ? mask : 0;
+    b.entry = entry;
+    b.exit = exit;
+    return b;
+  }
+  // processes hosting any of `ranks`, minus self (0 when self hosts none)
+  uint64_t peer_mask(const int* ranks, int count) const;
+  uint64_t local_alloc(uint64_t bytes);  // world == 1 scratch
+};
+
+namespace mics {
+// collectives planners (collectives.cpp), shared with the sync/step drivers
+struct CopyPlan {
+  std::vector<CopySeg> segs;
+  uint32_t tiles = 0;
+  void add(const void* src, const std::vector<void*>& dsts, uint64_t bytes);
+};
+struct RedPlan {
+  std::vector<RedJob> jobs;
+  std::vector<std::vector<const void*>> srcs;  // per job
+  uint32_t tiles = 0;
+  uint32_t tile_elems = 0;
+  explicit RedPlan(mics_dtype in_t) : tile_elems(reduce_tile_elems(in_t)) {}
+  void add(const std::vector<const void*>& src, void* dst, uint64_t elems, uint64_t valid);
+};
+struct AdamPlan {
+  std::vector<AdamJob> jobs;
+  std::vector<std::vector<const void*>> srcs;
+  uint32_t tiles = 0;
+  void add(const std::vector<const void*>& src, float* param, float* m, float* v, uint16_t* pbf16, float* gout,
+           uint64_t elems, uint64_t sub);
+};
+
+// A device-resident, replayable launch (built once, launched many times).
+struct Launch {
+  enum Kind { COPY, REDUCE, ADAM, BARRIER } kind = COPY;
+  void* d_desc = nullptr;  // owned device table (cudaMalloc)
+  int ndesc = 0;
+  uint32_t ntiles = 0;
+  int grid = 1;
+  mics_dtype in_t = MICS_F32, acc_t = MICS_F32;
+  double scale = 1.0;
+  int mode = 0;
+  AdamScalars adam{};
+  BarrierArg bar{};
+  void release();
+};
+Launch make_copy_launch(mics_ctx* ctx, const CopyPlan& plan, const BarrierArg& bar, bool persistent);
+Launch make_reduce_launch(mics_ctx* ctx, const RedPlan& plan, mics_dtype in_t, mics_dtype acc_t, double scale, int mode,
+                          const BarrierArg& bar, bool persistent);
+Launch make_adam_launch(mics_ctx* ctx, const AdamPlan& plan, const AdamScalars& sc, const BarrierArg& bar,
+                        bool persistent);
+void enqueue(mics_ctx* ctx, const Launch& l);
+
+void check_group(const mics_ctx* ctx, const int* ranks, int p);
+}  // namespace mics

@@ -1,0 +1,226 @@
+// Runtime of libmics: context, symmetric arena, CUDA IPC peer mapping, flag
+// barriers, descriptor ring, traffic log.  The B200 counterpart of the
+// reference's VirtualRankEngine (collectives.hpp:42-62, collectives.cpp:25-67):
+// instead of spawning std::threads per call and copying whole buffers into
+// mailbox slots, virtual ranks are (GPU, arena region) pairs and peers pull each
+// other's data over NVLink/NVSwitch from IPC-mapped memory.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+
+namespace mics {
+
+namespace {
+constexpr uint64_t kFlagsBytes = 4096;   // arena head: MICS_MAX_WORLD flag slots (u64), rest reserved
+constexpr uint64_t kAlign = 256;
+constexpr uint64_t kRingBytes = 16ull << 20;
+}  // namespace
+
+[[noreturn]] void raise(mics_status code, const std::string& what) {
+  throw Error{code, std::string(mics_status_name(code)) + ": " + what};
+}
+
+void cuda_check(cudaError_t e, const char* expr, const char* file, int line) {
+  if (e != cudaSuccess)
+    raise(MICS_CUDA_ERROR, std::string(cudaGetErrorString(e)) + " in " + expr + " (" + file + ":" +
+                               std::to_string(line) + ")");
+}
+
+void check_group(const mics_ctx* ctx, const int* ranks, int p) {
+  if (p < 0 || p > MICS_MAX_GROUP) raise(MICS_OUT_OF_RANGE, "group size " + std::to_string(p) + " out of range");
+  if (p > 0 && !ranks) raise(MICS_OUT_OF_RANGE, "null rank list");
+  std::vector<char> seen(size_t(ctx->n), 0);
+  for (int i = 0; i < p; ++i) {
+    if (ranks[i] < 0 || ranks[i] >= ctx->n)
+      raise(MICS_OUT_OF_RANGE, "rank " + std::to_string(ranks[i]) + " outside [0, " + std::to_string(ctx->n) + ")");
+    if (seen[size_t(ranks[i])]++) raise(MICS_SHAPE_ERROR, "collective group has duplicate ranks");  // collectives.cpp:19-23
+  }
+}
+
+AdamScalars make_adam_scalars(double lr, double b1, double b2, double eps, double wd, int step, double grad_scale) {
+  // scalars prepared in double then rounded once (the documented Adam formula, include/mics.h)
+  AdamScalars s;
+  const double bc1 = 1.0 - std::pow(b1, double(step));
+  const double bc2 = 1.0 - std::pow(b2, double(step));
+  s.b1 = float(b1);
+  s.omb1 = float(1.0 - b1);
+  s.b2 = float(b2);
+  s.omb2 = float(1.0 - b2);
+  s.eps = float(eps);
+  s.wd = float(wd);
+  s.step_size = float(lr / bc1);
+  s.bc2_sqrt = float(std::sqrt(bc2));
+  s.grad_scale = float(grad_scale);
+  return s;
+}
+
+}  // namespace mics
+
+using mics::raise;
+
+uint64_t mics_ctx::peer_mask(const int* ranks, int count) const {
+  uint64_t mask = 0;
+  bool mine = false;
+  for (int i = 0; i < count; ++i) {
+    const int w = process_of(ranks[i]);
+    if (w == wrank) mine = true;
+    else mask |= 1ull << w;
+  }
+  return mine ? mask : 0;
+}
+
+uint64_t mics_ctx::local_alloc(uint64_t bytes) {
+  if (world != 1) raise(MICS_CONFIG_ERROR, "host-buffer API needs a single-process context");
+  const uint64_t off = used;
+  const uint64_t sz = mics::round_up(bytes ? bytes : 1, mics::kAlign);
+  if (off + sz > cap)
+    raise(MICS_INFEASIBLE, "arena exhausted: need " + std::to_string(sz) + " bytes, " + std::to_string(cap - off) +
+                               " free (raise arena_bytes)");
+  used += sz;
+  return off;
+}
+
+void* mics_ctx::ring_reserve(uint64_t bytes) {
+  bytes = mics::round_up(bytes ? bytes : 16, mics::kAlign);
+  if (bytes > ring_cap) raise(MICS_OUT_OF_RANGE, "descriptor table larger than the descriptor ring");
+  if (ring_head + bytes > ring_cap) {  // wrap: earlier tables may still be in flight
+    MICS_CUDA(cudaStreamSynchronize(stream));
+    ring_head = 0;
+  }
+  void* d = ring + ring_head;
+  ring_head += bytes;
+  return d;
+}
+
+void mics_ctx::ring_upload(void* dev, const void* host, uint64_t bytes) {
+  // pageable source: the runtime stages it before returning, so `host` may die.
+  MICS_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, stream));
+}
+
+void* mics_ctx::ring_put(const void* host, uint64_t bytes) {
+  void* d = ring_reserve(bytes);
+  ring_upload(d, host, bytes);
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI: context
+namespace mics {
+mics_ctx* create_ctx(const mics_init_args* a) {
+  if (!a) raise(MICS_OUT_OF_RANGE, "null init args");
+  if (a->n_ranks < 1) raise(MICS_OUT_OF_RANGE, "n_ranks must be >= 1");
+  if (a->world < 1 || a->world > MICS_MAX_WORLD) raise(MICS_OUT_OF_RANGE, "world must be in [1, 64]");
+  if (a->world_rank < 0 || a->world_rank >= a->world) raise(MICS_OUT_OF_RANGE, "world_rank out of range");
+  if (a->n_ranks % a->world) raise(MICS_NON_DIVISIBLE, "world must divide n_ranks (node-major rank placement)");
+  auto* c = new mics_ctx();
+  try {
+    c->n = a->n_ranks;
+    c->world = a->world;
+    c->wrank = a->world_rank;
+    c->per = a->n_ranks / a->world;
+    c->device = a->device;
+    MICS_CUDA(cudaSetDevice(c->device));
+    cudaDeviceProp prop;
+    MICS_CUDA(cudaGetDeviceProperties(&prop, c->device));
+    if (prop.major != 10)
+      raise(MICS_CONFIG_ERROR, std::string("libmics is built for sm_100a (B200); device is ") + prop.name);
+    c->nsm = prop.multiProcessorCount;
+    MICS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->cap = (a->arena_bytes ? a->arena_bytes : (1ull << 30)) + kFlagsBytes;
+    c->cap = round_up(c->cap, 2ull << 20);
+    MICS_CUDA(cudaMalloc(&c->base, c->cap));
+    MICS_CUDA(cudaMemset(c->base, 0, kFlagsBytes));
+    c->used = kFlagsBytes;
+    c->peer_base[c->wrank] = c->base;
+    MICS_CUDA(cudaMalloc(&c->d_tab, sizeof(PeerTab)));
+    MICS_CUDA(cudaMemset(c->d_tab, 0, sizeof(PeerTab)));
+    MICS_CUDA(cudaMalloc(&c->d_nbar, sizeof(uint64_t) * MICS_MAX_WORLD));
+    MICS_CUDA(cudaMemset(c->d_nbar, 0, sizeof(uint64_t) * MICS_MAX_WORLD));
+    MICS_CUDA(cudaMalloc(&c->d_tickets, 2 * sizeof(unsigned)));
+    MICS_CUDA(cudaMemset(c->d_tickets, 0, 2 * sizeof(unsigned)));
+    c->ring_cap = kRingBytes;
+    MICS_CUDA(cudaMalloc(&c->ring, c->ring_cap));
+    MICS_CUDA(cudaDeviceSynchronize());
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  return c;
+}
+
+void destroy_ctx(mics_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (int w = 0; w < c->world; ++w)
+    if (w != c->wrank && c->peer_base[w]) cudaIpcCloseMemHandle(c->peer_base[w]);
+  cudaFree(c->ring);
+  cudaFree(c->d_tickets);
+  cudaFree(c->d_nbar);
+  cudaFree(c->d_tab);
+  cudaFree(c->base);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+void ipc_export(mics_ctx* c, void* handle) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == MICS_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  MICS_CUDA(cudaIpcGetMemHandle(&h, c->base));
+  std::memcpy(handle, &h, sizeof(h));
+}
+
+void ipc_import(mics_ctx* c, const void* handles) {
+  if (c->ipc_ready) raise(MICS_CONFIG_ERROR, "IPC handles already imported");
+  MICS_CUDA(cudaSetDevice(c->device));
+  for (int w = 0; w < c->world; ++w) {
+    if (w == c->wrank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + size_t(w) * MICS_IPC_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    MICS_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->peer_base[w] = static_cast<char*>(p);
+  }
+  PeerTab tab;
+  std::memset(&tab, 0, sizeof(tab));
+  for (int w = 0; w < c->world; ++w) {
+    // slot w on our arena is written by process w; slot wrank on process w's arena is ours
+    tab.local_flag[w] = reinterpret_cast<uint64_t*>(c->base) + w;
+    tab.remote_flag[w] = reinterpret_cast<uint64_t*>(c->peer_base[w]) + c->wrank;
+  }
+  MICS_CUDA(cudaMemcpy(c->d_tab, &tab, sizeof(tab), cudaMemcpyHostToDevice));
+  c->ipc_ready = c->world > 1;
+}
+
+mics_buf alloc_sym(mics_ctx* c, uint64_t bytes_per_rank) {
+  mics_buf b;
+  b.stride = round_up(bytes_per_rank ? bytes_per_rank : 1, kAlign);
+  const uint64_t total = b.stride * uint64_t(c->per);
+  if (c->used + total > c->cap)
+    raise(MICS_INFEASIBLE, "arena exhausted: need " + std::to_string(total) + " bytes, " +
+                               std::to_string(c->cap - c->used) + " free (raise arena_bytes)");
+  b.offset = c->used;
+  c->used += total;
+  return b;
+}
+
+void check_buf_rank(const mics_ctx* c, mics_buf b, int rank, uint64_t off, uint64_t bytes) {
+  if (rank < 0 || rank >= c->n) raise(MICS_OUT_OF_RANGE, "rank " + std::to_string(rank) + " out of range");
+  if (off + bytes > b.stride)
+    raise(MICS_OUT_OF_RANGE, "access [" + std::to_string(off) + ", " + std::to_string(off + bytes) +
+                                 ") outside the rank's " + std::to_string(b.stride) + "-byte region");
+}
+
+void barrier_all(mics_ctx* c) {
+  if (c->world == 1) return;
+  uint64_t mask = 0;
+  for (int w = 0; w < c->world; ++w)
+    if (w != c->wrank) mask |= 1ull << w;
+  launch_barrier(c->stream, c->barrier(mask, 1, 0));
+  c->launches++;
+}
+}  // namespace mics

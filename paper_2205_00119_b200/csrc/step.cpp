@@ -1,0 +1,316 @@
+// MiCS step driver: one global training step of the communication hot path,
+// executed for real in the order the reference's simulator models it
+// (simulator.cpp:265-280):
+//   for each of s micro-steps:
+//     forward pass  — per-layer parameter all-gather, layers 0..L-1
+//     backward pass — per-layer parameter all-gather, layers L-1..0
+//     micro-step sync — coalesced reduce-scatter of every layer's gradient inside
+//                       the partition group (2-hop hop 1, sync_schedule.hpp:118-147)
+//   boundary — replication-group all-reduce fused with sharded fp32 Adam (hop 2,
+//              :153-185 + the optimizer the reference leaves out)
+//
+// Everything is planned once into device-resident descriptor tables (persistent
+// Launches) and replayed every step.  Layout per rank (symmetric arena):
+//   param_bf16 [shard]  master/m/v fp32 [shard]  gathered bf16 [2 x max layer]
+//   grads [s x grad_elems] (resident) or [grad_elems] (generated each micro-step)
+//   gradient accumulator = the mics_sync shard (fp32, padded to r*sub)
+// Layer l's chunk is ceil(E_l/p) rounded up to 8 elements, so every all-gather
+// and reduce-scatter descriptor is 16-byte aligned.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "internal.h"
+#include "sync.h"
+
+
+namespace mics {
+
+namespace {
+constexpr uint32_t kAlignElems = 8;
+
+void release(mics_step* st) {
+  for (auto& v : st->ag)
+    for (auto& l : v) l.release();
+  for (auto& l : st->rs) l.release();
+  st->bnd.rs.release();
+  st->bnd.ag.release();
+}
+
+// flat all-gather of layer l into gathered buffer (l % 2) of every local rank
+std::vector<Launch> build_layer_ag(mics_step* st, int l) {
+  mics_ctx* ctx = st->ctx;
+  mics_sync* sy = st->sync;
+  const int p = sy->p, n = sy->n;
+  const uint64_t c = sy->chunk[size_t(l)], cb = c * 2, soff = sy->shard_off[size_t(l)] * 2;
+  const uint64_t goff = uint64_t(l % 2) * st->gathered_half;
+  auto G = [&](int r, uint64_t pos) { return ctx->rank_ptr(st->gathered, r) + goff + pos * cb; };
+  std::vector<Launch> out;
+  const int k = st->cfg.hier_k;
+  if (k <= 0 || p <= k) {
+    CopyPlan plan;
+    for (int g = 0; g < n / p; ++g) {
+      std::vector<void*> dummy;
+      for (int i = 0; i < p; ++i) {
+        std::vector<void*> dsts;
+        for (int j = 0; j < p; ++j)
+          if (ctx->local(g * p + j)) dsts.push_back(G(g * p + j, uint64_t(i)));
+        plan.add(ctx->rank_ptr(st->pbf16, g * p + i) + soff, dsts, cb);
+      }
+    }
+    // no barrier: shards are static between boundaries; the micro-step
+    // reduce-scatter and Adam barriers order every write against these reads
+    out.push_back(make_copy_launch(ctx, plan, ctx->barrier(0, 0, 0), true));
+    return out;
+  }
+  // hierarchical: stage 1 (channels) with stage 2 folded into addressing, then stage 3
+  const int q = p / k;
+  CopyPlan ph1, ph2;
+  uint64_t mask = 0;
+  for (int g = 0; g < n / p; ++g) {
+    const int base = g * p;
+    std::vector<int> ranks(static_cast<size_t>(p));
+    for (int i = 0; i < p; ++i) ranks[size_t(i)] = base + i;
+    mask |= ctx->peer_mask(ranks.data(), p);
+    for (int mm = 0; mm < q; ++mm)
+      for (int j = 0; j < k; ++j) {
+        const int r = base + mm * k + j;
+        if (!ctx->local(r)) continue;
+        for (int m2 = 0; m2 < q; ++m2)
+          ph1.add(ctx->rank_ptr(st->pbf16, base + m2 * k + j) + soff, {G(r, uint64_t(m2) * k + j)}, cb);
+        for (int j2 = 0; j2 < k; ++j2) {
+          if (j2 == j) continue;
+          for (int t = 0; t < q; ++t) {
+            const uint64_t pos = uint64_t(t) * k + j2;
+            ph2.add(G(base + mm * k + j2, pos), {G(r, pos)}, cb);
+          }
+        }
+      }
+  }
+  out.push_back(make_copy_launch(ctx, ph1, ctx->barrier(mask, 0, 1), true));
+  out.push_back(make_copy_launch(ctx, ph2, ctx->barrier(mask, 0, 1), true));
+  return out;
+}
+
+void enqueue_generate(mics_step* st, int t) {
+  mics_ctx* ctx = st->ctx;
+  const uint64_t szg = dtype_size(st->cfg.grad_t);
+  const uint64_t off = st->cfg.resident_grads ? uint64_t(t) * st->sync->grad_elems * szg : 0;
+  for (int r = 0; r < ctx->n; ++r) {
+    if (!ctx->local(r)) continue;
+    launch_generate(ctx->stream, ctx->rank_ptr(st->grads, r) + off, st->cfg.grad_t, st->cfg.seed, r, t, 0, 0,
+                    st->sync->grad_elems, ctx->nsm * 8);
+    ctx->launches++;
+  }
+}
+
+void enqueue_boundary(mics_step* st) {
+  mics_ctx* ctx = st->ctx;
+  st->adam_step++;
+  if (st->bnd.has_rs) enqueue(ctx, st->bnd.rs);
+  if (st->bnd.has_ag) {
+    st->bnd.ag.adam = make_adam_scalars(st->cfg.lr, st->cfg.beta1, st->cfg.beta2, st->cfg.eps, st->cfg.weight_decay,
+                                        st->adam_step, st->adam.grad_scale);
+    enqueue(ctx, st->bnd.ag);
+  }
+}
+
+void enqueue_micro(mics_step* st, int t) {
+  for (size_t l = 0; l < st->layers.size(); ++l)
+    for (auto& x : st->ag[l]) enqueue(st->ctx, x);
+  for (size_t l = st->layers.size(); l-- > 0;)
+    for (auto& x : st->ag[l]) enqueue(st->ctx, x);
+  enqueue(st->ctx, st->rs[size_t(t)]);
+}
+}  // namespace
+
+mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
+  if (!cfg || cfg->nlayers < 1 || !cfg->layer_params) raise(MICS_OUT_OF_RANGE, "step config needs >= 1 layer");
+  if (cfg->grad_t != MICS_F32 && cfg->grad_t != MICS_BF16) raise(MICS_TYPE_MISMATCH, "gradients must be f32 or bf16");
+  if (cfg->hier_k > 0) {
+    if (!mics_partition_shape_ok(cfg->p, cfg->hier_k) || ctx->n % cfg->hier_k)
+      raise(MICS_SHAPE_ERROR, "partition size p=" + std::to_string(cfg->p) + " is not node-aligned for k=" +
+                                  std::to_string(cfg->hier_k));
+  }
+  if (cfg->alternative) raise(MICS_CONFIG_ERROR, "the step driver runs the 2-hop schedule (use mics_sync_alt_step)");
+  auto* st = new mics_step();
+  try {
+    st->ctx = ctx;
+    st->cfg = *cfg;
+    st->layers.assign(cfg->layer_params, cfg->layer_params + cfg->nlayers);
+    st->cfg.layer_params = nullptr;
+    st->sync = sync_create(ctx, cfg->p, cfg->s, cfg->nlayers, st->layers.data(), MICS_F32, kAlignElems);
+    mics_sync* sy = st->sync;
+    const uint64_t S = sy->shard_elems, szg = dtype_size(cfg->grad_t);
+    uint64_t maxl = 0;
+    for (uint64_t c : sy->chunk) maxl = std::max(maxl, c * uint64_t(sy->p) * 2);
+    st->gathered_half = round_up(maxl, 256);
+    st->pbf16 = alloc_sym(ctx, S * 2);
+    st->master = alloc_sym(ctx, S * 4);
+    st->m = alloc_sym(ctx, S * 4);
+    st->v = alloc_sym(ctx, S * 4);
+    st->gathered = alloc_sym(ctx, 2 * st->gathered_half);
+    st->grads = alloc_sym(ctx, (cfg->resident_grads ? uint64_t(cfg->s) : 1) * sy->grad_elems * szg);
+    // initial state: master = generator(seed ^ 0x5eed, "rank" = partition position r % p, layer 255),
+    // so every replica of a shard starts identical; m = v = 0; bf16 copy of master
+    for (int r = 0; r < ctx->n; ++r) {
+      if (!ctx->local(r)) continue;
+      launch_generate(ctx->stream, ctx->rank_ptr(st->master, r), MICS_F32, cfg->seed ^ 0x5eedull, r % cfg->p, 0, 255,
+                      0, S, ctx->nsm * 8);
+      MICS_CUDA(cudaMemsetAsync(ctx->rank_ptr(st->m, r), 0, S * 4, ctx->stream));
+      MICS_CUDA(cudaMemsetAsync(ctx->rank_ptr(st->v, r), 0, S * 4, ctx->stream));
+      launch_cast_bf16(ctx->stream, reinterpret_cast<const float*>(ctx->rank_ptr(st->master, r)),
+                       reinterpret_cast<uint16_t*>(ctx->rank_ptr(st->pbf16, r)), S, ctx->nsm * 8);
+    }
+    if (cfg->resident_grads)
+      for (int t = 0; t < cfg->s; ++t) enqueue_generate(st, t);
+    // plans
+    for (int l = 0; l < cfg->nlayers; ++l) st->ag.push_back(build_layer_ag(st, l));
+    for (int t = 0; t < cfg->s; ++t)
+      st->rs.push_back(build_micro_launch(sy, st->grads, cfg->resident_grads ? uint64_t(t) * sy->grad_elems * szg : 0,
+                                          cfg->grad_t, 1.0, t == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE, true,
+                                          false, 1, 1));
+    st->adam.lr = cfg->lr;
+    st->adam.beta1 = cfg->beta1;
+    st->adam.beta2 = cfg->beta2;
+    st->adam.eps = cfg->eps;
+    st->adam.weight_decay = cfg->weight_decay;
+    st->adam.step = 1;
+    st->adam.grad_scale = 1.0 / (double(ctx->n) * cfg->s);  // mean over the global batch of n*s micro-batches
+    st->adam.param = st->master;
+    st->adam.exp_avg = st->m;
+    st->adam.exp_avg_sq = st->v;
+    st->adam.param_bf16 = st->pbf16;
+    st->adam.write_grad = 0;
+    st->bnd = build_boundary(sy, &st->adam, true, false);
+    // stats (per rank per step), algorithmic bytes of SURVEY §8(d)
+    const int p = sy->p, r = sy->n / p;
+    uint64_t csum = 0;
+    for (uint64_t c : sy->chunk) csum += c;
+    st->stats.ag_bytes_in = 2ull * uint64_t(cfg->s) * uint64_t(p - 1) * csum * 2;
+    st->stats.rs_bytes_in = uint64_t(cfg->s) * uint64_t(p - 1) * csum * szg;
+    st->stats.ar_bytes_in = r > 1 ? 2ull * uint64_t(r - 1) * sy->sub * 4 : 0;
+    st->stats.adam_hbm_bytes = S * 30;
+    st->stats.gen_bytes = cfg->resident_grads ? 0 : uint64_t(cfg->s) * sy->grad_elems * szg;
+    st->stats.shard_elems = S;
+    st->stats.gathered_max_bytes = maxl;
+    st->stats.grad_elems = sy->grad_elems;
+    // everybody's initial parameters are written before anyone gathers them
+    MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+    barrier_all(ctx);
+    MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+    // kernels one step launches on this process (enqueue() skips empty launches)
+    uint64_t per = 0;
+    for (int t = 0; t < cfg->s; ++t) {
+      per += cfg->resident_grads ? 0 : uint64_t(ctx->per);
+      for (auto& v : st->ag)
+        for (auto& x : v) per += 2 * uint64_t((x.ndesc || x.bar.mask) ? 1 : 0);
+      per += (st->rs[size_t(t)].ndesc || st->rs[size_t(t)].bar.mask) ? 1 : 0;
+    }
+    if (st->bnd.has_rs) per += (st->bnd.rs.ndesc || st->bnd.rs.bar.mask) ? 1 : 0;
+    if (st->bnd.has_ag) per += (st->bnd.ag.ndesc || st->bnd.ag.bar.mask) ? 1 : 0;
+    st->stats.launches = per;
+  } catch (...) {
+    release(st);
+    delete st;
+    throw;
+  }
+  return st;
+}
+
+void step_destroy(mics_step* st) {
+  if (!st) return;
+  cudaStreamSynchronize(st->ctx->stream);
+  release(st);
+  delete st->sync;
+  delete st;
+}
+
+void step_run(mics_step* st, int iters) {
+  for (int it = 0; it < iters; ++it) {
+    for (int t = 0; t < st->cfg.s; ++t) {
+      if (!st->cfg.resident_grads) enqueue_generate(st, t);
+      enqueue_micro(st, t);
+    }
+    enqueue_boundary(st);
+  }
+  st->stats.adam_step = st->adam_step;
+}
+
+// One step with CUDA events around each phase; returns milliseconds per phase.
+void step_profile(mics_step* st, double* ag_ms, double* rs_ms, double* bnd_ms, double* gen_ms) {
+  mics_ctx* ctx = st->ctx;
+  const int s = st->cfg.s;
+  std::vector<cudaEvent_t> ev(size_t(4 * s + 2));
+  for (auto& e : ev) MICS_CUDA(cudaEventCreate(&e));
+  int k = 0;
+  for (int t = 0; t < s; ++t) {
+    MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
+    if (!st->cfg.resident_grads) enqueue_generate(st, t);
+    MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
+    for (size_t l = 0; l < st->layers.size(); ++l)
+      for (auto& x : st->ag[l]) enqueue(ctx, x);
+    for (size_t l = st->layers.size(); l-- > 0;)
+      for (auto& x : st->ag[l]) enqueue(ctx, x);
+    MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
+    enqueue(ctx, st->rs[size_t(t)]);
+    MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
+  }
+  MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
+  enqueue_boundary(st);
+  MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
+  MICS_CUDA(cudaEventSynchronize(ev[size_t(k - 1)]));
+  float a = 0, r = 0, g = 0, b = 0, x;
+  for (int t = 0; t < s; ++t) {
+    MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * t)], ev[size_t(4 * t + 1)]));
+    g += x;
+    MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * t + 1)], ev[size_t(4 * t + 2)]));
+    a += x;
+    MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * t + 2)], ev[size_t(4 * t + 3)]));
+    r += x;
+  }
+  MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * s)], ev[size_t(4 * s + 1)]));
+  b = x;
+  for (auto& e : ev) cudaEventDestroy(e);
+  *ag_ms = a;
+  *rs_ms = r;
+  *bnd_ms = b;
+  *gen_ms = g;
+  st->stats.adam_step = st->adam_step;
+}
+
+// End-to-end variant through host memory: every micro-step each local rank's
+// gradients are copied from (pinned) host memory — host_grads holds s gradient
+// sets of grad_elems, shared by the local ranks, one DMA per rank — and after the
+// boundary a fixed-size slice of every local rank's updated master shard is read back.
+void step_run_host(mics_step* st, const void* host_grads, int iters, void* host_result) {
+  mics_ctx* ctx = st->ctx;
+  const uint64_t szg = dtype_size(st->cfg.grad_t), gb = st->sync->grad_elems * szg;
+  const uint64_t rb = std::min(st->host_result_elems, st->sync->shard_elems) * 4;
+  for (int it = 0; it < iters; ++it) {
+    for (int t = 0; t < st->cfg.s; ++t) {
+      const uint64_t off = st->cfg.resident_grads ? uint64_t(t) * gb : 0;
+      for (int r = 0; r < ctx->n; ++r) {
+        if (!ctx->local(r)) continue;
+        MICS_CUDA(cudaMemcpyAsync(ctx->rank_ptr(st->grads, r) + off,
+                                  static_cast<const char*>(host_grads) + uint64_t(t) * gb, gb,
+                                  cudaMemcpyHostToDevice, ctx->stream));
+      }
+      enqueue_micro(st, t);
+    }
+    enqueue_boundary(st);
+    if (host_result) {
+      int li = 0;
+      for (int r = 0; r < ctx->n; ++r) {
+        if (!ctx->local(r)) continue;
+        MICS_CUDA(cudaMemcpyAsync(static_cast<char*>(host_result) + uint64_t(li) * rb, ctx->rank_ptr(st->master, r), rb,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+        ++li;
+      }
+    }
+  }
+  st->stats.adam_step = st->adam_step;
+}
+
+}  // namespace mics

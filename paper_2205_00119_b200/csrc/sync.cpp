@@ -1,0 +1,289 @@
+// 2-hop gradient synchronisation (sync_schedule.hpp) on the device.
+//
+// mics_sync is SyncState<T> (sync_schedule.hpp:45-51) for every rank of the job,
+// with the shard resident in the symmetric arena.  The schedule keeps the
+// reference's state machine (check_micro_step :87-103 -> MICS_BOUNDARY_VIOLATION),
+// its SyncEvent log (:27-32, byte counts of :142-144, :179-182, :219-222) and its
+// traffic accounting; the data movement is the sm_100a pull engines:
+//   micro-step  (:118-147) one k_reduce launch over every partition group and
+//               segment: shard (+)= fold_{i<p} grad_i (ascending position)
+//   boundary    (:153-185) k_reduce in place inside every replication group, then
+//               k_copy (reference AR) or k_adam (AR's all-gather fused with Adam)
+//   alternative (:189-232) AR over all n ranks into scratch + owned-chunk accumulate
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <string>
+
+#include "internal.h"
+#include "sync.h"
+
+namespace mics {
+
+namespace {
+void check_window(const mics_sync* st, bool at_boundary) {  // check_micro_step, sync_schedule.hpp:87-103
+  if (at_boundary && st->micro_step != st->s)
+    raise(MICS_BOUNDARY_VIOLATION, "boundary sync requires micro_step = s, have " + std::to_string(st->micro_step) +
+                                       " of " + std::to_string(st->s));
+  if (!at_boundary && st->micro_step >= st->s)
+    raise(MICS_BOUNDARY_VIOLATION, "micro-step past accumulation boundary (micro_step = s = " +
+                                       std::to_string(st->s) + ")");
+}
+std::vector<int> iota_ranks(int first, int count, int stride) {
+  std::vector<int> r(static_cast<size_t>(count));
+  for (int i = 0; i < count; ++i) r[size_t(i)] = first + i * stride;
+  return r;
+}
+}  // namespace
+
+mics_sync* sync_create(mics_ctx* ctx, int p, int s, int nseg, const uint64_t* seg_len, mics_dtype acc_t,
+                       uint32_t align) {
+  const int n = ctx->n;
+  if (p < 1 || p > n)  // build_group_layout, topology.cpp:22-27
+    raise(MICS_OUT_OF_RANGE, "partition size p=" + std::to_string(p) + " must satisfy 1 <= p <= n=" +
+                                 std::to_string(n));
+  if (n % p) raise(MICS_NON_DIVISIBLE, "partition size p=" + std::to_string(p) + " does not divide n=" +
+                                           std::to_string(n));
+  if (s < 1) raise(MICS_OUT_OF_RANGE, "micro-step count s must be >= 1");  // make_sync_states :61
+  if (nseg < 1 || !seg_len) raise(MICS_OUT_OF_RANGE, "need at least one gradient segment");
+  if (acc_t == MICS_BF16) raise(MICS_TYPE_MISMATCH, "shard accumulate type must be i64, f32 or f64");
+  if (align < 1) align = 1;
+  auto* st = new mics_sync();
+  st->ctx = ctx;
+  st->n = n;
+  st->p = p;
+  st->s = s;
+  st->nseg = nseg;
+  st->acc_t = acc_t;
+  uint64_t so = 0, go = 0;
+  for (int i = 0; i < nseg; ++i) {
+    const uint64_t c = round_up(ceil_div(seg_len[i], uint64_t(p)), align);  // owned_chunk_elems :53-56
+    st->len.push_back(seg_len[i]);
+    st->chunk.push_back(c);
+    st->shard_off.push_back(so);
+    st->grad_off.push_back(go);
+    so += c;
+    go += c * uint64_t(p);
+  }
+  st->shard_elems = so;
+  st->grad_elems = go;
+  const int r = n / p;
+  st->sub = round_up(ceil_div(so, uint64_t(r)), 4);
+  const uint64_t sz = dtype_size(acc_t);
+  st->shard = alloc_sym(ctx, std::max<uint64_t>(uint64_t(r) * st->sub, 1) * sz);
+  // SyncState shards start at T{} (make_sync_states :65)
+  MICS_CUDA(cudaMemsetAsync(ctx->base + st->shard.offset, 0, st->shard.stride * uint64_t(ctx->per), ctx->stream));
+  return st;
+}
+
+// ---- micro-step: one reduce launch over all partition groups and segments
+Launch build_micro_launch(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode,
+                          bool persistent, bool record, int entry, int exit) {
+  mics_ctx* ctx = st->ctx;
+  const int p = st->p;
+  const uint64_t szg = dtype_size(grad_t), sza = dtype_size(st->acc_t);
+  RedPlan plan(grad_t);
+  uint64_t mask = 0;
+  for (int g = 0; g < st->n / p; ++g) {
+    const std::vector<int> ranks = iota_ranks(g * p, p, 1);
+    if (record) {
+      for (int i = 0; i < p; ++i)
+        for (int j = 0; j < p; ++j)
+          if (i != j)
+            for (int q = 0; q < st->nseg; ++q) ctx->record(g * p + i, g * p + j, st->chunk[size_t(q)] * szg);
+    }
+    mask |= ctx->peer_mask(ranks.data(), p);
+    for (int j = 0; j < p; ++j) {
+      const int rank = g * p + j;
+      if (!ctx->local(rank)) continue;
+      for (int q = 0; q < st->nseg; ++q) {
+        const uint64_t c = st->chunk[size_t(q)], first = uint64_t(j) * c;
+        std::vector<const void*> srcs(static_cast<size_t>(p));
+        for (int i = 0; i < p; ++i)
+          srcs[size_t(i)] = ctx->rank_ptr(grads, g * p + i) + goff + (st->grad_off[size_t(q)] + first) * szg;
+        const uint64_t len = st->len[size_t(q)];
+        plan.add(srcs, ctx->rank_ptr(st->shard, rank) + st->shard_off[size_t(q)] * sza, c,
+                 len > first ? len - first : 0);
+      }
+    }
+  }
+  return make_reduce_launch(ctx, plan, grad_t, st->acc_t, scale, mode, ctx->barrier(mask, entry, exit), persistent);
+}
+
+void micro_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode) {
+  check_window(st, false);
+  if (!(grad_t == st->acc_t || (grad_t == MICS_BF16 && st->acc_t == MICS_F32)))
+    raise(MICS_TYPE_MISMATCH, "gradient type does not match the shard type");
+  if (goff + st->grad_elems * dtype_size(grad_t) > grads.stride)
+    raise(MICS_SIZE_MISMATCH, "gradient buffer smaller than the padded gradient layout");
+  Launch l = build_micro_launch(st, grads, goff, grad_t, scale, mode, false, true, 1, 1);
+  enqueue(st->ctx, l);
+  uint64_t cs = 0;
+  for (uint64_t c : st->chunk) cs += c;
+  for (int g = 0; g < st->n / st->p; ++g)  // :142-144
+    st->events.push_back({st->micro_step, 0, g, int64_t(uint64_t(st->p - 1) * cs * dtype_size(grad_t))});
+  st->micro_step++;
+}
+
+// ---- boundary
+BoundaryLaunches build_boundary(mics_sync* st, const mics_adam* adam, bool persistent, bool record) {
+  mics_ctx* ctx = st->ctx;
+  const int n = st->n, p = st->p, r = n / p;
+  const uint64_t sza = dtype_size(st->acc_t), sub = st->sub;
+  BoundaryLaunches out;
+  uint64_t rmask = 0, pmask = 0;
+  for (int j = 0; j < p; ++j) {
+    const std::vector<int> ranks = iota_ranks(j, r, p);
+    rmask |= ctx->peer_mask(ranks.data(), r);
+  }
+  for (int g = 0; g < n / p; ++g) {
+    const std::vector<int> ranks = iota_ranks(g * p, p, 1);
+    pmask |= ctx->peer_mask(ranks.data(), p);
+  }
+  if (record && r > 1) {  // all_reduce over the padded shard: RS + AG messages (collectives.cpp:185-190)
+    const uint64_t padded = ceil_div(st->shard_elems, uint64_t(r)) * uint64_t(r);
+    for (int j = 0; j < p; ++j)
+      for (int a = 0; a < r; ++a)
+        for (int b = 0; b < r; ++b)
+          if (a != b) {
+            ctx->record(j + a * p, j + b * p, padded / uint64_t(r) * sza);
+            ctx->record(j + a * p, j + b * p, padded / uint64_t(r) * sza);
+          }
+  }
+  if (r > 1) {  // reduce-scatter in place: position i folds slice i of every replica's shard
+    RedPlan rs(st->acc_t);
+    for (int rho = 0; rho < n; ++rho) {
+      if (!ctx->local(rho)) continue;
+      const int j = rho % p, i = rho / p;
+      std::vector<const void*> srcs(static_cast<size_t>(r));
+      for (int q = 0; q < r; ++q) srcs[size_t(q)] = ctx->rank_ptr(st->shard, j + q * p) + uint64_t(i) * sub * sza;
+      rs.add(srcs, ctx->rank_ptr(st->shard, rho) + uint64_t(i) * sub * sza, sub, sub);
+    }
+    out.rs = make_reduce_launch(ctx, rs, st->acc_t, st->acc_t, 1.0, MICS_RS_STORE, ctx->barrier(rmask, 1, 1),
+                                persistent);
+    out.has_rs = true;
+  }
+  if (adam) {
+    if (st->acc_t != MICS_F32) raise(MICS_TYPE_MISMATCH, "the fused Adam update needs an f32 shard");
+    AdamPlan ap;
+    const uint64_t asub = r > 1 ? sub : round_up(std::max<uint64_t>(st->shard_elems, 1), 4);
+    for (int rho = 0; rho < n; ++rho) {
+      if (!ctx->local(rho)) continue;
+      const int j = rho % p;
+      std::vector<const void*> srcs(static_cast<size_t>(r));
+      for (int q = 0; q < r; ++q) srcs[size_t(q)] = ctx->rank_ptr(st->shard, j + q * p);
+      uint16_t* pb = adam->param_bf16.stride ? reinterpret_cast<uint16_t*>(ctx->rank_ptr(adam->param_bf16, rho)) : nullptr;
+      ap.add(srcs, reinterpret_cast<float*>(ctx->rank_ptr(adam->param, rho)),
+             reinterpret_cast<float*>(ctx->rank_ptr(adam->exp_avg, rho)),
+             reinterpret_cast<float*>(ctx->rank_ptr(adam->exp_avg_sq, rho)), pb,
+             adam->write_grad ? reinterpret_cast<float*>(ctx->rank_ptr(st->shard, rho)) : nullptr, st->shard_elems,
+             asub);
+    }
+    // exit barrier with the replication group (done reading its slices) and the
+    // partition group (their next all-gather reads the parameters updated here)
+    out.ag = make_adam_launch(ctx, ap,
+                              make_adam_scalars(adam->lr, adam->beta1, adam->beta2, adam->eps, adam->weight_decay,
+                                                adam->step, adam->grad_scale),
+                              ctx->barrier(rmask | pmask, 0, 1), persistent);
+    out.has_ag = true;
+  } else if (r > 1) {
+    CopyPlan ag;
+    for (int rho = 0; rho < n; ++rho) {
+      if (!ctx->local(rho)) continue;
+      const int j = rho % p, i = rho / p;
+      for (int q = 0; q < r; ++q) {
+        if (q == i) continue;
+        const uint64_t o = uint64_t(q) * sub * sza;
+        ag.add(ctx->rank_ptr(st->shard, j + q * p) + o, {ctx->rank_ptr(st->shard, rho) + o}, sub * sza);
+      }
+    }
+    out.ag = make_copy_launch(ctx, ag, ctx->barrier(rmask, 0, 1), persistent);
+    out.has_ag = true;
+  }
+  return out;
+}
+
+void boundary(mics_sync* st, const mics_adam* adam) {
+  check_window(st, true);
+  BoundaryLaunches b = build_boundary(st, adam, false, true);
+  if (b.has_rs) enqueue(st->ctx, b.rs);
+  if (b.has_ag) enqueue(st->ctx, b.ag);
+  const int r = st->n / st->p;
+  const uint64_t padded = ceil_div(st->shard_elems, uint64_t(r)) * uint64_t(r);
+  for (int j = 0; j < st->p; ++j)  // :179-182
+    st->events.push_back(
+        {st->s, 1, j, int64_t(2 * uint64_t(r - 1) * (padded / uint64_t(r)) * dtype_size(st->acc_t))});
+  st->micro_step = 0;  // :184
+}
+
+// ---- alternative (DeepSpeed-default) schedule: all-reduce over all n ranks
+void alt_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale) {
+  check_window(st, false);
+  if (!(grad_t == st->acc_t || (grad_t == MICS_BF16 && st->acc_t == MICS_F32)))
+    raise(MICS_TYPE_MISMATCH, "gradient type does not match the shard type");
+  if (goff + st->grad_elems * dtype_size(grad_t) > grads.stride)
+    raise(MICS_SIZE_MISMATCH, "gradient buffer smaller than the padded gradient layout");
+  mics_ctx* ctx = st->ctx;
+  const int n = st->n, p = st->p;
+  const uint64_t szg = dtype_size(grad_t), sza = dtype_size(st->acc_t);
+  if (!st->alt_ready) {  // per segment: n slices of ceil(p*chunk/n) elements (SPMD: same on every process)
+    uint64_t off = 0;
+    for (int q = 0; q < st->nseg; ++q) {
+      const uint64_t sub = ceil_div(uint64_t(p) * st->chunk[size_t(q)], uint64_t(n));
+      st->alt_sub.push_back(sub);
+      st->alt_off.push_back(off);
+      off += sub * uint64_t(n);
+    }
+    st->alt = alloc_sym(ctx, std::max<uint64_t>(off, 1) * sza);
+    st->alt_ready = true;
+  }
+  std::vector<int> all = iota_ranks(0, n, 1);
+  const uint64_t mask = ctx->peer_mask(all.data(), n);
+  RedPlan rs(grad_t);
+  CopyPlan ag;
+  RedPlan acc(st->acc_t);
+  for (int rho = 0; rho < n; ++rho) {
+    if (!ctx->local(rho)) continue;
+    for (int q = 0; q < st->nseg; ++q) {
+      const uint64_t total = uint64_t(p) * st->chunk[size_t(q)], sub = st->alt_sub[size_t(q)];
+      const uint64_t first = uint64_t(rho) * sub;
+      const uint64_t elems = first < total ? std::min(sub, total - first) : 0;
+      std::vector<const void*> srcs(static_cast<size_t>(n));
+      for (int i = 0; i < n; ++i)
+        srcs[size_t(i)] = ctx->rank_ptr(grads, i) + goff + (st->grad_off[size_t(q)] + first) * szg;
+      const uint64_t len = st->len[size_t(q)];
+      rs.add(srcs, ctx->rank_ptr(st->alt, rho) + (st->alt_off[size_t(q)] + first) * sza, elems,
+             len > first ? len - first : 0);
+      for (int i = 0; i < n; ++i) {
+        if (i == rho) continue;
+        const uint64_t f2 = uint64_t(i) * sub;
+        const uint64_t e2 = f2 < total ? std::min(sub, total - f2) : 0;
+        const uint64_t o = (st->alt_off[size_t(q)] + f2) * sza;
+        ag.add(ctx->rank_ptr(st->alt, i) + o, {ctx->rank_ptr(st->alt, rho) + o}, e2 * sza);
+      }
+      const uint64_t c = st->chunk[size_t(q)];
+      acc.add({ctx->rank_ptr(st->alt, rho) + (st->alt_off[size_t(q)] + uint64_t(rho % p) * c) * sza},
+              ctx->rank_ptr(st->shard, rho) + st->shard_off[size_t(q)] * sza, c, c);
+    }
+  }
+  enqueue(ctx, make_reduce_launch(ctx, rs, grad_t, st->acc_t, scale, MICS_RS_STORE, ctx->barrier(mask, 1, 1), false));
+  enqueue(ctx, make_copy_launch(ctx, ag, ctx->barrier(mask, 0, 1), false));
+  enqueue(ctx, make_reduce_launch(ctx, acc, st->acc_t, st->acc_t, 1.0, MICS_RS_ACCUMULATE, ctx->barrier(0, 0, 0), false));
+  const uint64_t padded = ceil_div(st->grad_elems, uint64_t(n)) * uint64_t(n);  // :200-201
+  for (int a = 0; a < n; ++a)
+    for (int b = 0; b < n; ++b)
+      if (a != b) {
+        ctx->record(a, b, padded / uint64_t(n) * szg);
+        ctx->record(a, b, padded / uint64_t(n) * szg);
+      }
+  st->events.push_back({st->micro_step, 2, 0, int64_t(2 * uint64_t(n - 1) * (padded / uint64_t(n)) * szg)});
+  st->micro_step++;
+}
+
+void alt_boundary(mics_sync* st) {
+  check_window(st, true);
+  st->micro_step = 0;
+}
+
+}  // namespace mics

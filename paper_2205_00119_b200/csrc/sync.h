@@ -1,0 +1,62 @@
+// Sync-state and step-driver internals shared by sync.cpp, step.cpp and capi.cpp.
+#pragma once
+
+#include <array>
+#include <vector>
+
+#include "internal.h"
+
+struct mics_sync {
+  mics_ctx* ctx = nullptr;
+  int n = 0, p = 0, s = 1, nseg = 0;
+  mics_dtype acc_t = MICS_F32;
+  std::vector<uint64_t> len, chunk, shard_off, grad_off;
+  uint64_t shard_elems = 0, grad_elems = 0, sub = 0;
+  mics_buf shard{};
+  int micro_step = 0;
+  std::vector<std::array<int64_t, 4>> events;
+  // alternative schedule scratch (lazily allocated)
+  bool alt_ready = false;
+  mics_buf alt{};
+  std::vector<uint64_t> alt_sub, alt_off;
+};
+
+namespace mics {
+
+struct BoundaryLaunches {
+  Launch rs, ag;
+  bool has_rs = false, has_ag = false;
+};
+
+mics_buf alloc_sym(mics_ctx* c, uint64_t bytes_per_rank);
+void barrier_all(mics_ctx* c);
+void check_buf_rank(const mics_ctx* c, mics_buf b, int rank, uint64_t off, uint64_t bytes);
+
+mics_sync* sync_create(mics_ctx* ctx, int p, int s, int nseg, const uint64_t* seg_len, mics_dtype acc_t,
+                       uint32_t align);
+Launch build_micro_launch(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode,
+                          bool persistent, bool record, int entry, int exit);
+BoundaryLaunches build_boundary(mics_sync* st, const mics_adam* adam, bool persistent, bool record);
+void micro_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode);
+void boundary(mics_sync* st, const mics_adam* adam);
+void alt_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale);
+void alt_boundary(mics_sync* st);
+
+}  // namespace mics
+
+// MiCS step driver state (step.cpp)
+struct mics_step {
+  mics_ctx* ctx = nullptr;
+  mics_step_cfg cfg{};
+  std::vector<uint64_t> layers;
+  mics_sync* sync = nullptr;
+  mics_buf pbf16{}, master{}, m{}, v{}, gathered{}, grads{};
+  uint64_t gathered_half = 0;                 // bytes of one gathered buffer
+  std::vector<std::vector<mics::Launch>> ag;  // per layer: 1 launch (flat) or 2 (hierarchical)
+  std::vector<mics::Launch> rs;               // per micro-step
+  mics::BoundaryLaunches bnd;
+  mics_adam adam{};
+  int adam_step = 0;
+  mics_step_stats stats{};
+  uint64_t host_result_elems = 4096;
+};

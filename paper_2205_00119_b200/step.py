@@ -1,0 +1,115 @@
+"""MiCS step driver (host side of csrc/step.cpp) and the BASELINE.json workloads.
+
+A step = s micro-steps of {per-layer parameter all-gather (fwd), per-layer
+all-gather (bwd), coalesced gradient reduce-scatter} + the boundary all-reduce
+fused with sharded fp32 Adam (simulator.cpp:265-280 order, executed for real).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+from ._lib import Buf, StepCfg, StepStats, check, lib
+from .engine import DTYPE, Engine
+from .topology import transformer_layer_params
+
+
+@dataclass
+class Workload:
+    name: str
+    layer_params: list
+    p: int
+    s: int
+    grad_dtype: str = "f32"
+    hier_k: int = 0
+    n: int = 8
+    micro_batch: int = 8          # samples per rank per micro-step
+    note: str = ""
+
+    @property
+    def params(self) -> int:
+        return sum(self.layer_params)
+
+
+def workloads() -> dict:
+    """BASELINE.json configs."""
+    bert_large = transformer_layer_params(1024, 4096, 24, 30522, 512)
+    gpt2_xl = transformer_layer_params(1600, 6400, 48, 50257, 1024)
+    bert_10b = transformer_layer_params(2560, 10240, 127, 32008, 512)
+    return {
+        "C1": Workload("C1 4-layer MLP H=1024 (W+b), n=8, p=2, s=4, fp32", [1024 * 1024 + 1024] * 4, p=2, s=4),
+        "C3": Workload("C3 BERT-large-shaped 334M, n=8, p=2, s=4, fp32 grads", bert_large, p=2, s=4),
+        "C4": Workload("C4 GPT-2 1.5B-shaped, n=8, p=4, hierarchical k=2, bf16 grads", gpt2_xl, p=4, s=4,
+                       grad_dtype="bf16", hier_k=2),
+        "C5p2": Workload("C5 10B dense (BERT-10B), n=8, p=2, bf16 grads", bert_10b, p=2, s=4, grad_dtype="bf16"),
+        "C5p8": Workload("C5 10B dense (BERT-10B), n=8, p=8 (ZeRO-3), bf16 grads", bert_10b, p=8, s=4,
+                         grad_dtype="bf16"),
+    }
+
+
+@dataclass
+class StepOptions:
+    resident_grads: bool = True
+    seed: int = 2205
+    lr: float = 1e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+
+
+class MicsStep:
+    def __init__(self, engine: Engine, wl: Workload, opts: StepOptions = field(default_factory=StepOptions)):
+        if not isinstance(opts, StepOptions):
+            opts = StepOptions()
+        self.engine = engine
+        self.wl = wl
+        self.opts = opts
+        self._layers = (C.c_uint64 * len(wl.layer_params))(*wl.layer_params)
+        cfg = StepCfg(wl.p, wl.s, len(wl.layer_params), C.cast(self._layers, C.POINTER(C.c_uint64)),
+                      DTYPE[wl.grad_dtype], wl.hier_k, int(opts.resident_grads), 0, opts.seed, opts.lr, opts.beta1,
+                      opts.beta2, opts.eps, opts.weight_decay)
+        h = C.c_void_p()
+        check(lib.mics_step_create(engine.ctx, C.byref(cfg), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            check(lib.mics_step_destroy(self.h))
+            self.h = None
+
+    def run(self, iterations: int = 1) -> None:
+        """Enqueue `iterations` global steps on the engine's stream."""
+        check(lib.mics_step_run(self.engine.ctx, self.h, iterations))
+
+    def run_host(self, host_grads_ptr: int, iterations: int = 1, host_result_ptr: int | None = None) -> None:
+        check(lib.mics_step_run_host(self.engine.ctx, self.h, C.c_void_p(host_grads_ptr), iterations,
+                                     C.c_void_p(host_result_ptr) if host_result_ptr else None))
+
+    def profile(self) -> dict:
+        a, r, b, g = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        check(lib.mics_step_profile(self.engine.ctx, self.h, C.byref(a), C.byref(r), C.byref(b), C.byref(g)))
+        return {"allgather_ms": a.value, "reducescatter_ms": r.value, "boundary_ms": b.value, "generate_ms": g.value}
+
+    def stats(self) -> StepStats:
+        s = StepStats()
+        check(lib.mics_step_stats_get(self.h, C.byref(s)))
+        return s
+
+    def buffers(self) -> dict:
+        bufs = [Buf() for _ in range(6)]
+        check(lib.mics_step_buffers(self.h, *[C.byref(b) for b in bufs]))
+        return dict(zip(["param_bf16", "master", "exp_avg", "exp_avg_sq", "gathered", "grads"], bufs))
+
+    def sync_info(self):
+        from ._lib import SyncInfo
+        h = C.c_void_p()
+        check(lib.mics_step_sync(self.h, C.byref(h)))
+        info = SyncInfo()
+        check(lib.mics_sync_get_info(h, C.byref(info)))
+        segs = []
+        for i in range(info.nseg):
+            ln, ch, so, go = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+            check(lib.mics_sync_seg(h, i, C.byref(ln), C.byref(ch), C.byref(so), C.byref(go)))
+            segs.append((ln.value, ch.value, so.value, go.value))
+        return info, segs
