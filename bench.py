@@ -1,0 +1,458 @@
+"""MiCS step benchmark (BASELINE.json metric: MiCS step samples/s at 1/2/4/8 B200;
+partition-group collective GB/s vs NVLink).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3] [--impl mics|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU)
+  python bench.py --sweep ...                              (C2: AG/RS sweep 1 MiB..1 GiB vs NCCL)
+
+A step is one global MiCS step of the workload: s micro-steps of {per-layer bf16
+parameter all-gather fwd + bwd, coalesced fp32/bf16 gradient reduce-scatter} and the
+boundary replication-group all-reduce fused with sharded fp32 Adam.  The job has
+n = 8 ranks (the configs' 8 ranks) laid out node-major over the N GPUs, n/N virtual
+ranks per GPU: at N=1 every collective is intra-GPU (HBM-bound), at N=8 every
+partition group spans GPUs (NVLink-bound).  Total work is fixed ("strong").
+samples/s = n * micro_batch(8) * s / step time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_RANKS = 8
+MICRO_BATCH = 8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C3")
+    ap.add_argument("--impl", default="mics", choices=["mics", "reference"])
+    ap.add_argument("--ranks", type=int, default=N_RANKS)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--generated-grads", action="store_true", help="generate gradients inside the step (K6)")
+    ap.add_argument("--sweep", action="store_true", help="C2 collective sweep instead of the step")
+    return ap.parse_args()
+
+
+def env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        if not shutil.which("nvidia-smi"):
+            return
+        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits", "-lms", "100"],
+                                     stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def arena_bytes(wl, per, resident):
+    """Per-process arena for `per` local ranks (mirrors csrc/step.cpp's allocations)."""
+    p, s = wl.p, wl.s
+    chunks = [((e + p - 1) // p + 7) // 8 * 8 for e in wl.layer_params]
+    S = sum(chunks)
+    r = N_RANKS // p
+    sub = ((S + r - 1) // r + 3) // 4 * 4
+    szg = 2 if wl.grad_dtype == "bf16" else 4
+    gathered = 2 * (((max(chunks) * p * 2) + 255) // 256 * 256)
+    per_rank = r * sub * 4 + S * 2 + 3 * S * 4 + gathered + (s if resident else 1) * p * S * szg
+    return per * (per_rank + 8 * 4096) + (256 << 20)
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=GLOO)
+    return float(t.item())
+
+
+GLOO = None
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier(group=GLOO)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+# ----------------------------------------------------------------------------- CPU baseline (reference)
+def cpu_baseline(wl, threads):
+    """The reference's own step functions (oracle/_ref) on a bounded sample: ONE
+    full-size transformer block (or layer) of the workload, extrapolated to the
+    whole model by parameter count."""
+    import ctypes as C
+    from oracle.oracle import REF_SO, RefLib
+    sample = [max(wl.layer_params[1:] or wl.layer_params)]
+    if RefLib.available():
+        lib = C.CDLL(REF_SO)
+        lib.ref_step_sample.restype = C.c_double
+        arr = (C.c_uint64 * 1)(*sample)
+        sec = lib.ref_step_sample(threads, wl.n, wl.p, wl.s, 1, arr, 1)
+        kind = "reference"
+    else:  # the plain-C restatement, timed the same way (AG + 2-hop + Adam)
+        import numpy as np
+        from oracle.oracle import Oracle
+        ora = Oracle()
+        n, p, s, ln = wl.n, wl.p, wl.s, sample[0]
+        g = np.random.default_rng(0).standard_normal((s, n, ln)).astype(np.float32)
+        sh = np.zeros((p, (ln + p - 1) // p * 2), np.uint8)
+        t0 = time.perf_counter()
+        for _ in range(s):
+            for _ in range(2 * n // p):
+                ora.all_gather(sh)
+        out, _, _ = ora.two_hop(g, n, p, "f32")
+        for r in range(n):
+            ora.adam(np.zeros(out.shape[1]), np.zeros(out.shape[1]), np.zeros(out.shape[1]), out[r], 1e-4, 0.9,
+                     0.999, 1e-8, 0.0, 1, 1.0 / (n * s))
+        sec = time.perf_counter() - t0
+        kind, threads = "port", 1
+    if sec <= 0:
+        return None
+    scale = wl.params / sample[0]
+    step_s = sec * scale
+    return {"value": N_RANKS * MICRO_BATCH * wl.s / step_s, "unit": "samples/s", "cores": threads, "kind": kind,
+            "sample": f"1 of {len(wl.layer_params)} layers at full size ({sample[0]:,} params, all {wl.n} ranks, "
+                      f"p={wl.p}, s={wl.s}: per-layer all_gather fwd+bwd, two_hop_micro_step x s, "
+                      f"two_hop_boundary, Adam loop) = {sec:.2f} s, extrapolated x{scale:.1f} by parameter count",
+            "step_seconds": step_s}
+
+
+def run_reference(args, wl, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(wl, threads)
+        if cb is None:
+            print(json.dumps({"impl": "reference", "unavailable": "reference step sample failed"}))
+            return
+        if i >= args.warmup:
+            vals.append(cb)
+    v = statistics.median([c["value"] for c in vals])
+    line = {"impl": "reference", "metric": "MiCS step samples/s", "value": v, "unit": "samples/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * statistics.median([c["step_seconds"] for c in vals]),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": wl.name, "n_ranks": wl.n, "p": wl.p, "s": wl.s,
+                                            "micro_batch": MICRO_BATCH},
+            "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "samples/s"},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- NCCL comparator
+def nccl_step(wl, rank, world, steps, warmup):
+    """The same MiCS step with stock NCCL collectives on split communicators and
+    torch's fused Adam (only meaningful with one rank per GPU)."""
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device())
+    p, s, n = wl.p, wl.s, world
+    pg = {g: dist.new_group(list(range(g * p, (g + 1) * p))) for g in range(n // p)}
+    rg = {j: dist.new_group(list(range(j, n, p))) for j in range(p)}
+    my_pg, my_rg = pg[rank // p], rg[rank % p]
+    chunks = [((e + p - 1) // p + 7) // 8 * 8 for e in wl.layer_params]
+    S = sum(chunks)
+    gdt = torch.bfloat16 if wl.grad_dtype == "bf16" else torch.float32
+    shard = torch.randn(S, device=dev).to(torch.bfloat16)
+    gathered = torch.empty(2 * max(chunks) * p, dtype=torch.bfloat16, device=dev)
+    grads = [torch.randn(p * S, device=dev).to(gdt) for _ in range(s)]
+    acc = torch.zeros(S, dtype=torch.float32, device=dev)
+    tmp = torch.empty(S, dtype=gdt, device=dev)
+    master = torch.nn.Parameter(torch.randn(S, device=dev))
+    opt = torch.optim.Adam([master], lr=1e-4, fused=True)
+    offs = [0]
+    for c in chunks:
+        offs.append(offs[-1] + c)
+
+    def one():
+        for t in range(s):
+            for order in (range(len(chunks)), reversed(range(len(chunks)))):
+                for l in order:
+                    c = chunks[l]
+                    out = gathered[(l % 2) * max(chunks) * p:(l % 2) * max(chunks) * p + c * p]
+                    dist.all_gather_into_tensor(out, shard[offs[l]:offs[l] + c], group=my_pg)
+            dist.reduce_scatter_tensor(tmp, grads[t], group=my_pg)
+            acc.add_(tmp.float()) if t else acc.copy_(tmp.float())
+        if n // p > 1:
+            dist.all_reduce(acc, group=my_rg)
+        master.grad = acc
+        opt.step()
+        shard.copy_(master.detach().to(torch.bfloat16))
+
+    for _ in range(warmup):
+        one()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        one()
+    e1.record()
+    e1.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    return {"value": n * MICRO_BATCH * s / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
+            "what": "torch.distributed NCCL all_gather_into_tensor / reduce_scatter_tensor / all_reduce on split "
+                    "groups + torch.optim.Adam(fused=True), same shapes"}
+
+
+# ----------------------------------------------------------------------------- main arm
+def run_mics(args, wl, rank, world, local):
+    import torch
+
+    from paper_2205_00119_b200 import dist as mdist
+    from paper_2205_00119_b200.step import MicsStep, StepOptions
+    from paper_2205_00119_b200.engine import Engine, host_alloc, host_free
+
+    torch.cuda.set_device(local)
+    n = args.ranks
+    if n % world:
+        raise SystemExit(f"--gpus {world} must divide the {n} ranks")
+    per = n // world
+    resident = not args.generated_grads
+    eng = Engine(n_ranks=n, world=world, world_rank=rank, device=local,
+                 arena_bytes=arena_bytes(wl, per, resident))
+    mdist.connect(eng, GLOO)
+    step = MicsStep(eng, wl, StepOptions(resident_grads=resident))
+    stats = step.stats()
+    ext = torch.cuda.ExternalStream(eng.stream())
+
+    # warm-up, then the timed region (barrier + sync on both sides)
+    step.run(args.warmup)
+    eng.synchronize()
+    barrier(world)
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = eng.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eng.barrier()
+    eng.synchronize()
+    barrier(world)
+    e0.record(ext)
+    step.run(args.steps)
+    e1.record(ext)
+    e1.synchronize()
+    eng.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    launches = eng.launches - l0
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    samples = n * MICRO_BATCH * wl.s
+    value = samples / (ms / 1e3)
+
+    # per-phase device times (CUDA events on the launching stream), one extra step
+    prof = step.profile()
+    prof = {k: max_over_ranks(v, world) for k, v in prof.items()}
+    L = len(wl.layer_params)
+    nag = 2 * wl.s * L * (2 if wl.hier_k and wl.p > wl.hier_k else 1)
+    phases = {"allgather": (prof["allgather_ms"], nag), "reducescatter": (prof["reducescatter_ms"], wl.s),
+              "boundary": (prof["boundary_ms"], 2)}
+    dom = max(phases, key=lambda k: phases[k][0])
+    dom_ms, dom_launches = phases[dom]
+    # algorithmic bytes of the dominant phase per process per step
+    p, s = wl.p, wl.s
+    chunks = [((e + p - 1) // p + 7) // 8 * 8 for e in wl.layer_params]
+    S = sum(chunks)
+    szg = 2 if wl.grad_dtype == "bf16" else 4
+    groups_here = len({r // p for r in eng.local_ranks})
+    if dom == "allgather":
+        kernel = "k_copy (per-layer partition-group all-gather)"
+        hbm = 2 * s * (per * p * S * 2 + groups_here * p * S * 2)        # writes + one read per source chunk
+        ingress = 2 * s * per * (p - 1) * S * 2 if world > 1 and p > per else 0
+    elif dom == "reducescatter":
+        kernel = "k_reduce (micro-step reduce-scatter + shard accumulate)"
+        hbm = s * per * (p * S * szg + 4 * S) + (s - 1) * per * 4 * S
+        ingress = s * per * (p - 1) * S * szg if world > 1 and p > per else 0
+    else:
+        r = n // p
+        sub = stats.ar_bytes_in // max(1, 2 * (r - 1) * 4) if r > 1 else S
+        kernel = "k_reduce + k_adam (boundary all-reduce fused with Adam)"
+        hbm = per * (r * sub * 4 + sub * 4 + S * 30)
+        ingress = per * stats.ar_bytes_in if world > 1 and r > per else 0
+    pk, pk_kind = peaks()
+    per_launch_ms = dom_ms / dom_launches
+    if ingress:
+        achieved = ingress / dom_launches / (per_launch_ms / 1e3) / 1e9
+        roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                "frac": achieved / NVLINK_PEER_GBS, "traffic": None, "kernel": kernel,
+                "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md); 900 nominal",
+                "hbm_GBps": hbm / dom_launches / (per_launch_ms / 1e3) / 1e9}
+    else:
+        achieved = hbm / dom_launches / (per_launch_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": kernel,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})"}
+    roof["launch_ms"] = per_launch_ms
+    roof["bytes_per_launch"] = (ingress or hbm) / dom_launches
+
+    # end-to-end through the C-ABI with host buffers: gradients H2D every micro-step
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        gbytes = stats.grad_elems * szg
+        host, hptr = host_alloc(s * gbytes)
+        res, rptr = host_alloc(per * 4096 * 4)
+        import numpy as np
+        pat = np.random.default_rng(rank).standard_normal(1 << 22).astype(
+            np.float32 if szg == 4 else np.float32).view(np.uint8)
+        if szg == 2:
+            pat = pat.view(np.uint32).astype(np.uint32).view(np.uint16)[1::2].copy().view(np.uint8)
+        for o in range(0, host.size, pat.size):  # synthetic gradient values, tiled
+            host[o:o + pat.size] = pat[:host.size - o]
+        step.run_host(hptr, 1, rptr)  # warm-up
+        eng.synchronize()
+        barrier(world)
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        h0.record(ext)
+        step.run_host(hptr, args.e2e_steps, rptr)
+        h1.record(ext)
+        h1.synchronize()
+        wall = (time.perf_counter() - t0) / args.e2e_steps
+        ems = max_over_ranks(max(h0.elapsed_time(h1) / args.e2e_steps, wall * 1e3), world)
+        e2e = {"value": samples / (ems / 1e3), "unit": "samples/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": per * s * gbytes, "d2h_bytes_per_step": per * min(4096, S) * 4,
+               "path": "mics_step_run_host (C-ABI): pinned host gradients -> H2D every micro-step, "
+                       "result slice D2H after the boundary"}
+        host_free(hptr)
+        host_free(rptr)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, os.cpu_count() or 1)
+
+    nccl = None
+    if world > 1 and per == 1:
+        try:
+            nccl = nccl_step(wl, rank, world, max(2, args.steps // 2), 1)
+        except Exception as e:  # noqa: BLE001
+            nccl = {"error": str(e)[:200]}
+
+    line = {
+        "metric": "MiCS step samples/s", "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl.name, "n_ranks": n, "ranks_per_gpu": per, "p": wl.p, "s": wl.s,
+                   "micro_batch": MICRO_BATCH, "params": wl.params, "grad_dtype": wl.grad_dtype,
+                   "param_dtype": "bf16 (fp32 master, m, v)", "hierarchical_k": wl.hier_k,
+                   "grads": "resident in HBM (generated before timing)" if resident else "generated in-step (K6)",
+                   "l2": "inputs larger than L2 (gradient sets of %.2f GB/rank)" % (s * stats.grad_elems * szg / 1e9),
+                   "parallelism": f"MiCS p={wl.p} x {n // wl.p} replicas"},
+        "roofline": roof,
+        "phases_ms": {k: v[0] for k, v in phases.items()},
+        "per_rank_bytes": {"allgather_in": stats.ag_bytes_in, "reducescatter_in": stats.rs_bytes_in,
+                           "boundary_in": stats.ar_bytes_in, "adam_hbm": stats.adam_hbm_bytes},
+        "collective_GBps": {"allgather_bus": stats.ag_bytes_in * per / (prof["allgather_ms"] / 1e3) / 1e9,
+                            "reducescatter_bus": stats.rs_bytes_in * per / (prof["reducescatter_ms"] / 1e3) / 1e9},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "nccl_comparator": nccl,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    step.close()
+    eng.close()
+
+
+def main():
+    global GLOO
+    args = parse()
+    rank, world, local = env()
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group(backend="cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
+        GLOO = dist.new_group(backend="gloo")
+    from paper_2205_00119_b200.step import workloads
+    wl = workloads()[args.workload]
+    if args.sweep:
+        from tools.sweep import run_sweep
+        run_sweep(args, rank, world, local)
+    elif args.impl == "reference":
+        run_reference(args, wl, rank)
+    else:
+        run_mics(args, wl, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier(group=GLOO)
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -15,19 +15,19 @@ def env_world():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def exchange(obj, world: int):
-    """all_gather_object over the default process group."""
+def exchange(obj, world: int, group=None):
+    """all_gather_object over `group` (default: the default process group)."""
     import torch.distributed as dist
     out = [None] * world
-    dist.all_gather_object(out, obj)
+    dist.all_gather_object(out, obj, group=group)
     return out
 
 
-def connect(engine: Engine) -> None:
+def connect(engine: Engine, group=None) -> None:
     """Export this process's arena handle, import everybody's (world order)."""
     if engine.world == 1:
         return
-    handles = exchange(engine.export_handle(), engine.world)
+    handles = exchange(engine.export_handle(), engine.world, group)
     engine.import_handles(handles)
 
 

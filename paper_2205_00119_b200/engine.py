@@ -16,7 +16,7 @@ import numpy as np
 from ._lib import IPC_HANDLE_BYTES, Buf, InitArgs, check, lib
 
 DTYPE = {"i64": 0, "f32": 1, "f64": 2, "bf16": 3}
-NP_DTYPE = {"i64": np.int64, "f32": np.float32, "f64": np.float64, "bf16": np.uint16}
+NP_DTYPE = {"i64": np.int64, "f32": np.float32, "f64": np.float64, "bf16": np.uint16, "u8": np.uint8}
 DTYPE_SIZE = {"i64": 8, "f32": 4, "f64": 8, "bf16": 2}
 
 

@@ -1,0 +1,152 @@
+"""Multi-process worker for tests/test_multigpu.py (one process per GPU, torchrun).
+
+Every process builds the same job (n virtual ranks over `world` GPUs, node-major),
+maps the peers' arenas through CUDA IPC and runs the collectives across GPUs over
+NVLink; each process checks the ranks it hosts against the CPU oracle.
+Exit status 0 = every check passed.
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+
+    from oracle.oracle import Oracle
+    from paper_2205_00119_b200 import dist as mdist
+    from paper_2205_00119_b200.collectives import (all_gather_device, all_reduce_device,
+                                                   hierarchical_all_gather_device, reduce_scatter_device)
+    from paper_2205_00119_b200.engine import Engine
+    from paper_2205_00119_b200.sync_schedule import AdamConfig, SyncStates, make_adam
+    from paper_2205_00119_b200.topology import build_group_layout
+
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    n = int(os.environ.get("MICS_TEST_RANKS", 8))
+    ora = Oracle()
+    eng = Engine(n_ranks=n, world=world, world_rank=rank, device=local, arena_bytes=1 << 30)
+    mdist.connect(eng)
+    mine = eng.local_ranks
+    fails = []
+
+    def expect(cond, what):
+        if not cond:
+            fails.append(what)
+
+    # ---- partition-group all-gather, p in {2, 4, n}: groups span GPUs when p > n/world
+    for p in (2, 4, n):
+        chunk = (1 << 20) + 48
+        src, dst = eng.alloc(chunk), eng.alloc(p * chunk)
+        shards = ora.random_shards(n, chunk, 100 + p)
+        for r in mine:
+            eng.h2d(src, r, shards[r])
+        eng.barrier()
+        for g in range(n // p):
+            ranks = list(range(g * p, (g + 1) * p))
+            all_gather_device(eng, ranks, [eng.ptr(src, r) for r in ranks], chunk,
+                              [eng.ptr(dst, r) if r in mine else 0 for r in ranks])
+        eng.synchronize()
+        for r in mine:
+            g = r // p
+            expect(np.array_equal(eng.d2h(dst, r, p * chunk, "u8"),
+                                  shards[g * p:(g + 1) * p].ravel()), f"all_gather p={p} r={r}")
+
+    # ---- reduce-scatter f32 across GPUs, bit-exact
+    for p in (2, 4, n):
+        chunk = 300_007
+        src, dst = eng.alloc(4 * p * chunk), eng.alloc(4 * chunk)
+        bufs = np.stack([ora.random_f32(p * chunk, -1, 1, 7 * r + p) for r in range(n)])
+        for r in mine:
+            eng.h2d(src, r, bufs[r])
+        eng.barrier()
+        for g in range(n // p):
+            ranks = list(range(g * p, (g + 1) * p))
+            reduce_scatter_device(eng, ranks, [eng.ptr(src, r) for r in ranks], p * chunk,
+                                  [eng.ptr(dst, r) if r in mine else 0 for r in ranks], "f32")
+        eng.synchronize()
+        for r in mine:
+            g = r // p
+            want = ora.reduce_scatter(bufs[g * p:(g + 1) * p], "f32")[r % p]
+            expect(np.array_equal(eng.d2h(dst, r, chunk).view(np.uint32), want.view(np.uint32)), f"rs p={p} r={r}")
+
+    # ---- all-reduce in replication groups (stride p)
+    p = 2
+    elems = 4 * 65_537
+    buf = eng.alloc(4 * elems)
+    bufs = np.stack([ora.random_f32(elems, -1, 1, 900 + r) for r in range(n)])
+    for r in mine:
+        eng.h2d(buf, r, bufs[r])
+    eng.barrier()
+    for j in range(p):
+        ranks = list(range(j, n, p))
+        all_reduce_device(eng, ranks, [eng.ptr(buf, r) for r in ranks], elems, "f32")
+    eng.synchronize()
+    for r in mine:
+        ranks = list(range(r % p, n, p))
+        want = ora.all_reduce(bufs[ranks], "f32")[0]
+        expect(np.array_equal(eng.d2h(buf, r, elems).view(np.uint32), want.view(np.uint32)), f"all_reduce r={r}")
+
+    # ---- hierarchical all-gather (k ranks per virtual node), incl. the corrupt hook
+    for p, k, corrupt in ((n, n // 2, False), (4, 2, False), (n, 2, True)):
+        chunk = 65_536 + 16
+        src, dst = eng.alloc(chunk), eng.alloc(p * chunk)
+        shards = ora.random_shards(n, chunk, 55 + p + k)
+        for r in mine:
+            eng.h2d(src, r, shards[r])
+        eng.barrier()
+        hierarchical_all_gather_device(eng, p, k, [eng.ptr(src, r) for r in range(n)], chunk,
+                                       [eng.ptr(dst, r) for r in range(n)], corrupt)
+        eng.synchronize()
+        want = ora.hier_all_gather(shards, p, k, corrupt)
+        for r in mine:
+            expect(np.array_equal(eng.d2h(dst, r, p * chunk, "u8"), want[r]),
+                   f"hier p={p} k={k} corrupt={corrupt} r={r}")
+
+    # ---- 2-hop schedule + fused Adam across GPUs
+    for p in (2, 4):
+        s, length = 3, 200_003
+        lay = build_group_layout(n, p)
+        st = SyncStates(eng, lay, [length], s, "f32")
+        grads = ora.random_f32(s * n * length, -1, 1, 31 + p).reshape(s, n, length)
+        gb = eng.alloc(4 * st.grad_elems)
+        for t in range(s):
+            for r in mine:
+                eng.h2d(gb, r, grads[t, r])
+            eng.barrier()
+            st.micro_step_device(gb)
+            eng.synchronize()
+        c = st.shard_elems
+        pb, mb, vb = (eng.alloc(4 * c) for _ in range(3))
+        p0 = ora.random_f32(c, -1, 1, 3)
+        for r in mine:
+            eng.h2d(pb, r, p0)
+            eng.memset(mb, r, 4 * c)
+            eng.memset(vb, r, 4 * c)
+        eng.barrier()
+        st.boundary(make_adam(st, AdamConfig(lr=1e-3, grad_scale=0.5, write_grad=True), pb, mb, vb))
+        eng.synchronize()
+        want, _, _ = ora.two_hop(grads, n, p, "f32")
+        for r in mine:
+            expect(np.array_equal(st.shard(r).view(np.uint32), want[r].view(np.uint32)), f"two_hop p={p} r={r}")
+            wp, _, _, _ = ora.adam(p0, np.zeros(c), np.zeros(c), want[r], 1e-3, 0.9, 0.999, 1e-8, 0, 1, 0.5)
+            expect(np.array_equal(eng.d2h(pb, r, c).view(np.uint32), wp.view(np.uint32)), f"adam p={p} r={r}")
+        st.close()
+
+    eng.synchronize()
+    eng.close()
+    dist.barrier()
+    if fails:
+        print(f"[rank {rank}] FAILED: {fails}", flush=True)
+        sys.exit(1)
+    print(f"[rank {rank}] ok ({len(mine)} local ranks)", flush=True)
+
+
+if __name__ == "__main__":
+    main()
