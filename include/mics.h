@@ -190,6 +190,19 @@ mics_status mics_batched_all_gather(mics_ctx* ctx, const mics_ag_desc* descs, in
 mics_status mics_batched_reduce_scatter(mics_ctx* ctx, const mics_rs_desc* descs, int count, mics_dtype in_t,
                                         mics_dtype acc_t, double scale, mics_rs_mode mode);
 
+/* Persistent (replayable) collectives: the descriptor table is built and uploaded
+ * once; mics_plan_run enqueues the same kernel `iterations` times (hot loops, the
+ * step driver, CUDA-graph capture).  Same semantics and barriers as the one-shot
+ * calls; traffic is not logged per run. */
+typedef struct mics_plan mics_plan;
+mics_status mics_plan_all_gather(mics_ctx* ctx, const int* ranks, int p, const void* const* d_shard,
+                                 uint64_t chunk_bytes, void* const* d_out, mics_plan** out);
+mics_status mics_plan_reduce_scatter(mics_ctx* ctx, const int* ranks, int p, const void* const* d_in,
+                                     uint64_t in_elems, uint64_t valid_elems, mics_dtype in_t, mics_dtype acc_t,
+                                     double scale, mics_rs_mode mode, void* const* d_out, mics_plan** out);
+mics_status mics_plan_run(mics_ctx* ctx, mics_plan* plan, int iterations);
+mics_status mics_plan_destroy(mics_plan* plan);
+
 /* ---------------------------------------------------------------- host-buffer drop-ins
  * Same signatures as the reference's by-value API (collectives.hpp:64-112) over
  * host memory: H2D, kernel, D2H.  Single-process contexts (world == 1) only. */

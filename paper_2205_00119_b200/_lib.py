@@ -118,6 +118,10 @@ _SIGS = [
     ("mics_hier_all_gather", I, [VP, I, I, PVP, U64, PVP, I]),
     ("mics_batched_all_gather", I, [VP, C.POINTER(AgDesc), I]),
     ("mics_batched_reduce_scatter", I, [VP, C.POINTER(RsDesc), I, I, I, D, I]),
+    ("mics_plan_all_gather", I, [VP, PI, I, PVP, U64, PVP, C.POINTER(VP)]),
+    ("mics_plan_reduce_scatter", I, [VP, PI, I, PVP, U64, U64, I, I, D, I, PVP, C.POINTER(VP)]),
+    ("mics_plan_run", I, [VP, VP, I]),
+    ("mics_plan_destroy", I, [VP]),
     ("mics_host_all_gather", I, [VP, PI, I, PVP, U64, PVP]),
     ("mics_host_reduce_scatter", I, [VP, PI, I, PVP, U64, I, PVP]),
     ("mics_host_all_reduce", I, [VP, PI, I, PVP, U64, I, PVP]),

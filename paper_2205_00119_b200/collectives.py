@@ -229,7 +229,47 @@ def batched_reduce_scatter_device(engine: Engine, descs, in_dtype: str = "f32", 
                                           mode))
 
 
-__all__ = ["CollectiveGroup", "all_gather", "reduce_scatter", "all_reduce", "hierarchical_all_gather",
+class Plan:
+    """A persistent collective (descriptor table uploaded once; ``run`` replays it)."""
+
+    def __init__(self, engine: Engine, handle):
+        self.engine = engine
+        self.h = handle
+
+    def run(self, iterations: int = 1) -> None:
+        check(lib.mics_plan_run(self.engine.ctx, self.h, iterations))
+
+    def close(self) -> None:
+        if self.h:
+            check(lib.mics_plan_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def plan_all_gather(engine: Engine, ranks, shard_ptrs, chunk_bytes: int, out_ptrs) -> Plan:
+    h = C.c_void_p()
+    check(lib.mics_plan_all_gather(engine.ctx, _ints(ranks), len(ranks), _ptrs(shard_ptrs), chunk_bytes,
+                                   _ptrs(out_ptrs), C.byref(h)))
+    return Plan(engine, h)
+
+
+def plan_reduce_scatter(engine: Engine, ranks, in_ptrs, in_elems: int, out_ptrs, in_dtype: str = "f32",
+                        acc_dtype: str | None = None, scale: float = 1.0, mode: int = RS_STORE,
+                        valid_elems: int | None = None) -> Plan:
+    acc = acc_dtype or ("f32" if in_dtype == "bf16" else in_dtype)
+    h = C.c_void_p()
+    check(lib.mics_plan_reduce_scatter(engine.ctx, _ints(ranks), len(ranks), _ptrs(in_ptrs), in_elems,
+                                       in_elems if valid_elems is None else valid_elems, dtype_code(in_dtype),
+                                       dtype_code(acc), scale, mode, _ptrs(out_ptrs), C.byref(h)))
+    return Plan(engine, h)
+
+
+__all__ = ["Plan", "plan_all_gather", "plan_reduce_scatter","CollectiveGroup", "all_gather", "reduce_scatter", "all_reduce", "hierarchical_all_gather",
            "batched_all_gather", "batched_reduce_scatter", "all_gather_device", "reduce_scatter_device",
            "all_reduce_device", "hierarchical_all_gather_device", "batched_all_gather_device",
            "batched_reduce_scatter_device", "RS_STORE", "RS_ACCUMULATE", "RS_ZERO_ACCUM", "DTYPE_SIZE"]

@@ -38,6 +38,9 @@ void host_batched_all_gather(mics_ctx*, int, const int*, const int*, const uint6
                              void* const*);
 void host_batched_reduce_scatter(mics_ctx*, int, const int*, const int*, const uint64_t*, const void* const*,
                                  mics_dtype, void* const*);
+Launch build_all_gather(mics_ctx*, const int*, int, const void* const*, uint64_t, void* const*, bool);
+Launch build_reduce_scatter(mics_ctx*, const int*, int, const void* const*, uint64_t, uint64_t, mics_dtype,
+                            mics_dtype, double, int, void* const*, bool);
 // step.cpp
 mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg);
 void step_destroy(mics_step* st);
@@ -46,8 +49,29 @@ void step_profile(mics_step* st, double* ag_ms, double* rs_ms, double* bnd_ms, d
 void step_run_host(mics_step* st, const void* host_grads, int iters, void* host_result);
 }  // namespace mics
 
+struct mics_plan {
+  std::vector<mics::Launch> launches;
+};
+
 namespace {
 thread_local std::string g_last_error;
+
+// build a persistent launch without logging traffic (a plan is not a transfer)
+template <typename F>
+mics_plan* make_plan(mics_ctx* ctx, F&& build) {
+  const bool was = ctx->traffic_on;
+  ctx->traffic_on = false;
+  auto* p = new mics_plan();
+  try {
+    p->launches.push_back(build());
+  } catch (...) {
+    ctx->traffic_on = was;
+    delete p;
+    throw;
+  }
+  ctx->traffic_on = was;
+  return p;
+}
 
 template <typename F>
 mics_status guard(F&& f) {
@@ -334,6 +358,41 @@ mics_status mics_batched_reduce_scatter(mics_ctx* ctx, const mics_rs_desc* d, in
   return guard([&] {
     need(ctx, "ctx");
     mics::batched_reduce_scatter(ctx, d, count, in_t, acc_t, scale, int(mode));
+  });
+}
+mics_status mics_plan_all_gather(mics_ctx* ctx, const int* ranks, int p, const void* const* d_shard, uint64_t chunk,
+                                 void* const* d_out, mics_plan** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "output");
+    *out = make_plan(ctx, [&] { return mics::build_all_gather(ctx, ranks, p, d_shard, chunk, d_out, true); });
+  });
+}
+mics_status mics_plan_reduce_scatter(mics_ctx* ctx, const int* ranks, int p, const void* const* d_in,
+                                     uint64_t in_elems, uint64_t valid, mics_dtype in_t, mics_dtype acc_t,
+                                     double scale, mics_rs_mode mode, void* const* d_out, mics_plan** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "output");
+    *out = make_plan(ctx, [&] {
+      return mics::build_reduce_scatter(ctx, ranks, p, d_in, in_elems, valid, in_t, acc_t, scale, int(mode), d_out,
+                                        true);
+    });
+  });
+}
+mics_status mics_plan_run(mics_ctx* ctx, mics_plan* plan, int iterations) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(plan, "plan");
+    for (int i = 0; i < iterations; ++i)
+      for (const auto& l : plan->launches) mics::enqueue(ctx, l);
+  });
+}
+mics_status mics_plan_destroy(mics_plan* plan) {
+  return guard([&] {
+    if (!plan) return;
+    for (auto& l : plan->launches) l.release();
+    delete plan;
   });
 }
 mics_status mics_host_all_gather(mics_ctx* ctx, const int* ranks, int p, const void* const* shards, uint64_t chunk,

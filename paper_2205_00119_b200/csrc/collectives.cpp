@@ -230,20 +230,26 @@ void plan_reduce_scatter(mics_ctx* ctx, RedPlan& plan, const int* ranks, int p, 
 
 }  // namespace
 
-void all_gather(mics_ctx* ctx, const int* ranks, int p, const void* const* shard, uint64_t chunk, void* const* out) {
+Launch build_all_gather(mics_ctx* ctx, const int* ranks, int p, const void* const* shard, uint64_t chunk,
+                        void* const* out, bool persistent) {
   check_group(ctx, ranks, p);
   check_ptrs(shard, p, ctx, ranks, false, "all_gather input");
   check_ptrs(const_cast<const void* const*>(out), p, ctx, ranks, true, "all_gather output");
   CopyPlan plan;
   plan_all_gather(ctx, plan, ranks, p, shard, chunk, out);
-  enqueue(ctx, make_copy_launch(ctx, plan, ctx->barrier(ctx->peer_mask(ranks, p), 1, 1), false));
+  return make_copy_launch(ctx, plan, ctx->barrier(ctx->peer_mask(ranks, p), 1, 1), persistent);
 }
 
-void reduce_scatter(mics_ctx* ctx, const int* ranks, int p, const void* const* in, uint64_t in_elems,
-                    uint64_t valid, mics_dtype in_t, mics_dtype acc_t, double scale, int mode, void* const* out) {
+void all_gather(mics_ctx* ctx, const int* ranks, int p, const void* const* shard, uint64_t chunk, void* const* out) {
+  enqueue(ctx, build_all_gather(ctx, ranks, p, shard, chunk, out, false));
+}
+
+Launch build_reduce_scatter(mics_ctx* ctx, const int* ranks, int p, const void* const* in, uint64_t in_elems,
+                            uint64_t valid, mics_dtype in_t, mics_dtype acc_t, double scale, int mode,
+                            void* const* out, bool persistent) {
   check_group(ctx, ranks, p);
   check_rs_types(in_t, acc_t);
-  if (p == 0) return;
+  if (p == 0) return Launch{};
   if (in_elems % uint64_t(p))
     raise(MICS_TYPE_MISMATCH, "reduce_scatter: " + std::to_string(in_elems) + " elements are not divisible into " +
                                   std::to_string(p) + " chunks");  // collectives.cpp:148-153
@@ -252,8 +258,13 @@ void reduce_scatter(mics_ctx* ctx, const int* ranks, int p, const void* const* i
   check_ptrs(const_cast<const void* const*>(out), p, ctx, ranks, true, "reduce_scatter output");
   RedPlan plan(in_t);
   plan_reduce_scatter(ctx, plan, ranks, p, in, in_elems, valid, in_t, out);
-  enqueue(ctx, make_reduce_launch(ctx, plan, in_t, acc_t, scale, mode,
-                                  ctx->barrier(ctx->peer_mask(ranks, p), 1, 1), false));
+  return make_reduce_launch(ctx, plan, in_t, acc_t, scale, mode, ctx->barrier(ctx->peer_mask(ranks, p), 1, 1),
+                            persistent);
+}
+
+void reduce_scatter(mics_ctx* ctx, const int* ranks, int p, const void* const* in, uint64_t in_elems,
+                    uint64_t valid, mics_dtype in_t, mics_dtype acc_t, double scale, int mode, void* const* out) {
+  enqueue(ctx, build_reduce_scatter(ctx, ranks, p, in, in_elems, valid, in_t, acc_t, scale, mode, out, false));
 }
 
 void all_reduce(mics_ctx* ctx, const int* ranks, int p, void* const* buf, uint64_t elems, mics_dtype dt) {

@@ -1,0 +1,106 @@
+"""C2 (BASELINE.json configs[1]): partition-group all-gather + reduce-scatter sweep,
+1 MiB..1 GiB gathered bytes per rank, p in {2,4,8} (<= GPUs), one rank per GPU, all
+n/p groups concurrent — libmics (persistent plans) vs NCCL on split communicators.
+
+    torchrun --nproc-per-node N bench.py --gpus N --sweep [--steps K]
+
+busBW = (p-1) * M / p / t per rank; one JSON line per point, times are
+CUDA-event medians, max over ranks.
+"""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+
+NVLINK = 770.0
+
+
+def _time(fn, stream_ext, reps, world, gloo):
+    import torch
+    import torch.distributed as dist
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream_ext)
+        fn()
+        e1.record(stream_ext)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    t = statistics.median(ts)
+    if world > 1:
+        x = torch.tensor([t], dtype=torch.float64)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX, group=gloo)
+        t = float(x.item())
+    return t * 1e3  # us
+
+
+def run_sweep(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import bench
+    from paper_2205_00119_b200 import dist as mdist
+    from paper_2205_00119_b200.collectives import RS_STORE, plan_all_gather, plan_reduce_scatter
+    from paper_2205_00119_b200.engine import Engine
+
+    gloo = bench.GLOO
+    maxlog = int(os.environ.get("MICS_SWEEP_MAXLOG", 30))
+    sizes = [1 << e for e in range(20, maxlog + 1)]
+    M = sizes[-1]
+    eng = Engine(n_ranks=world, world=world, world_rank=rank, device=local, arena_bytes=3 * M + (64 << 20))
+    mdist.connect(eng, gloo)
+    src, dst = eng.alloc(M), eng.alloc(M)
+    eng.generate(src, rank, M // 4, "f32", seed=rank)
+    eng.synchronize()
+    ext = torch.cuda.ExternalStream(eng.stream())
+    dev = torch.device("cuda", local)
+    t_in = torch.randn(M // 4, device=dev)
+    t_out = torch.empty(M // 4, device=dev)
+    results = []
+    for p in (2, 4, 8):
+        if p > world or world % p:
+            continue
+        g = rank // p
+        ranks = list(range(g * p, (g + 1) * p))
+        groups = [dist.new_group(list(range(h * p, (h + 1) * p))) for h in range(world // p)] if world > 1 else []
+        pg = groups[g] if groups else None
+        for m in sizes:
+            reps = 20 if m <= (64 << 20) else 5
+            chunk = m // p
+            ag = plan_all_gather(eng, ranks, [eng.ptr(src, r) for r in ranks], chunk, [eng.ptr(dst, r) for r in ranks])
+            rs = plan_reduce_scatter(eng, ranks, [eng.ptr(src, r) for r in ranks], m // 4,
+                                     [eng.ptr(dst, r) for r in ranks], "f32", mode=RS_STORE)
+            for plan, op in ((ag, "allgather"), (rs, "reducescatter")):
+                plan.run(3)
+                eng.synchronize()
+                bench.barrier(world)
+                us = _time(lambda: plan.run(1), ext, reps, world, gloo)
+                if pg is not None:
+                    a_in, a_out = t_in.view(torch.uint8)[:chunk], t_out.view(torch.uint8)[:m]
+                    r_in, r_out = t_in[:m // 4], t_out[:m // 4 // p]
+                    nccl = (lambda: dist.all_gather_into_tensor(a_out, a_in, group=pg)) if op == "allgather" else \
+                        (lambda: dist.reduce_scatter_tensor(r_out, r_in, group=pg))
+                    for _ in range(3):
+                        nccl()
+                    torch.cuda.synchronize()
+                    bench.barrier(world)
+                    nus = _time(nccl, torch.cuda.current_stream(), reps, world, gloo)
+                else:
+                    nus = None
+                bus = (p - 1) * m / p / (us * 1e-6) / 1e9
+                line = {"sweep": "C2", "op": op, "p": p, "gpus": world, "bytes": m, "mics_us": us,
+                        "mics_busbw_GBps": bus, "frac_nvlink_770": bus / NVLINK,
+                        "nccl_us": nus, "nccl_busbw_GBps": (p - 1) * m / p / (nus * 1e-6) / 1e9 if nus else None}
+                results.append(line)
+                if rank == 0:
+                    print(json.dumps(line), flush=True)
+            ag.close()
+            rs.close()
+    if rank == 0 and results:
+        big = [r for r in results if r["bytes"] >= (256 << 20)]
+        wins = sum(1 for r in results if r["nccl_us"] and r["mics_us"] < r["nccl_us"])
+        print(json.dumps({"sweep_summary": "C2", "points": len(results), "beats_nccl": wins,
+                          "min_frac_nvlink_>=256MiB": min(r["frac_nvlink_770"] for r in big) if big else None}),
+              flush=True)
+    eng.close()
