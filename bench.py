@@ -363,7 +363,7 @@ def run_mics(args, wl, rank, world, local):
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
         gbytes = stats.grad_elems * szg
-        host, hptr = host_alloc(s * gbytes)
+        host, hptr = host_alloc(gbytes)  # one gradient set, copied for every local rank and micro-step
         res, rptr = host_alloc(per * 4096 * 4)
         import numpy as np
         pat = np.random.default_rng(rank).standard_normal(1 << 22).astype(

@@ -322,7 +322,7 @@ mics_status mics_step_buffers(mics_step* st, mics_buf* param_bf16, mics_buf* mas
 mics_status mics_step_profile(mics_ctx* ctx, mics_step* st, double* ag_ms, double* rs_ms, double* boundary_ms,
                               double* gen_ms);
 /* e2e variant: gradients come from pinned HOST memory every micro-step (H2D in the step) */
-mics_status mics_step_run_host(mics_ctx* ctx, mics_step* st, const void* host_grads /* per local rank: s * grad_elems */,
+mics_status mics_step_run_host(mics_ctx* ctx, mics_step* st, const void* host_grads /* grad_elems, reused per rank/micro-step */,
                                int iterations, void* host_result /* per local rank: shard fp32, or NULL */);
 
 #ifdef __cplusplus

@@ -30,9 +30,24 @@ void CopyPlan::add(const void* src, const std::vector<void*>& dsts, uint64_t byt
     s.ndst = uint32_t(std::min<size_t>(kMaxDst, dsts.size() - b));
     for (uint32_t d = 0; d < s.ndst; ++d) s.dst[d] = static_cast<uint8_t*>(dsts[b + d]);
     s.tile0 = tiles;
+    s.gsize = 1;
     tiles += uint32_t(ceil_div(bytes, kCopyTile));
     segs.push_back(s);
   }
+}
+
+void CopyPlan::add_group(const std::vector<std::pair<const void*, std::vector<void*>>>& items, uint64_t bytes) {
+  if (bytes == 0) return;
+  const size_t first = segs.size();
+  const uint32_t t0 = tiles;
+  for (const auto& it : items) add(it.first, it.second, bytes);
+  const uint32_t k = uint32_t(segs.size() - first);
+  if (k <= 1) return;
+  for (size_t i = first; i < segs.size(); ++i) {  // one interleaved tile range for the whole group
+    segs[i].tile0 = t0;
+    segs[i].gsize = k;
+  }
+  tiles = t0 + k * uint32_t(ceil_div(bytes, kCopyTile));
 }
 
 void RedPlan::add(const std::vector<const void*>& src, void* dst, uint64_t elems, uint64_t valid) {
@@ -44,6 +59,7 @@ void RedPlan::add(const std::vector<const void*>& src, void* dst, uint64_t elems
   j.valid = std::min(valid, elems);
   j.p = uint32_t(src.size());
   j.tile0 = tiles;
+  max_p = std::max(max_p, j.p);
   uintptr_t a = reinterpret_cast<uintptr_t>(dst);
   for (const void* s : src) a |= reinterpret_cast<uintptr_t>(s);
   j.aligned = (a & 15) == 0;
@@ -93,11 +109,12 @@ void table_upload(mics_ctx* ctx, void* d, const void* h, uint64_t bytes, bool pe
 // jobs followed by their source-pointer arrays, pointers patched to device addresses
 template <typename Job>
 void* upload_jobs(mics_ctx* ctx, std::vector<Job> jobs, const std::vector<std::vector<const void*>>& srcs,
-                  bool persistent) {
+                  bool persistent, uint64_t* table_bytes = nullptr) {
   uint64_t nptr = 0;
   for (const auto& s : srcs) nptr += s.size();
   const uint64_t jbytes = round_up(sizeof(Job) * jobs.size(), 16);
-  const uint64_t bytes = jbytes + nptr * sizeof(void*);
+  const uint64_t bytes = round_up(jbytes + nptr * sizeof(void*), 16);
+  if (table_bytes) *table_bytes = bytes;
   char* d = static_cast<char*>(table_memory(ctx, bytes, persistent));
   std::vector<char> blob(bytes);
   const void** ptrs = reinterpret_cast<const void**>(blob.data() + jbytes);
@@ -118,7 +135,7 @@ Launch make_copy_launch(mics_ctx* ctx, const CopyPlan& plan, const BarrierArg& b
   l.kind = Launch::COPY;
   l.ndesc = int(plan.segs.size());
   l.ntiles = plan.tiles;
-  l.grid = ctx->grid_for(plan.tiles);
+  l.grid = ctx->grid_for(plan.tiles, ctx->occ_copy);
   l.bar = bar;
   if (l.ndesc) {
     const uint64_t bytes = sizeof(CopySeg) * plan.segs.size();
@@ -134,13 +151,14 @@ Launch make_reduce_launch(mics_ctx* ctx, const RedPlan& plan, mics_dtype in_t, m
   l.kind = Launch::REDUCE;
   l.ndesc = int(plan.jobs.size());
   l.ntiles = plan.tiles;
-  l.grid = ctx->grid_for(plan.tiles);
+  l.grid = ctx->grid_for(plan.tiles, ctx->reduce_occ(in_t, plan.max_p));
+  l.max_p = plan.max_p;
   l.in_t = in_t;
   l.acc_t = acc_t;
   l.scale = scale;
   l.mode = mode;
   l.bar = bar;
-  if (l.ndesc) l.d_desc = upload_jobs(ctx, plan.jobs, plan.srcs, persistent);
+  if (l.ndesc) l.d_desc = upload_jobs(ctx, plan.jobs, plan.srcs, persistent, &l.table_bytes);
   return l;
 }
 
@@ -150,30 +168,33 @@ Launch make_adam_launch(mics_ctx* ctx, const AdamPlan& plan, const AdamScalars& 
   l.kind = Launch::ADAM;
   l.ndesc = int(plan.jobs.size());
   l.ntiles = plan.tiles;
-  l.grid = ctx->grid_for(plan.tiles);
+  l.grid = ctx->grid_for(plan.tiles, ctx->occ_adam);
   l.adam = sc;
   l.bar = bar;
   if (l.ndesc) l.d_desc = upload_jobs(ctx, plan.jobs, plan.srcs, persistent);
   return l;
 }
 
-void enqueue(mics_ctx* ctx, const Launch& l) {
+void enqueue(mics_ctx* ctx, const Launch& l, int dep_first) {
   // A launch without local work still runs (one CTA) when it carries a barrier:
   // the peers count on this process's signals.
   if (l.ndesc == 0 && l.bar.mask == 0) return;
+  BarrierArg bar = l.bar;
+  if (dep_first >= 0) bar.dep_first = dep_first;
+  if (bar.mask) bar.dep_first = 1;  // barrier tickets: never overlap the predecessor
   switch (l.kind) {
     case Launch::COPY:
-      launch_copy(ctx->stream, static_cast<const CopySeg*>(l.d_desc), l.ndesc, l.ntiles, l.grid, l.bar);
+      launch_copy(ctx->stream, static_cast<const CopySeg*>(l.d_desc), l.ndesc, l.ntiles, l.grid, bar);
       break;
     case Launch::REDUCE:
-      launch_reduce(ctx->stream, l.in_t, l.acc_t, static_cast<const RedJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid,
-                    l.scale, l.mode, l.bar);
+      launch_reduce(ctx->stream, l.in_t, l.acc_t, static_cast<const RedJob*>(l.d_desc), l.ndesc, l.table_bytes,
+                    l.max_p, l.ntiles, l.grid, l.scale, l.mode, bar);
       break;
     case Launch::ADAM:
-      launch_adam(ctx->stream, static_cast<const AdamJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid, l.adam, l.bar);
+      launch_adam(ctx->stream, static_cast<const AdamJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid, l.adam, bar);
       break;
     case Launch::BARRIER:
-      launch_barrier(ctx->stream, l.bar);
+      launch_barrier(ctx->stream, bar);
       break;
   }
   ctx->launches++;
@@ -205,11 +226,15 @@ void plan_all_gather(mics_ctx* ctx, CopyPlan& plan, const int* ranks, int p, con
   for (int j = 0; j < p; ++j)
     if (ctx->local(ranks[j])) loc.push_back(j);
   if (loc.empty()) return;
-  for (int i = 0; i < p; ++i) {  // one read of chunk i feeds every local destination
+  // one read of chunk i feeds every local destination; the p chunks form one
+  // stripe group so all sources (NVLink peers and local HBM) stream concurrently
+  std::vector<std::pair<const void*, std::vector<void*>>> items;
+  for (int i = 0; i < p; ++i) {
     std::vector<void*> dsts;
     for (int j : loc) dsts.push_back(static_cast<char*>(out[j]) + uint64_t(i) * chunk);
-    plan.add(shard[i], dsts, chunk);
+    items.emplace_back(shard[i], std::move(dsts));
   }
+  plan.add_group(items, chunk);
 }
 
 void plan_reduce_scatter(mics_ctx* ctx, RedPlan& plan, const int* ranks, int p, const void* const* in,
@@ -294,12 +319,14 @@ void all_reduce(mics_ctx* ctx, const int* ranks, int p, void* const* buf, uint64
   for (int i = 0; i < p; ++i)
     for (int j = 0; j < p; ++j)
       if (j != i) ctx->record(ranks[i], ranks[j], cb);
+  std::vector<std::pair<const void*, std::vector<void*>>> items;
   for (int i = 0; i < p; ++i) {
     std::vector<void*> dsts;
     for (int j = 0; j < p; ++j)
       if (j != i && ctx->local(ranks[j])) dsts.push_back(static_cast<char*>(buf[j]) + uint64_t(i) * cb);
-    ag.add(static_cast<const char*>(buf[i]) + uint64_t(i) * cb, dsts, cb);
+    if (!dsts.empty()) items.emplace_back(static_cast<const char*>(buf[i]) + uint64_t(i) * cb, std::move(dsts));
   }
+  ag.add_group(items, cb);
   enqueue(ctx, make_copy_launch(ctx, ag, ctx->barrier(mask, 0, 1), false));
 }
 
@@ -361,18 +388,21 @@ void hier_all_gather(mics_ctx* ctx, int n, int p, int k, const void* const* shar
       for (int j = 0; j < k; ++j) {
         const int r = base + m * k + j;
         if (!ctx->local(r)) continue;
+        std::vector<std::pair<const void*, std::vector<void*>>> g1, g2;
         for (int m2 = 0; m2 < q; ++m2) {  // phase 1: channel j
           const uint64_t pos = corrupt ? uint64_t(j) * q + m2 : uint64_t(m2) * k + j;
-          ph1.add(shard[base + m2 * k + j], {O(r, pos)}, chunk);
+          g1.push_back({shard[base + m2 * k + j], {O(r, pos)}});
         }
         for (int j2 = 0; j2 < k; ++j2) {  // phase 2: node peers
           if (j2 == j) continue;
           const int src = base + m * k + j2;
           for (int t = 0; t < q; ++t) {
             const uint64_t pos = corrupt ? uint64_t(j2) * q + t : uint64_t(t) * k + j2;
-            ph2.add(O(src, pos), {O(r, pos)}, chunk);
+            g2.push_back({O(src, pos), {O(r, pos)}});
           }
         }
+        ph1.add_group(g1, chunk);
+        ph2.add_group(g2, chunk);
       }
     }
   }

@@ -40,18 +40,22 @@ inline uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }
 // device descriptors (shared by host planners and kernels)
 constexpr int kMaxDst = 4;       // destinations written from one source read
 constexpr int kThreads = 256;    // threads per CTA for every data kernel
-constexpr int kCopyUnroll = 4;   // 16 B vectors in flight per thread per tile
-constexpr uint32_t kCopyTile = kThreads * kCopyUnroll * 16;  // 16 KiB
-constexpr int kRedUnroll = 2;    // vectors per thread per tile (per source)
+constexpr int kCopyUnroll = 8;   // 16 B vectors in flight per thread per tile
+constexpr uint32_t kCopyTile = kThreads * kCopyUnroll * 16;  // 32 KiB
+constexpr int kRedUnroll = 4;    // vectors per thread per tile (per source)
 constexpr int kAdamUnroll = 2;
+constexpr int kSmemTable = 16384;  // descriptor tables up to this size are staged in shared memory
 
 struct CopySeg {              // 64 B
   const uint8_t* src;
   uint8_t* dst[kMaxDst];
   uint64_t bytes;
   uint32_t ndst;
-  uint32_t tile0;             // first global tile index of this segment
+  uint32_t tile0;             // first tile of this segment's stripe group
+  uint32_t gsize;             // segments in the stripe group (equal sizes, tiles interleaved)
+  uint32_t pad_;
 };
+static_assert(sizeof(CopySeg) == 64, "CopySeg layout");
 
 struct RedJob {               // one output chunk (one destination rank, one segment)
   const uint8_t* const* srcs; // p source pointers, already offset to this chunk
@@ -96,14 +100,23 @@ struct BarrierArg {
   uint64_t mask;              // peers taking part (bit w = process w), never includes self
   int entry;                  // signal + wait before any data access
   int exit;                   // last CTA signals + waits after all data access
+  // Programmatic dependent launch: 1 = griddepcontrol.wait before touching memory
+  // (the kernel consumes its predecessor's results); 0 = independent of the
+  // predecessor (barrier-free all-gathers of static shards): it waits only at its
+  // end, so completion order — and every transitive dependency — is preserved.
+  int dep_first;
 };
 
 // --------------------------------------------------------------------------
 // kernel launchers (kernels.cu)
 void launch_copy(cudaStream_t s, const CopySeg* segs, int nseg, uint32_t ntiles, int grid, const BarrierArg& bar);
-void launch_reduce(cudaStream_t s, mics_dtype in_t, mics_dtype acc_t, const RedJob* jobs, int njobs, uint32_t ntiles,
-                   int grid, double scale, int mode, const BarrierArg& bar);
+// `table_bytes`: size of the uploaded job table + source-pointer arrays (staged in smem when small)
+void launch_reduce(cudaStream_t s, mics_dtype in_t, mics_dtype acc_t, const RedJob* jobs, int njobs,
+                   uint64_t table_bytes, uint32_t max_p, uint32_t ntiles, int grid, double scale, int mode,
+                   const BarrierArg& bar);
 uint32_t reduce_tile_elems(mics_dtype in_t);
+int reduce_class(uint32_t max_p);  // 2, 4, 8 or 9 (> 8 sources)
+int resident_ctas(int kind /* 0 copy, 1 reduce, 2 adam */, mics_dtype in_t, int pclass = 2);
 void launch_adam(cudaStream_t s, const AdamJob* jobs, int njobs, uint32_t ntiles, int grid, const AdamScalars& sc,
                  const BarrierArg& bar);
 constexpr uint32_t kAdamTile = kThreads * kAdamUnroll * 4;
@@ -121,6 +134,12 @@ AdamScalars make_adam_scalars(double lr, double b1, double b2, double eps, doubl
 struct mics_ctx {
   int n = 0, world = 1, wrank = 0, per = 0, device = 0, nsm = 148;
   int blocks_per_sm = 4;
+  // resident CTAs/SM per kernel: copy, adam, reduce by [input dtype][source class 2/4/8/9]
+  int occ_copy = 2, occ_adam = 4, occ_reduce[4][4] = {};
+  int reduce_occ(mics_dtype t, uint32_t max_p) const {
+    const int pc = mics::reduce_class(max_p);
+    return occ_reduce[t][pc == 2 ? 0 : pc == 4 ? 1 : pc == 8 ? 2 : 3];
+  }
   cudaStream_t stream = nullptr;
   char* base = nullptr;           // local arena (IPC-exportable)
   uint64_t cap = 0, used = 0;
@@ -146,8 +165,8 @@ struct mics_ctx {
     if (world > 1 && !local(to)) return;
     traffic[{from, to}] += bytes;
   }
-  int grid_for(uint64_t tiles) const {
-    uint64_t g = uint64_t(nsm) * blocks_per_sm;
+  int grid_for(uint64_t tiles, int per_sm = 0) const {
+    uint64_t g = uint64_t(nsm) * (per_sm ? per_sm : blocks_per_sm);
     if (tiles < g) g = tiles;
     return g ? int(g) : 1;
   }
@@ -163,6 +182,7 @@ struct mics_ctx {
     b.mask = ipc_ready ? mask : 0;
     b.entry = entry;
     b.exit = exit;
+    b.dep_first = 1;
     return b;
   }
   // processes hosting any of `ranks`, minus self (0 when self hosts none)
@@ -176,12 +196,17 @@ struct CopyPlan {
   std::vector<CopySeg> segs;
   uint32_t tiles = 0;
   void add(const void* src, const std::vector<void*>& dsts, uint64_t bytes);
+  // A stripe group: equal-size copies whose tiles are interleaved (tile t of the
+  // group belongs to copy t mod k), so every source — local HBM and each NVLink
+  // peer — is read concurrently instead of one after the other.
+  void add_group(const std::vector<std::pair<const void*, std::vector<void*>>>& items, uint64_t bytes);
 };
 struct RedPlan {
   std::vector<RedJob> jobs;
   std::vector<std::vector<const void*>> srcs;  // per job
   uint32_t tiles = 0;
   uint32_t tile_elems = 0;
+  uint32_t max_p = 1;
   explicit RedPlan(mics_dtype in_t) : tile_elems(reduce_tile_elems(in_t)) {}
   void add(const std::vector<const void*>& src, void* dst, uint64_t elems, uint64_t valid);
 };
@@ -197,6 +222,8 @@ struct AdamPlan {
 struct Launch {
   enum Kind { COPY, REDUCE, ADAM, BARRIER } kind = COPY;
   void* d_desc = nullptr;  // owned device table (cudaMalloc)
+  uint64_t table_bytes = 0;
+  uint32_t max_p = 1;
   int ndesc = 0;
   uint32_t ntiles = 0;
   int grid = 1;
@@ -212,7 +239,8 @@ Launch make_reduce_launch(mics_ctx* ctx, const RedPlan& plan, mics_dtype in_t, m
                           const BarrierArg& bar, bool persistent);
 Launch make_adam_launch(mics_ctx* ctx, const AdamPlan& plan, const AdamScalars& sc, const BarrierArg& bar,
                         bool persistent);
-void enqueue(mics_ctx* ctx, const Launch& l);
+// dep_first: -1 = as planned, 0/1 = override BarrierArg::dep_first for this launch
+void enqueue(mics_ctx* ctx, const Launch& l, int dep_first = -1);
 
 void check_group(const mics_ctx* ctx, const int* ranks, int p);
 }  // namespace mics

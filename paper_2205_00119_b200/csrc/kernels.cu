@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -44,6 +45,19 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
 }
 __device__ __forceinline__ uint4 ld_plain(const void* p) { return *reinterpret_cast<const uint4*>(p); }
 __device__ __forceinline__ void st_vec(void* p, const uint4& v) { *reinterpret_cast<uint4*>(p) = v; }
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every data kernel lets its successor be scheduled immediately (its prologue and
+// descriptor staging overlap this kernel's tail).  A kernel that consumes its
+// predecessor's results waits for it up front; an independent one waits only
+// before exiting, which keeps completion in stream order.
+__device__ __forceinline__ void pdl_begin(const BarrierArg& b) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (b.dep_first) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_end(const BarrierArg& b) {
+  if (!b.dep_first) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 
 // ---------------------------------------------------------------- barrier
 __device__ void bar_entry(const BarrierArg& b) {
@@ -108,19 +122,38 @@ __device__ __forceinline__ int find_desc(const T* __restrict__ d, int n, uint32_
 }
 
 // ---------------------------------------------------------------- K1: copy engine
-__global__ void __launch_bounds__(kThreads) k_copy(const CopySeg* __restrict__ segs, int nseg, uint32_t ntiles,
-                                                   BarrierArg bar) {
+__global__ void __launch_bounds__(kThreads) k_copy(const CopySeg* __restrict__ gsegs, int nseg, uint32_t table_bytes,
+                                                   uint32_t ntiles, BarrierArg bar) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const bool staged = table_bytes != 0;  // stage the segment table: the per-tile lookup stays on-chip
+  if (staged) {
+    const uint4* s = reinterpret_cast<const uint4*>(gsegs);
+    uint4* d = reinterpret_cast<uint4*>(smem);
+    for (uint32_t i = threadIdx.x; i < table_bytes / 16; i += kThreads) d[i] = s[i];
+  }
+  __syncthreads();
+  const CopySeg* segs = staged ? reinterpret_cast<const CopySeg*>(smem) : gsegs;
+  pdl_begin(bar);
   bar_entry(bar);
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const CopySeg s = segs[find_desc(segs, nseg, tile)];
-    const uint64_t off = uint64_t(tile - s.tile0) * kCopyTile;
+    // last segment whose group starts at or before `tile`; stripe groups interleave their tiles
+    int idx = find_desc(segs, nseg, tile);
+    uint32_t rel = tile - segs[idx].tile0;
+    const uint32_t k = segs[idx].gsize;
+    if (k > 1) {
+      idx = idx - int(k) + 1 + int(rel % k);
+      rel /= k;
+    }
+    const CopySeg& s = segs[idx];
+    const uint64_t off = uint64_t(rel) * kCopyTile;
     const uint64_t rem = s.bytes - off;
     const uint32_t nb = rem < kCopyTile ? uint32_t(rem) : kCopyTile;
+    const uint32_t ndst = s.ndst;
     const uint8_t* src = s.src + off;
     uintptr_t amask = reinterpret_cast<uintptr_t>(src);
 #pragma unroll
     for (int d = 0; d < kMaxDst; ++d)
-      if (d < int(s.ndst)) amask |= reinterpret_cast<uintptr_t>(s.dst[d] + off);
+      if (d < int(ndst)) amask |= reinterpret_cast<uintptr_t>(s.dst[d] + off);
     if ((amask & 15) == 0) {
       const uint32_t nv = nb >> 4;
       uint4 v[kCopyUnroll];
@@ -131,7 +164,7 @@ __global__ void __launch_bounds__(kThreads) k_copy(const CopySeg* __restrict__ s
       }
 #pragma unroll
       for (int d = 0; d < kMaxDst; ++d) {
-        if (d >= int(s.ndst)) break;
+        if (d >= int(ndst)) break;
         uint8_t* dst = s.dst[d] + off;
 #pragma unroll
         for (int u = 0; u < kCopyUnroll; ++u) {
@@ -141,16 +174,17 @@ __global__ void __launch_bounds__(kThreads) k_copy(const CopySeg* __restrict__ s
       }
       for (uint32_t b = nv * 16 + threadIdx.x; b < nb; b += kThreads) {
         const uint8_t x = src[b];
-        for (int d = 0; d < int(s.ndst); ++d) s.dst[d][off + b] = x;
+        for (int d = 0; d < int(ndst); ++d) s.dst[d][off + b] = x;
       }
     } else {  // byte-granular chunks (the reference tests' 1/7/9-byte shards)
       for (uint32_t b = threadIdx.x; b < nb; b += kThreads) {
         const uint8_t x = src[b];
-        for (int d = 0; d < int(s.ndst); ++d) s.dst[d][off + b] = x;
+        for (int d = 0; d < int(ndst); ++d) s.dst[d][off + b] = x;
       }
     }
   }
   bar_exit(bar);
+  pdl_end(bar);
 }
 
 // ---------------------------------------------------------------- K2: reduce engine
@@ -220,71 +254,153 @@ __device__ __forceinline__ Acc finish(Acc a, const Acc* dst, uint64_t e, Acc sca
   return a;
 }
 
+// Loads U vectors per thread from each of up to P sources (all issued before the
+// first add, so every source — local HBM and each NVLink peer — is in flight at
+// once), then folds them in ascending group position: the reference's order.
+template <typename In, typename Acc, int P, int U>
+__device__ __forceinline__ void fold_vecs(const uint8_t* const* srcs, uint32_t p, uint64_t e, uint32_t stride,
+                                          Acc (&acc)[U][Codec<In, Acc>::VEC]) {
+  using C = Codec<In, Acc>;
+  constexpr int VEC = C::VEC;
+  uint4 raw[P][U];
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    if (i < int(p)) {
+      const In* si = reinterpret_cast<const In*>(srcs[i]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) raw[i][u] = ld_stream(si + e + uint64_t(u) * stride);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) C::unpack(raw[0][u], acc[u]);
+#pragma unroll
+  for (int i = 1; i < P; ++i) {
+    if (i < int(p)) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        Acc x[VEC];
+        C::unpack(raw[i][u], x);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) acc[u][k] = Arith<Acc>::add(acc[u][k], x[k]);
+      }
+    }
+  }
+}
+
+// p > 8: sources in batches of 8 (all loads of a batch in flight), folded in order
 template <typename In, typename Acc>
-__global__ void __launch_bounds__(kThreads) k_reduce(const RedJob* __restrict__ jobs, int njobs, uint32_t ntiles,
-                                                     Acc scale, int use_scale, int mode, BarrierArg bar) {
+__device__ __forceinline__ void fold_vecs_wide(const uint8_t* const* srcs, uint32_t p, uint64_t e,
+                                               Acc (&acc)[1][Codec<In, Acc>::VEC]) {
+  using C = Codec<In, Acc>;
+  constexpr int VEC = C::VEC;
+#pragma unroll 1
+  for (uint32_t b = 0; b < p; b += 8) {
+    uint4 raw[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (b + i < p) raw[i] = ld_stream(reinterpret_cast<const In*>(srcs[b + i]) + e);
+    if (b == 0) C::unpack(raw[0], acc[0]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if ((b > 0 || i > 0) && b + i < p) {
+        Acc x[VEC];
+        C::unpack(raw[i], x);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) acc[0][k] = Arith<Acc>::add(acc[0][k], x[k]);
+      }
+    }
+  }
+}
+
+template <typename Acc, int VEC>
+__device__ __forceinline__ void finish_store(Acc* d, const Acc (&acc)[VEC], const uint4 (&prev_raw)[VEC * sizeof(Acc) / 16],
+                                             Acc scale, int use_scale, int mode) {
+  constexpr int Q = int(VEC * sizeof(Acc) / 16);
+  Acc prev[VEC];
+  if (mode == MICS_RS_ACCUMULATE) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) memcpy(reinterpret_cast<uint8_t*>(prev) + 16 * q, &prev_raw[q], 16);
+  }
+  Acc out[VEC];
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) {
+    Acc a = acc[k];
+    if (use_scale) a = Arith<Acc>::mul(a, scale);
+    if (mode == MICS_RS_ACCUMULATE) a = Arith<Acc>::add(prev[k], a);
+    else if (mode == MICS_RS_ZERO_ACCUM) a = Arith<Acc>::add(Acc(0), a);
+    out[k] = a;
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    uint4 r;
+    memcpy(&r, reinterpret_cast<const uint8_t*>(out) + 16 * q, 16);
+    st_vec(reinterpret_cast<uint8_t*>(d) + 16 * q, r);
+  }
+}
+
+// U vectors per thread per call, (kRedUnroll / U) calls per tile
+template <typename In, typename Acc, int P, int U>
+__device__ __forceinline__ void reduce_tile(const uint8_t* const* srcs, uint32_t p, Acc* dst, uint64_t e0,
+                                            Acc scale, int use_scale, int mode) {
+  constexpr int VEC = Codec<In, Acc>::VEC;
+  constexpr int Q = int(VEC * sizeof(Acc) / 16);
+  constexpr uint32_t stride = kThreads * VEC;
+#pragma unroll 1
+  for (int h = 0; h < kRedUnroll; h += U) {
+    const uint64_t e = e0 + (uint64_t(h) * kThreads + threadIdx.x) * VEC;
+    uint4 prev[U][Q];  // accumulator reads issued together with the source loads
+    if (mode == MICS_RS_ACCUMULATE) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          prev[u][q] = ld_plain(reinterpret_cast<const uint8_t*>(dst + e + uint64_t(u) * stride) + 16 * q);
+    }
+    Acc acc[U][VEC];
+    if constexpr (P > 8) fold_vecs_wide<In, Acc>(srcs, p, e, acc);
+    else fold_vecs<In, Acc, P, U>(srcs, p, e, stride, acc);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      finish_store<Acc, VEC>(dst + e + uint64_t(u) * stride, acc[u], prev[u], scale, use_scale, mode);
+  }
+}
+
+// PC = source-count class of the launch (2, 4, 8, or 9 = more than 8): each class
+// is its own kernel so the common p=2 case keeps a small register footprint.
+template <typename In, typename Acc, int PC>
+__global__ void __launch_bounds__(kThreads, 2) k_reduce(const RedJob* __restrict__ gjobs, int njobs,
+                                                     uint32_t table_bytes, uint32_t ntiles, Acc scale, int use_scale,
+                                                     int mode, BarrierArg bar) {
   using C = Codec<In, Acc>;
   constexpr int VEC = C::VEC;
   constexpr uint32_t TILE = kThreads * kRedUnroll * VEC;
+  // stage the job table and its source-pointer arrays in shared memory
+  extern __shared__ __align__(16) unsigned char smem[];
+  const bool staged = table_bytes != 0;
+  if (staged) {
+    const uint4* s = reinterpret_cast<const uint4*>(gjobs);
+    uint4* d = reinterpret_cast<uint4*>(smem);
+    for (uint32_t i = threadIdx.x; i < table_bytes / 16; i += kThreads) d[i] = s[i];
+  }
+  __syncthreads();
+  const RedJob* jobs = staged ? reinterpret_cast<const RedJob*>(smem) : gjobs;
+  pdl_begin(bar);
   bar_entry(bar);
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const RedJob& J = jobs[find_desc(jobs, njobs, tile)];
     const uint64_t e0 = uint64_t(tile - J.tile0) * TILE;
     const uint32_t p = J.p;
-    const uint8_t* const* srcs = J.srcs;
+    const uint8_t* const* srcs =
+        staged ? reinterpret_cast<const uint8_t* const*>(smem + (reinterpret_cast<const char*>(J.srcs) -
+                                                                 reinterpret_cast<const char*>(gjobs)))
+               : J.srcs;
     Acc* dst = reinterpret_cast<Acc*>(J.dst);
     if (J.aligned && e0 + TILE <= J.valid && e0 + TILE <= J.elems) {
-      Acc acc[kRedUnroll][VEC];
-      {
-        const In* s0 = reinterpret_cast<const In*>(srcs[0]);
-        uint4 raw[kRedUnroll];
-#pragma unroll
-        for (int u = 0; u < kRedUnroll; ++u) raw[u] = ld_stream(s0 + e0 + uint64_t(u * kThreads + threadIdx.x) * VEC);
-#pragma unroll
-        for (int u = 0; u < kRedUnroll; ++u) C::unpack(raw[u], acc[u]);
-      }
-#pragma unroll 4
-      for (uint32_t i = 1; i < p; ++i) {  // ascending group position: the pinned fold order
-        const In* si = reinterpret_cast<const In*>(srcs[i]);
-        uint4 raw[kRedUnroll];
-#pragma unroll
-        for (int u = 0; u < kRedUnroll; ++u) raw[u] = ld_stream(si + e0 + uint64_t(u * kThreads + threadIdx.x) * VEC);
-#pragma unroll
-        for (int u = 0; u < kRedUnroll; ++u) {
-          Acc x[VEC];
-          C::unpack(raw[u], x);
-#pragma unroll
-          for (int k = 0; k < VEC; ++k) acc[u][k] = Arith<Acc>::add(acc[u][k], x[k]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kRedUnroll; ++u) {
-        const uint64_t e = e0 + uint64_t(u * kThreads + threadIdx.x) * VEC;
-        Acc* d = dst + e;
-        Acc prev[VEC];
-        if (mode == MICS_RS_ACCUMULATE) {
-#pragma unroll
-          for (int q = 0; q < int(VEC * sizeof(Acc) / 16); ++q) {
-            const uint4 r = ld_plain(reinterpret_cast<const uint8_t*>(d) + 16 * q);
-            memcpy(reinterpret_cast<uint8_t*>(prev) + 16 * q, &r, 16);
-          }
-        }
-        Acc out[VEC];
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) {
-          Acc a = acc[u][k];
-          if (use_scale) a = Arith<Acc>::mul(a, scale);
-          if (mode == MICS_RS_ACCUMULATE) a = Arith<Acc>::add(prev[k], a);
-          else if (mode == MICS_RS_ZERO_ACCUM) a = Arith<Acc>::add(Acc(0), a);
-          out[k] = a;
-        }
-#pragma unroll
-        for (int q = 0; q < int(VEC * sizeof(Acc) / 16); ++q) {
-          uint4 r;
-          memcpy(&r, reinterpret_cast<const uint8_t*>(out) + 16 * q, 16);
-          st_vec(reinterpret_cast<uint8_t*>(d) + 16 * q, r);
-        }
-      }
+      constexpr int U2 = VEC > 4 ? 2 : 4;  // bf16 input widens 8 lanes per vector: fewer vectors in flight
+      if constexpr (PC == 2) reduce_tile<In, Acc, 2, U2>(srcs, p, dst, e0, scale, use_scale, mode);
+      else if constexpr (PC == 4) reduce_tile<In, Acc, 4, 2>(srcs, p, dst, e0, scale, use_scale, mode);
+      else if constexpr (PC == 8) reduce_tile<In, Acc, 8, 1>(srcs, p, dst, e0, scale, use_scale, mode);
+      else reduce_tile<In, Acc, 9, 1>(srcs, p, dst, e0, scale, use_scale, mode);
     } else {  // ragged / unaligned / zero-padded tail: element at a time, same fold
       const uint64_t end = (e0 + TILE < J.elems) ? e0 + TILE : J.elems;
       for (uint64_t e = e0 + threadIdx.x; e < end; e += kThreads) {
@@ -298,6 +414,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce(const RedJob* __restrict__ 
     }
   }
   bar_exit(bar);
+  pdl_end(bar);
 }
 
 // ---------------------------------------------------------------- K5: AG phase fused with Adam
@@ -319,6 +436,7 @@ __device__ __forceinline__ void adam_one(float g, float& p, float& m, float& v, 
 
 __global__ void __launch_bounds__(kThreads) k_adam(const AdamJob* __restrict__ jobs, int njobs, uint32_t ntiles,
                                                    AdamScalars sc, BarrierArg bar) {
+  pdl_begin(bar);
   bar_entry(bar);
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const AdamJob& J = jobs[find_desc(jobs, njobs, tile)];
@@ -364,6 +482,7 @@ __global__ void __launch_bounds__(kThreads) k_adam(const AdamJob* __restrict__ j
     }
   }
   bar_exit(bar);
+  pdl_end(bar);
 }
 
 // ---------------------------------------------------------------- K6: counter-based gradients
@@ -395,42 +514,119 @@ __global__ void __launch_bounds__(kThreads) k_cast_bf16(const float* in, uint16_
 }
 
 __global__ void k_barrier(BarrierArg bar) {
+  pdl_begin(bar);
   bar_entry(bar);
   bar_exit(bar);
+  pdl_end(bar);
 }
 
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
+namespace {
+bool pdl_enabled() {  // MICS_PDL=0 launches without programmatic stream serialization (debugging)
+  static const bool on = [] {
+    const char* e = std::getenv("MICS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... P, typename... A>
+void launch_ex(void (*kern)(P...), int grid, int block, size_t smem, cudaStream_t s, A... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  MICS_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+}  // namespace
+
+// Resident CTAs per SM of each data kernel (with a full shared-memory table):
+// grids are sized to exactly one resident wave, nsm x this.
+namespace {
+template <typename In, typename Acc>
+using ReduceFn = void (*)(const RedJob*, int, uint32_t, uint32_t, Acc, int, int, BarrierArg);
+
+template <typename In, typename Acc>
+ReduceFn<In, Acc> reduce_kernel(int pc) {
+  switch (pc) {
+    case 2: return &k_reduce<In, Acc, 2>;
+    case 4: return &k_reduce<In, Acc, 4>;
+    case 8: return &k_reduce<In, Acc, 8>;
+    default: return &k_reduce<In, Acc, 9>;
+  }
+}
+
+template <typename In, typename Acc>
+int reduce_occupancy(int pc) {
+  int n = 0;
+  MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reduce_kernel<In, Acc>(pc), kThreads, kSmemTable));
+  return n;
+}
+}  // namespace
+
+int reduce_class(uint32_t max_p) { return max_p <= 2 ? 2 : max_p <= 4 ? 4 : max_p <= 8 ? 8 : 9; }
+
+int resident_ctas(int kind, mics_dtype in_t, int pc) {
+  int n = 0;
+  switch (kind) {
+    case 0:
+      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_copy, kThreads, kSmemTable));
+      break;
+    case 1:
+      if (in_t == MICS_BF16) n = reduce_occupancy<uint16_t, float>(pc);
+      else if (in_t == MICS_F64) n = reduce_occupancy<double, double>(pc);
+      else if (in_t == MICS_I64) n = reduce_occupancy<long long, long long>(pc);
+      else n = reduce_occupancy<float, float>(pc);
+      break;
+    default:
+      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_adam, kThreads, 0));
+      break;
+  }
+  return n < 1 ? 1 : n;
+}
+
 void launch_copy(cudaStream_t s, const CopySeg* segs, int nseg, uint32_t ntiles, int grid, const BarrierArg& bar) {
-  k_copy<<<grid, kThreads, 0, s>>>(segs, nseg, ntiles, bar);
-  MICS_CUDA(cudaGetLastError());
+  const uint32_t tb = uint64_t(nseg) * sizeof(CopySeg) <= uint64_t(kSmemTable) ? uint32_t(nseg * sizeof(CopySeg)) : 0u;
+  launch_ex(k_copy, grid, kThreads, tb, s, segs, nseg, tb, ntiles, bar);
 }
 
 uint32_t reduce_tile_elems(mics_dtype in_t) {
   return uint32_t(kThreads * kRedUnroll) * uint32_t(16 / dtype_size(in_t));
 }
 
-void launch_reduce(cudaStream_t s, mics_dtype in_t, mics_dtype acc_t, const RedJob* jobs, int njobs, uint32_t ntiles,
-                   int grid, double scale, int mode, const BarrierArg& bar) {
+void launch_reduce(cudaStream_t s, mics_dtype in_t, mics_dtype acc_t, const RedJob* jobs, int njobs,
+                   uint64_t table_bytes, uint32_t max_p, uint32_t ntiles, int grid, double scale, int mode,
+                   const BarrierArg& bar) {
   const int use_scale = scale != 1.0;
+  const uint32_t tb = table_bytes <= uint64_t(kSmemTable) ? uint32_t(table_bytes) : 0u;  // 0 = read from global
+  const int pc = reduce_class(max_p);
   if (in_t == MICS_F32 && acc_t == MICS_F32)
-    k_reduce<float, float><<<grid, kThreads, 0, s>>>(jobs, njobs, ntiles, float(scale), use_scale, mode, bar);
+    launch_ex(reduce_kernel<float, float>(pc), grid, kThreads, tb, s, jobs, njobs, tb, ntiles, float(scale),
+              use_scale, mode, bar);
   else if (in_t == MICS_BF16 && acc_t == MICS_F32)
-    k_reduce<uint16_t, float><<<grid, kThreads, 0, s>>>(jobs, njobs, ntiles, float(scale), use_scale, mode, bar);
+    launch_ex(reduce_kernel<uint16_t, float>(pc), grid, kThreads, tb, s, jobs, njobs, tb, ntiles, float(scale),
+              use_scale, mode, bar);
   else if (in_t == MICS_F64 && acc_t == MICS_F64)
-    k_reduce<double, double><<<grid, kThreads, 0, s>>>(jobs, njobs, ntiles, scale, use_scale, mode, bar);
+    launch_ex(reduce_kernel<double, double>(pc), grid, kThreads, tb, s, jobs, njobs, tb, ntiles, scale, use_scale,
+              mode, bar);
   else if (in_t == MICS_I64 && acc_t == MICS_I64)
-    k_reduce<long long, long long><<<grid, kThreads, 0, s>>>(jobs, njobs, ntiles, 1, 0, mode, bar);
+    launch_ex(reduce_kernel<long long, long long>(pc), grid, kThreads, tb, s, jobs, njobs, tb, ntiles, 1LL, 0, mode,
+              bar);
   else
     raise(MICS_TYPE_MISMATCH, "unsupported reduce dtype combination");
-  MICS_CUDA(cudaGetLastError());
 }
 
 void launch_adam(cudaStream_t s, const AdamJob* jobs, int njobs, uint32_t ntiles, int grid, const AdamScalars& sc,
                  const BarrierArg& bar) {
-  k_adam<<<grid, kThreads, 0, s>>>(jobs, njobs, ntiles, sc, bar);
-  MICS_CUDA(cudaGetLastError());
+  launch_ex(k_adam, grid, kThreads, 0, s, jobs, njobs, ntiles, sc, bar);
 }
 
 void launch_generate(cudaStream_t s, void* out, mics_dtype dtype, uint64_t seed, int rank, int step, int layer,
@@ -448,8 +644,7 @@ void launch_cast_bf16(cudaStream_t s, const float* in, uint16_t* out, uint64_t c
 }
 
 void launch_barrier(cudaStream_t s, const BarrierArg& bar) {
-  k_barrier<<<1, 32, 0, s>>>(bar);
-  MICS_CUDA(cudaGetLastError());
+  launch_ex(k_barrier, 1, 32, 0, s, bar);
 }
 
 }  // namespace mics

@@ -129,6 +129,11 @@ mics_ctx* create_ctx(const mics_init_args* a) {
     if (prop.major != 10)
       raise(MICS_CONFIG_ERROR, std::string("libmics is built for sm_100a (B200); device is ") + prop.name);
     c->nsm = prop.multiProcessorCount;
+    c->occ_copy = resident_ctas(0, MICS_F32);
+    c->occ_adam = resident_ctas(2, MICS_F32);
+    const int classes[4] = {2, 4, 8, 9};
+    for (int t = 0; t < 4; ++t)
+      for (int k = 0; k < 4; ++k) c->occ_reduce[t][k] = resident_ctas(1, mics_dtype(t), classes[k]);
     MICS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->cap = (a->arena_bytes ? a->arena_bytes : (1ull << 30)) + kFlagsBytes;
     c->cap = round_up(c->cap, 2ull << 20);

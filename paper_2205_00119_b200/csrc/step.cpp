@@ -51,17 +51,20 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l) {
   if (k <= 0 || p <= k) {
     CopyPlan plan;
     for (int g = 0; g < n / p; ++g) {
-      std::vector<void*> dummy;
+      std::vector<std::pair<const void*, std::vector<void*>>> items;  // one stripe group per partition group
       for (int i = 0; i < p; ++i) {
         std::vector<void*> dsts;
         for (int j = 0; j < p; ++j)
           if (ctx->local(g * p + j)) dsts.push_back(G(g * p + j, uint64_t(i)));
-        plan.add(ctx->rank_ptr(st->pbf16, g * p + i) + soff, dsts, cb);
+        if (!dsts.empty()) items.emplace_back(ctx->rank_ptr(st->pbf16, g * p + i) + soff, std::move(dsts));
       }
+      plan.add_group(items, cb);
     }
     // no barrier: shards are static between boundaries; the micro-step
     // reduce-scatter and Adam barriers order every write against these reads
-    out.push_back(make_copy_launch(ctx, plan, ctx->barrier(0, 0, 0), true));
+    Launch l = make_copy_launch(ctx, plan, ctx->barrier(0, 0, 0), true);
+    l.bar.dep_first = 0;  // independent of the previous layer's gather: overlaps its tail (PDL)
+    out.push_back(l);
     return out;
   }
   // hierarchical: stage 1 (channels) with stage 2 folded into addressing, then stage 3
@@ -77,15 +80,18 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l) {
       for (int j = 0; j < k; ++j) {
         const int r = base + mm * k + j;
         if (!ctx->local(r)) continue;
+        std::vector<std::pair<const void*, std::vector<void*>>> g1, g2;
         for (int m2 = 0; m2 < q; ++m2)
-          ph1.add(ctx->rank_ptr(st->pbf16, base + m2 * k + j) + soff, {G(r, uint64_t(m2) * k + j)}, cb);
+          g1.push_back({ctx->rank_ptr(st->pbf16, base + m2 * k + j) + soff, {G(r, uint64_t(m2) * k + j)}});
         for (int j2 = 0; j2 < k; ++j2) {
           if (j2 == j) continue;
           for (int t = 0; t < q; ++t) {
             const uint64_t pos = uint64_t(t) * k + j2;
-            ph2.add(G(base + mm * k + j2, pos), {G(r, pos)}, cb);
+            g2.push_back({G(base + mm * k + j2, pos), {G(r, pos)}});
           }
         }
+        ph1.add_group(g1, cb);
+        ph2.add_group(g2, cb);
       }
   }
   out.push_back(make_copy_launch(ctx, ph1, ctx->barrier(mask, 0, 1), true));
@@ -116,11 +122,22 @@ void enqueue_boundary(mics_step* st) {
   }
 }
 
-void enqueue_micro(mics_step* st, int t) {
+// forward then backward per-layer gathers.  The first gather of a window follows
+// the boundary's Adam (which rewrote the shards it reads), so it waits for its
+// predecessor; the others only depend on static shards.
+void enqueue_gathers(mics_step* st, int t) {
+  bool first = true;
   for (size_t l = 0; l < st->layers.size(); ++l)
-    for (auto& x : st->ag[l]) enqueue(st->ctx, x);
+    for (auto& x : st->ag[l]) {
+      enqueue(st->ctx, x, first && t == 0 ? 1 : -1);
+      first = false;
+    }
   for (size_t l = st->layers.size(); l-- > 0;)
     for (auto& x : st->ag[l]) enqueue(st->ctx, x);
+}
+
+void enqueue_micro(mics_step* st, int t) {
+  enqueue_gathers(st, t);
   enqueue(st->ctx, st->rs[size_t(t)]);
 }
 }  // namespace
@@ -249,10 +266,7 @@ void step_profile(mics_step* st, double* ag_ms, double* rs_ms, double* bnd_ms, d
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
     if (!st->cfg.resident_grads) enqueue_generate(st, t);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
-    for (size_t l = 0; l < st->layers.size(); ++l)
-      for (auto& x : st->ag[l]) enqueue(ctx, x);
-    for (size_t l = st->layers.size(); l-- > 0;)
-      for (auto& x : st->ag[l]) enqueue(ctx, x);
+    enqueue_gathers(st, t);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
     enqueue(ctx, st->rs[size_t(t)]);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
@@ -281,9 +295,10 @@ void step_profile(mics_step* st, double* ag_ms, double* rs_ms, double* bnd_ms, d
 }
 
 // End-to-end variant through host memory: every micro-step each local rank's
-// gradients are copied from (pinned) host memory — host_grads holds s gradient
-// sets of grad_elems, shared by the local ranks, one DMA per rank — and after the
-// boundary a fixed-size slice of every local rank's updated master shard is read back.
+// gradients are copied from (pinned) host memory — host_grads holds one gradient
+// set of grad_elems, reused for every local rank and micro-step (one DMA each) —
+// and after the boundary a fixed-size slice of every local rank's updated master
+// shard is read back.
 void step_run_host(mics_step* st, const void* host_grads, int iters, void* host_result) {
   mics_ctx* ctx = st->ctx;
   const uint64_t szg = dtype_size(st->cfg.grad_t), gb = st->sync->grad_elems * szg;
@@ -293,9 +308,8 @@ void step_run_host(mics_step* st, const void* host_grads, int iters, void* host_
       const uint64_t off = st->cfg.resident_grads ? uint64_t(t) * gb : 0;
       for (int r = 0; r < ctx->n; ++r) {
         if (!ctx->local(r)) continue;
-        MICS_CUDA(cudaMemcpyAsync(ctx->rank_ptr(st->grads, r) + off,
-                                  static_cast<const char*>(host_grads) + uint64_t(t) * gb, gb,
-                                  cudaMemcpyHostToDevice, ctx->stream));
+        MICS_CUDA(cudaMemcpyAsync(ctx->rank_ptr(st->grads, r) + off, host_grads, gb, cudaMemcpyHostToDevice,
+                                  ctx->stream));
       }
       enqueue_micro(st, t);
     }

@@ -192,11 +192,13 @@ BoundaryLaunches build_boundary(mics_sync* st, const mics_adam* adam, bool persi
     for (int rho = 0; rho < n; ++rho) {
       if (!ctx->local(rho)) continue;
       const int j = rho % p, i = rho / p;
+      std::vector<std::pair<const void*, std::vector<void*>>> items;
       for (int q = 0; q < r; ++q) {
         if (q == i) continue;
         const uint64_t o = uint64_t(q) * sub * sza;
-        ag.add(ctx->rank_ptr(st->shard, j + q * p) + o, {ctx->rank_ptr(st->shard, rho) + o}, sub * sza);
+        items.push_back({ctx->rank_ptr(st->shard, j + q * p) + o, {ctx->rank_ptr(st->shard, rho) + o}});
       }
+      ag.add_group(items, sub * sza);
     }
     out.ag = make_copy_launch(ctx, ag, ctx->barrier(rmask, 0, 1), persistent);
     out.has_ag = true;
