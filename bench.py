@@ -147,6 +147,18 @@ def peaks():
 NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 
 
+def ncu_traffic(workload, n_gpus, phase):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel,
+    from the committed `ncu --set full` captures (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            table = json.load(fh)
+    except OSError:
+        return None
+    ent = table.get(f"{workload.split(' ')[0]}|{n_gpus}|{phase}")
+    return ent["dram_bytes_per_launch"] if ent else None
+
+
 # ----------------------------------------------------------------------------- CPU baseline (reference)
 def cpu_baseline(wl, threads):
     """The reference's own step functions (oracle/_ref) on a bounded sample: ONE
@@ -283,6 +295,12 @@ def run_mics(args, wl, rank, world, local):
         raise SystemExit(f"--gpus {world} must divide the {n} ranks")
     per = n // world
     resident = not args.generated_grads
+    free = torch.cuda.mem_get_info(local)[0]
+    if resident and arena_bytes(wl, per, True) > 0.92 * free:
+        resident = False  # s resident gradient sets do not fit (C5): generate them per micro-step (K6)
+    if arena_bytes(wl, per, resident) > 0.95 * free:
+        raise SystemExit(f"{wl.name}: {per} ranks/GPU need {arena_bytes(wl, per, resident) / 1e9:.1f} GB, "
+                         f"{free / 1e9:.1f} GB free — use more GPUs")
     eng = Engine(n_ranks=n, world=world, world_rank=rank, device=local,
                  arena_bytes=arena_bytes(wl, per, resident))
     mdist.connect(eng, GLOO)
@@ -317,47 +335,39 @@ def run_mics(args, wl, rank, world, local):
     # per-phase device times (CUDA events on the launching stream), one extra step
     prof = step.profile()
     prof = {k: max_over_ranks(v, world) for k, v in prof.items()}
-    L = len(wl.layer_params)
-    nag = 2 * wl.s * L * (2 if wl.hier_k and wl.p > wl.hier_k else 1)
-    phases = {"allgather": (prof["allgather_ms"], nag), "reducescatter": (prof["reducescatter_ms"], wl.s),
-              "boundary": (prof["boundary_ms"], 2)}
+    # algorithmic bytes per phase, summed by the library from the planned descriptor
+    # tables (this process, per step): pulled from peers over NVLink / local HBM r+w
+    kernels = {"allgather": "k_copy (per-layer partition-group all-gather)",
+               "reducescatter": "k_reduce (micro-step reduce-scatter + shard accumulate)",
+               "boundary": "k_reduce + k_adam (boundary all-reduce fused with Adam)"}
+    phases = {"allgather": (prof["allgather_ms"], stats.ag_launches, stats.ag_remote_bytes, stats.ag_hbm_bytes),
+              "reducescatter": (prof["reducescatter_ms"], stats.rs_launches, stats.rs_remote_bytes,
+                                stats.rs_hbm_bytes),
+              "boundary": (prof["boundary_ms"], stats.bnd_launches, stats.bnd_remote_bytes, stats.bnd_hbm_bytes)}
     dom = max(phases, key=lambda k: phases[k][0])
-    dom_ms, dom_launches = phases[dom]
-    # algorithmic bytes of the dominant phase per process per step
-    p, s = wl.p, wl.s
-    chunks = [((e + p - 1) // p + 7) // 8 * 8 for e in wl.layer_params]
-    S = sum(chunks)
-    szg = 2 if wl.grad_dtype == "bf16" else 4
-    groups_here = len({r // p for r in eng.local_ranks})
-    if dom == "allgather":
-        kernel = "k_copy (per-layer partition-group all-gather)"
-        hbm = 2 * s * (per * p * S * 2 + groups_here * p * S * 2)        # writes + one read per source chunk
-        ingress = 2 * s * per * (p - 1) * S * 2 if world > 1 and p > per else 0
-    elif dom == "reducescatter":
-        kernel = "k_reduce (micro-step reduce-scatter + shard accumulate)"
-        hbm = s * per * (p * S * szg + 4 * S) + (s - 1) * per * 4 * S
-        ingress = s * per * (p - 1) * S * szg if world > 1 and p > per else 0
-    else:
-        r = n // p
-        sub = stats.ar_bytes_in // max(1, 2 * (r - 1) * 4) if r > 1 else S
-        kernel = "k_reduce + k_adam (boundary all-reduce fused with Adam)"
-        hbm = per * (r * sub * 4 + sub * 4 + S * 30)
-        ingress = per * stats.ar_bytes_in if world > 1 and r > per else 0
+    dom_ms, dom_launches, remote, hbm = phases[dom]
+    dom_launches = max(1, dom_launches)
     pk, pk_kind = peaks()
-    per_launch_ms = dom_ms / dom_launches
-    if ingress:
-        achieved = ingress / dom_launches / (per_launch_ms / 1e3) / 1e9
-        roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
-                "frac": achieved / NVLINK_PEER_GBS, "traffic": None, "kernel": kernel,
-                "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md); 900 nominal",
-                "hbm_GBps": hbm / dom_launches / (per_launch_ms / 1e3) / 1e9}
+    per_launch_s = dom_ms / dom_launches / 1e3
+    nv_gbs = remote / dom_launches / per_launch_s / 1e9
+    hbm_gbs = hbm / dom_launches / per_launch_s / 1e9
+    if remote and remote / NVLINK_PEER_GBS >= hbm / pk["hbm_gbs"]:  # the resource with the longer ideal time
+        roof = {"bound": "nvlink", "achieved": nv_gbs, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                "frac": nv_gbs / NVLINK_PEER_GBS,
+                "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md; 900 nominal). "
+                               "Both directions loaded at once (every GPU sends and receives): 670 GB/s pull, "
+                               "706 GB/s push measured by tools/probe_bulk.cu",
+                "bytes_per_launch": remote / dom_launches}
     else:
-        achieved = hbm / dom_launches / (per_launch_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": kernel,
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})"}
-    roof["launch_ms"] = per_launch_ms
-    roof["bytes_per_launch"] = (ingress or hbm) / dom_launches
+        roof = {"bound": "hbm", "achieved": hbm_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": hbm_gbs / pk["hbm_gbs"], "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})",
+                "bytes_per_launch": hbm / dom_launches}
+    roof.update({"traffic": ncu_traffic(wl.name, world, dom), "kernel": kernels[dom], "phase": dom,
+                 "launch_ms": per_launch_s * 1e3, "launches_per_step": dom_launches, "nvlink_GBps": nv_gbs,
+                 "hbm_GBps": hbm_gbs})
+    p, s = wl.p, wl.s
+    S = stats.shard_elems
+    szg = 2 if wl.grad_dtype == "bf16" else 4
 
     # end-to-end through the C-ABI with host buffers: gradients H2D every micro-step
     e2e = None
@@ -415,8 +425,8 @@ def run_mics(args, wl, rank, world, local):
         "phases_ms": {k: v[0] for k, v in phases.items()},
         "per_rank_bytes": {"allgather_in": stats.ag_bytes_in, "reducescatter_in": stats.rs_bytes_in,
                            "boundary_in": stats.ar_bytes_in, "adam_hbm": stats.adam_hbm_bytes},
-        "collective_GBps": {"allgather_bus": stats.ag_bytes_in * per / (prof["allgather_ms"] / 1e3) / 1e9,
-                            "reducescatter_bus": stats.rs_bytes_in * per / (prof["reducescatter_ms"] / 1e3) / 1e9},
+        "phase_GBps": {k: {"nvlink": v[2] / (v[0] / 1e3) / 1e9, "hbm": v[3] / (v[0] / 1e3) / 1e9}
+                       for k, v in phases.items() if v[0] > 0},
         "gpu_launches": launches,
         "clocks": clk,
         "e2e": e2e,

@@ -309,6 +309,11 @@ typedef struct {
   uint64_t gathered_max_bytes;
   uint64_t grad_elems;
   int adam_step;
+  /* this process, per step, summed from the planned descriptor tables: bytes pulled
+   * from peers over NVLink and local HBM bytes (reads + writes), and launches, per phase */
+  uint64_t ag_remote_bytes, ag_hbm_bytes, ag_launches;
+  uint64_t rs_remote_bytes, rs_hbm_bytes, rs_launches;
+  uint64_t bnd_remote_bytes, bnd_hbm_bytes, bnd_launches;
 } mics_step_stats;
 
 mics_status mics_step_create(mics_ctx* ctx, const mics_step_cfg* cfg, mics_step** out);

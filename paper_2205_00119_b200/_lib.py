@@ -74,7 +74,10 @@ class StepCfg(C.Structure):
 class StepStats(C.Structure):
     _fields_ = [("ag_bytes_in", U64), ("rs_bytes_in", U64), ("ar_bytes_in", U64), ("adam_hbm_bytes", U64),
                 ("gen_bytes", U64), ("launches", U64), ("shard_elems", U64), ("gathered_max_bytes", U64),
-                ("grad_elems", U64), ("adam_step", I)]
+                ("grad_elems", U64), ("adam_step", I),
+                ("ag_remote_bytes", U64), ("ag_hbm_bytes", U64), ("ag_launches", U64),
+                ("rs_remote_bytes", U64), ("rs_hbm_bytes", U64), ("rs_launches", U64),
+                ("bnd_remote_bytes", U64), ("bnd_hbm_bytes", U64), ("bnd_launches", U64)]
 
 
 # (name, restype, argtypes); restype I is a mics_status

@@ -137,6 +137,10 @@ Launch make_copy_launch(mics_ctx* ctx, const CopyPlan& plan, const BarrierArg& b
   l.ntiles = plan.tiles;
   l.grid = ctx->grid_for(plan.tiles, ctx->occ_copy);
   l.bar = bar;
+  for (const auto& s : plan.segs) {
+    (ctx->is_local_ptr(s.src) ? l.hbm_bytes : l.remote_bytes) += s.bytes;
+    l.hbm_bytes += s.bytes * s.ndst;
+  }
   if (l.ndesc) {
     const uint64_t bytes = sizeof(CopySeg) * plan.segs.size();
     l.d_desc = table_memory(ctx, bytes, persistent);
@@ -158,6 +162,12 @@ Launch make_reduce_launch(mics_ctx* ctx, const RedPlan& plan, mics_dtype in_t, m
   l.scale = scale;
   l.mode = mode;
   l.bar = bar;
+  const uint64_t szi = dtype_size(in_t), sza = dtype_size(acc_t);
+  for (size_t j = 0; j < plan.jobs.size(); ++j) {
+    const RedJob& J = plan.jobs[j];
+    for (const void* s : plan.srcs[j]) (ctx->is_local_ptr(s) ? l.hbm_bytes : l.remote_bytes) += J.valid * szi;
+    l.hbm_bytes += J.elems * sza * (mode == MICS_RS_ACCUMULATE ? 2 : 1);
+  }
   if (l.ndesc) l.d_desc = upload_jobs(ctx, plan.jobs, plan.srcs, persistent, &l.table_bytes);
   return l;
 }
@@ -171,6 +181,14 @@ Launch make_adam_launch(mics_ctx* ctx, const AdamPlan& plan, const AdamScalars& 
   l.grid = ctx->grid_for(plan.tiles, ctx->occ_adam);
   l.adam = sc;
   l.bar = bar;
+  for (size_t j = 0; j < plan.jobs.size(); ++j) {
+    const AdamJob& J = plan.jobs[j];
+    for (size_t q = 0; q < plan.srcs[j].size(); ++q) {  // owner q holds slice [q*sub, (q+1)*sub)
+      const uint64_t lo = std::min<uint64_t>(q * J.sub, J.elems), hi = std::min<uint64_t>((q + 1) * J.sub, J.elems);
+      (ctx->is_local_ptr(plan.srcs[j][q]) ? l.hbm_bytes : l.remote_bytes) += (hi - lo) * 4;
+    }
+    l.hbm_bytes += J.elems * (24 + (J.pbf16 ? 2 : 0) + (J.gout ? 4 : 0));  // r/w p, m, v; w bf16; w grad
+  }
   if (l.ndesc) l.d_desc = upload_jobs(ctx, plan.jobs, plan.srcs, persistent);
   return l;
 }

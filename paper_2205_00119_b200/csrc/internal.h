@@ -187,6 +187,10 @@ struct mics_ctx {
   }
   // processes hosting any of `ranks`, minus self (0 when self hosts none)
   uint64_t peer_mask(const int* ranks, int count) const;
+  bool is_local_ptr(const void* p) const {
+    const char* c = static_cast<const char*>(p);
+    return !ipc_ready || (c >= base && c < base + cap);
+  }
   uint64_t local_alloc(uint64_t bytes);  // world == 1 scratch
 };
 
@@ -232,6 +236,9 @@ struct Launch {
   int mode = 0;
   AdamScalars adam{};
   BarrierArg bar{};
+  // algorithmic bytes one launch moves on this GPU: pulled from peers over NVLink,
+  // and local HBM reads + writes (the roofline numerators of bench.py)
+  uint64_t remote_bytes = 0, hbm_bytes = 0;
   void release();
 };
 Launch make_copy_launch(mics_ctx* ctx, const CopyPlan& plan, const BarrierArg& bar, bool persistent);

@@ -94,8 +94,12 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l) {
         ph2.add_group(g2, cb);
       }
   }
+  // phase 1's exit barrier publishes every rank's stage-1 chunks before phase 2
+  // reads them.  Phase 2 needs no barrier of its own: the next overwrite of a
+  // gathered buffer (phase 1 of layer l+2) sits behind layer l+1's phase-1
+  // barrier, which every node peer only reaches after finishing phase 2 of l.
   out.push_back(make_copy_launch(ctx, ph1, ctx->barrier(mask, 0, 1), true));
-  out.push_back(make_copy_launch(ctx, ph2, ctx->barrier(mask, 0, 1), true));
+  out.push_back(make_copy_launch(ctx, ph2, ctx->barrier(0, 0, 0), true));
   return out;
 }
 
@@ -217,17 +221,28 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     MICS_CUDA(cudaStreamSynchronize(ctx->stream));
     barrier_all(ctx);
     MICS_CUDA(cudaStreamSynchronize(ctx->stream));
-    // kernels one step launches on this process (enqueue() skips empty launches)
-    uint64_t per = 0;
-    for (int t = 0; t < cfg->s; ++t) {
-      per += cfg->resident_grads ? 0 : uint64_t(ctx->per);
-      for (auto& v : st->ag)
-        for (auto& x : v) per += 2 * uint64_t((x.ndesc || x.bar.mask) ? 1 : 0);
-      per += (st->rs[size_t(t)].ndesc || st->rs[size_t(t)].bar.mask) ? 1 : 0;
+    // kernels and algorithmic bytes of one step on this process (enqueue() skips empty launches)
+    auto runs = [](const Launch& x) -> uint64_t { return (x.ndesc || x.bar.mask) ? 1 : 0; };
+    mics_step_stats& S2 = st->stats;
+    for (auto& v : st->ag)
+      for (auto& x : v) {  // forward + backward pass, every micro-step
+        S2.ag_launches += 2 * uint64_t(cfg->s) * runs(x);
+        S2.ag_remote_bytes += 2 * uint64_t(cfg->s) * x.remote_bytes;
+        S2.ag_hbm_bytes += 2 * uint64_t(cfg->s) * x.hbm_bytes;
+      }
+    for (auto& x : st->rs) {
+      S2.rs_launches += runs(x);
+      S2.rs_remote_bytes += x.remote_bytes;
+      S2.rs_hbm_bytes += x.hbm_bytes;
     }
-    if (st->bnd.has_rs) per += (st->bnd.rs.ndesc || st->bnd.rs.bar.mask) ? 1 : 0;
-    if (st->bnd.has_ag) per += (st->bnd.ag.ndesc || st->bnd.ag.bar.mask) ? 1 : 0;
-    st->stats.launches = per;
+    for (const Launch* x : {&st->bnd.rs, &st->bnd.ag}) {
+      if ((x == &st->bnd.rs && !st->bnd.has_rs) || (x == &st->bnd.ag && !st->bnd.has_ag)) continue;
+      S2.bnd_launches += runs(*x);
+      S2.bnd_remote_bytes += x->remote_bytes;
+      S2.bnd_hbm_bytes += x->hbm_bytes;
+    }
+    S2.launches = S2.ag_launches + S2.rs_launches + S2.bnd_launches +
+                  (cfg->resident_grads ? 0 : uint64_t(cfg->s) * uint64_t(ctx->per));
   } catch (...) {
     release(st);
     delete st;
