@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--generated-grads", action="store_true", help="generate gradients inside the step (K6)")
+    ap.add_argument("--schedule", default="two_hop", choices=["two_hop", "alternative"],
+                    help="2-hop sync (MiCS) or the DeepSpeed-default all-reduce over all ranks every micro-step")
     ap.add_argument("--sweep", action="store_true", help="C2 collective sweep instead of the step")
     return ap.parse_args()
 
@@ -104,16 +106,18 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- helpers
-def arena_bytes(wl, per, resident):
+def arena_bytes(wl, per, resident, n=N_RANKS, alternative=False):
     """Per-process arena for `per` local ranks (mirrors csrc/step.cpp's allocations)."""
     p, s = wl.p, wl.s
     chunks = [((e + p - 1) // p + 7) // 8 * 8 for e in wl.layer_params]
     S = sum(chunks)
-    r = N_RANKS // p
+    r = n // p
     sub = ((S + r - 1) // r + 3) // 4 * 4
     szg = 2 if wl.grad_dtype == "bf16" else 4
     gathered = 2 * (((max(chunks) * p * 2) + 255) // 256 * 256)
     per_rank = r * sub * 4 + S * 2 + 3 * S * 4 + gathered + (s if resident else 1) * p * S * szg
+    if alternative:  # all-n reduce-scatter scratch: n slices of ceil(p*chunk/n) per layer
+        per_rank += sum(-(-p * c // n) * n for c in chunks) * 4
     return per * (per_rank + 8 * 4096) + (256 << 20)
 
 
@@ -295,16 +299,19 @@ def run_mics(args, wl, rank, world, local):
         raise SystemExit(f"--gpus {world} must divide the {n} ranks")
     per = n // world
     resident = not args.generated_grads
+    alt = args.schedule == "alternative"
     free = torch.cuda.mem_get_info(local)[0]
-    if resident and arena_bytes(wl, per, True) > 0.92 * free:
+
+    def need(res):
+        return arena_bytes(wl, per, res, n, alt)
+    if resident and need(True) > 0.92 * free:
         resident = False  # s resident gradient sets do not fit (C5): generate them per micro-step (K6)
-    if arena_bytes(wl, per, resident) > 0.95 * free:
-        raise SystemExit(f"{wl.name}: {per} ranks/GPU need {arena_bytes(wl, per, resident) / 1e9:.1f} GB, "
+    if need(resident) > 0.95 * free:
+        raise SystemExit(f"{wl.name}: {per} ranks/GPU need {need(resident) / 1e9:.1f} GB, "
                          f"{free / 1e9:.1f} GB free — use more GPUs")
-    eng = Engine(n_ranks=n, world=world, world_rank=rank, device=local,
-                 arena_bytes=arena_bytes(wl, per, resident))
+    eng = Engine(n_ranks=n, world=world, world_rank=rank, device=local, arena_bytes=need(resident))
     mdist.connect(eng, GLOO)
-    step = MicsStep(eng, wl, StepOptions(resident_grads=resident))
+    step = MicsStep(eng, wl, StepOptions(resident_grads=resident, alternative=args.schedule == "alternative"))
     stats = step.stats()
     ext = torch.cuda.ExternalStream(eng.stream())
 
@@ -420,7 +427,7 @@ def run_mics(args, wl, rank, world, local):
                    "param_dtype": "bf16 (fp32 master, m, v)", "hierarchical_k": wl.hier_k,
                    "grads": "resident in HBM (generated before timing)" if resident else "generated in-step (K6)",
                    "l2": "inputs larger than L2 (gradient sets of %.2f GB/rank)" % (s * stats.grad_elems * szg / 1e9),
-                   "parallelism": f"MiCS p={wl.p} x {n // wl.p} replicas"},
+                   "parallelism": f"MiCS p={wl.p} x {n // wl.p} replicas", "schedule": args.schedule},
         "roofline": roof,
         "phases_ms": {k: v[0] for k, v in phases.items()},
         "per_rank_bytes": {"allgather_in": stats.ag_bytes_in, "reducescatter_in": stats.rs_bytes_in,

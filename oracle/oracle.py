@@ -67,6 +67,13 @@ class Oracle:
         L = self.lib
         L.ora_splitmix64.restype = C.c_uint64
         L.ora_splitmix64.argtypes = [C.c_uint64]
+        L.ora_f32_to_bf16.restype = C.c_uint16
+        L.ora_f32_to_bf16.argtypes = [C.c_float]
+
+    def f32_to_bf16(self, a):
+        """Round-to-nearest-even bf16 of every element (ora_f32_to_bf16)."""
+        a = np.ascontiguousarray(a, np.float32).ravel()
+        return np.array([self.lib.ora_f32_to_bf16(float(x)) for x in a], np.uint16)
 
     # ---- generators
     def random_shards(self, count, chunk, seed):

@@ -43,7 +43,7 @@ constexpr int kThreads = 256;    // threads per CTA for every data kernel
 constexpr int kCopyUnroll = 8;   // 16 B vectors in flight per thread per tile
 constexpr uint32_t kCopyTile = kThreads * kCopyUnroll * 16;  // 32 KiB
 constexpr int kRedUnroll = 4;    // vectors per thread per tile (per source)
-constexpr int kAdamUnroll = 2;
+constexpr int kAdamUnroll = 4;
 constexpr int kSmemTable = 16384;  // descriptor tables up to this size are staged in shared memory
 
 struct CopySeg {              // 64 B

@@ -441,7 +441,40 @@ __global__ void __launch_bounds__(kThreads) k_adam(const AdamJob* __restrict__ j
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const AdamJob& J = jobs[find_desc(jobs, njobs, tile)];
     const uint64_t e0 = uint64_t(tile - J.tile0) * kAdamTile;
+    if (e0 + kAdamTile <= J.elems) {
+      // full tile: every load of the tile (the reduced gradient, mostly from NVLink
+      // peers, and the local p, m, v) is issued before the first update
+      uint4 gr[kAdamUnroll];
+      float4 p[kAdamUnroll], m[kAdamUnroll], v[kAdamUnroll];
 #pragma unroll
+      for (int u = 0; u < kAdamUnroll; ++u) {
+        const uint64_t e = e0 + uint64_t(u * kThreads + threadIdx.x) * 4;
+        gr[u] = ld_stream(J.srcs[uint32_t(e / J.sub)] + e);  // sub % 4 == 0: one owner per vector
+        p[u] = *reinterpret_cast<const float4*>(J.param + e);
+        m[u] = *reinterpret_cast<const float4*>(J.m + e);
+        v[u] = *reinterpret_cast<const float4*>(J.v + e);
+      }
+#pragma unroll
+      for (int u = 0; u < kAdamUnroll; ++u) {
+        const uint64_t e = e0 + uint64_t(u * kThreads + threadIdx.x) * 4;
+        adam_one(__uint_as_float(gr[u].x), p[u].x, m[u].x, v[u].x, sc);
+        adam_one(__uint_as_float(gr[u].y), p[u].y, m[u].y, v[u].y, sc);
+        adam_one(__uint_as_float(gr[u].z), p[u].z, m[u].z, v[u].z, sc);
+        adam_one(__uint_as_float(gr[u].w), p[u].w, m[u].w, v[u].w, sc);
+        *reinterpret_cast<float4*>(J.param + e) = p[u];
+        *reinterpret_cast<float4*>(J.m + e) = m[u];
+        *reinterpret_cast<float4*>(J.v + e) = v[u];
+        if (J.pbf16) {
+          uint2 pk;
+          pk.x = uint32_t(f32_to_bf16(p[u].x)) | (uint32_t(f32_to_bf16(p[u].y)) << 16);
+          pk.y = uint32_t(f32_to_bf16(p[u].z)) | (uint32_t(f32_to_bf16(p[u].w)) << 16);
+          *reinterpret_cast<uint2*>(J.pbf16 + e) = pk;
+        }
+        if (J.gout) st_vec(J.gout + e, gr[u]);
+      }
+      continue;
+    }
+#pragma unroll 1
     for (int u = 0; u < kAdamUnroll; ++u) {
       const uint64_t e = e0 + uint64_t(u * kThreads + threadIdx.x) * 4;
       if (e >= J.elems) continue;

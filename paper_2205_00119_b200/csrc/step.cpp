@@ -33,7 +33,8 @@ constexpr uint32_t kAlignElems = 8;
 void release(mics_step* st) {
   for (auto& v : st->ag)
     for (auto& l : v) l.release();
-  for (auto& l : st->rs) l.release();
+  for (auto& v : st->micro)
+    for (auto& l : v) l.release();
   st->bnd.rs.release();
   st->bnd.ag.release();
 }
@@ -140,9 +141,13 @@ void enqueue_gathers(mics_step* st, int t) {
     for (auto& x : st->ag[l]) enqueue(st->ctx, x);
 }
 
+void enqueue_sync(mics_step* st, int t) {
+  for (auto& x : st->micro[size_t(t)]) enqueue(st->ctx, x);
+}
+
 void enqueue_micro(mics_step* st, int t) {
   enqueue_gathers(st, t);
-  enqueue(st->ctx, st->rs[size_t(t)]);
+  enqueue_sync(st, t);
 }
 }  // namespace
 
@@ -154,7 +159,6 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
       raise(MICS_SHAPE_ERROR, "partition size p=" + std::to_string(cfg->p) + " is not node-aligned for k=" +
                                   std::to_string(cfg->hier_k));
   }
-  if (cfg->alternative) raise(MICS_CONFIG_ERROR, "the step driver runs the 2-hop schedule (use mics_sync_alt_step)");
   auto* st = new mics_step();
   try {
     st->ctx = ctx;
@@ -188,10 +192,14 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
       for (int t = 0; t < cfg->s; ++t) enqueue_generate(st, t);
     // plans
     for (int l = 0; l < cfg->nlayers; ++l) st->ag.push_back(build_layer_ag(st, l));
-    for (int t = 0; t < cfg->s; ++t)
-      st->rs.push_back(build_micro_launch(sy, st->grads, cfg->resident_grads ? uint64_t(t) * sy->grad_elems * szg : 0,
-                                          cfg->grad_t, 1.0, t == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE, true,
-                                          false, 1, 1));
+    for (int t = 0; t < cfg->s; ++t) {
+      const uint64_t goff = cfg->resident_grads ? uint64_t(t) * sy->grad_elems * szg : 0;
+      const int mode = t == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE;
+      if (cfg->alternative)  // DeepSpeed default (sync_schedule.hpp:189-224): all-reduce over all n
+        st->micro.push_back(build_alt(sy, st->grads, goff, cfg->grad_t, 1.0, true, mode));
+      else  // 2-hop hop 1: reduce-scatter inside the partition group
+        st->micro.push_back({build_micro_launch(sy, st->grads, goff, cfg->grad_t, 1.0, mode, true, false, 1, 1)});
+    }
     st->adam.lr = cfg->lr;
     st->adam.beta1 = cfg->beta1;
     st->adam.beta2 = cfg->beta2;
@@ -204,7 +212,27 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     st->adam.exp_avg_sq = st->v;
     st->adam.param_bf16 = st->pbf16;
     st->adam.write_grad = 0;
-    st->bnd = build_boundary(sy, &st->adam, true, false);
+    if (!cfg->alternative) {
+      st->bnd = build_boundary(sy, &st->adam, true, false);
+    } else {  // shards already hold the global sum: the boundary is Adam on the own shard
+      AdamPlan ap;
+      uint64_t pmask = 0;
+      for (int g = 0; g < sy->n / sy->p; ++g) {
+        std::vector<int> ranks(static_cast<size_t>(sy->p));
+        for (int i = 0; i < sy->p; ++i) ranks[size_t(i)] = g * sy->p + i;
+        pmask |= ctx->peer_mask(ranks.data(), sy->p);
+      }
+      for (int r = 0; r < ctx->n; ++r) {
+        if (!ctx->local(r)) continue;
+        ap.add({ctx->rank_ptr(sy->shard, r)}, reinterpret_cast<float*>(ctx->rank_ptr(st->master, r)),
+               reinterpret_cast<float*>(ctx->rank_ptr(st->m, r)), reinterpret_cast<float*>(ctx->rank_ptr(st->v, r)),
+               reinterpret_cast<uint16_t*>(ctx->rank_ptr(st->pbf16, r)), nullptr, S, round_up(S, 4));
+      }
+      st->bnd.ag = make_adam_launch(ctx, ap, make_adam_scalars(cfg->lr, cfg->beta1, cfg->beta2, cfg->eps,
+                                                               cfg->weight_decay, 1, st->adam.grad_scale),
+                                    ctx->barrier(pmask, 0, 1), true);
+      st->bnd.has_ag = true;
+    }
     // stats (per rank per step), algorithmic bytes of SURVEY §8(d)
     const int p = sy->p, r = sy->n / p;
     uint64_t csum = 0;
@@ -230,11 +258,12 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
         S2.ag_remote_bytes += 2 * uint64_t(cfg->s) * x.remote_bytes;
         S2.ag_hbm_bytes += 2 * uint64_t(cfg->s) * x.hbm_bytes;
       }
-    for (auto& x : st->rs) {
-      S2.rs_launches += runs(x);
-      S2.rs_remote_bytes += x.remote_bytes;
-      S2.rs_hbm_bytes += x.hbm_bytes;
-    }
+    for (auto& v : st->micro)
+      for (auto& x : v) {
+        S2.rs_launches += runs(x);
+        S2.rs_remote_bytes += x.remote_bytes;
+        S2.rs_hbm_bytes += x.hbm_bytes;
+      }
     for (const Launch* x : {&st->bnd.rs, &st->bnd.ag}) {
       if ((x == &st->bnd.rs && !st->bnd.has_rs) || (x == &st->bnd.ag && !st->bnd.has_ag)) continue;
       S2.bnd_launches += runs(*x);
@@ -283,7 +312,7 @@ void step_profile(mics_step* st, double* ag_ms, double* rs_ms, double* bnd_ms, d
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
     enqueue_gathers(st, t);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
-    enqueue(ctx, st->rs[size_t(t)]);
+    enqueue_sync(st, t);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
   }
   MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));

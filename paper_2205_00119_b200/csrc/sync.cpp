@@ -220,12 +220,10 @@ void boundary(mics_sync* st, const mics_adam* adam) {
 }
 
 // ---- alternative (DeepSpeed-default) schedule: all-reduce over all n ranks
-void alt_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale) {
-  check_window(st, false);
-  if (!(grad_t == st->acc_t || (grad_t == MICS_BF16 && st->acc_t == MICS_F32)))
-    raise(MICS_TYPE_MISMATCH, "gradient type does not match the shard type");
-  if (goff + st->grad_elems * dtype_size(grad_t) > grads.stride)
-    raise(MICS_SIZE_MISMATCH, "gradient buffer smaller than the padded gradient layout");
+// RS over all n ranks into the scratch buffer, AG of the reduced slices, then
+// the owned chunk is accumulated into the shard (sync_schedule.hpp:189-224).
+std::vector<Launch> build_alt(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale,
+                              bool persistent, int acc_mode) {
   mics_ctx* ctx = st->ctx;
   const int n = st->n, p = st->p;
   const uint64_t szg = dtype_size(grad_t), sza = dtype_size(st->acc_t);
@@ -257,21 +255,42 @@ void alt_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, d
       const uint64_t len = st->len[size_t(q)];
       rs.add(srcs, ctx->rank_ptr(st->alt, rho) + (st->alt_off[size_t(q)] + first) * sza, elems,
              len > first ? len - first : 0);
+      std::vector<std::pair<const void*, std::vector<void*>>> items;
+      uint64_t e2 = 0;
       for (int i = 0; i < n; ++i) {
         if (i == rho) continue;
         const uint64_t f2 = uint64_t(i) * sub;
-        const uint64_t e2 = f2 < total ? std::min(sub, total - f2) : 0;
+        const uint64_t ei = f2 < total ? std::min(sub, total - f2) : 0;
         const uint64_t o = (st->alt_off[size_t(q)] + f2) * sza;
-        ag.add(ctx->rank_ptr(st->alt, i) + o, {ctx->rank_ptr(st->alt, rho) + o}, e2 * sza);
+        if (ei == sub) items.push_back({ctx->rank_ptr(st->alt, i) + o, {ctx->rank_ptr(st->alt, rho) + o}});
+        else ag.add(ctx->rank_ptr(st->alt, i) + o, {ctx->rank_ptr(st->alt, rho) + o}, ei * sza);  // ragged last slice
+        e2 = sub;
       }
+      ag.add_group(items, e2 * sza);
       const uint64_t c = st->chunk[size_t(q)];
       acc.add({ctx->rank_ptr(st->alt, rho) + (st->alt_off[size_t(q)] + uint64_t(rho % p) * c) * sza},
               ctx->rank_ptr(st->shard, rho) + st->shard_off[size_t(q)] * sza, c, c);
     }
   }
-  enqueue(ctx, make_reduce_launch(ctx, rs, grad_t, st->acc_t, scale, MICS_RS_STORE, ctx->barrier(mask, 1, 1), false));
-  enqueue(ctx, make_copy_launch(ctx, ag, ctx->barrier(mask, 0, 1), false));
-  enqueue(ctx, make_reduce_launch(ctx, acc, st->acc_t, st->acc_t, 1.0, MICS_RS_ACCUMULATE, ctx->barrier(0, 0, 0), false));
+  std::vector<Launch> out;
+  out.push_back(make_reduce_launch(ctx, rs, grad_t, st->acc_t, scale, MICS_RS_STORE, ctx->barrier(mask, 1, 1),
+                                   persistent));
+  out.push_back(make_copy_launch(ctx, ag, ctx->barrier(mask, 0, 1), persistent));
+  out.push_back(make_reduce_launch(ctx, acc, st->acc_t, st->acc_t, 1.0, acc_mode, ctx->barrier(0, 0, 0),
+                                   persistent));
+  return out;
+}
+
+void alt_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale) {
+  check_window(st, false);
+  if (!(grad_t == st->acc_t || (grad_t == MICS_BF16 && st->acc_t == MICS_F32)))
+    raise(MICS_TYPE_MISMATCH, "gradient type does not match the shard type");
+  if (goff + st->grad_elems * dtype_size(grad_t) > grads.stride)
+    raise(MICS_SIZE_MISMATCH, "gradient buffer smaller than the padded gradient layout");
+  mics_ctx* ctx = st->ctx;
+  const int n = st->n;
+  const uint64_t szg = dtype_size(grad_t);
+  for (const Launch& l : build_alt(st, grads, goff, grad_t, scale, false, MICS_RS_ACCUMULATE)) enqueue(ctx, l);
   const uint64_t padded = ceil_div(st->grad_elems, uint64_t(n)) * uint64_t(n);  // :200-201
   for (int a = 0; a < n; ++a)
     for (int b = 0; b < n; ++b)

@@ -40,6 +40,8 @@ BoundaryLaunches build_boundary(mics_sync* st, const mics_adam* adam, bool persi
 void micro_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode);
 void boundary(mics_sync* st, const mics_adam* adam);
 void alt_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale);
+std::vector<Launch> build_alt(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale,
+                              bool persistent, int acc_mode);
 void alt_boundary(mics_sync* st);
 
 }  // namespace mics
@@ -53,7 +55,9 @@ struct mics_step {
   mics_buf pbf16{}, master{}, m{}, v{}, gathered{}, grads{};
   uint64_t gathered_half = 0;                 // bytes of one gathered buffer
   std::vector<std::vector<mics::Launch>> ag;  // per layer: 1 launch (flat) or 2 (hierarchical)
-  std::vector<mics::Launch> rs;               // per micro-step
+  // per micro-step: the 2-hop reduce-scatter, or the alternative schedule's
+  // all-n reduce-scatter + all-gather + owned-chunk accumulate
+  std::vector<std::vector<mics::Launch>> micro;
   mics::BoundaryLaunches bnd;
   mics_adam adam{};
   int adam_step = 0;

@@ -50,6 +50,7 @@ def workloads() -> dict:
 @dataclass
 class StepOptions:
     resident_grads: bool = True
+    alternative: bool = False     # DeepSpeed-default global all-reduce every micro-step instead of 2-hop
     seed: int = 2205
     lr: float = 1e-4
     beta1: float = 0.9
@@ -67,7 +68,8 @@ class MicsStep:
         self.opts = opts
         self._layers = (C.c_uint64 * len(wl.layer_params))(*wl.layer_params)
         cfg = StepCfg(wl.p, wl.s, len(wl.layer_params), C.cast(self._layers, C.POINTER(C.c_uint64)),
-                      DTYPE[wl.grad_dtype], wl.hier_k, int(opts.resident_grads), 0, opts.seed, opts.lr, opts.beta1,
+                      DTYPE[wl.grad_dtype], wl.hier_k, int(opts.resident_grads), int(opts.alternative), opts.seed,
+                      opts.lr, opts.beta1,
                       opts.beta2, opts.eps, opts.weight_decay)
         h = C.c_void_p()
         check(lib.mics_step_create(engine.ctx, C.byref(cfg), C.byref(h)))

@@ -1,0 +1,121 @@
+"""GPU parity of the MiCS step driver (csrc/step.cpp) against a restatement of the
+step on the CPU: per-layer all-gathers, s micro-step reduce-scatters with the
+pinned fold order, the boundary replication-group fold and the documented Adam —
+bit-exact, for the 2-hop schedule, the alternative (global all-reduce) schedule,
+bf16 gradients and the hierarchical all-gather.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def u32(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+def bf16_to_f32(b):
+    return (b.astype(np.uint32) << 16).view(np.float32)
+
+
+def expected_step(oracle, n, p, s, segs, grad_dtype, seed, alternative, opts):
+    """Returns per-rank (master, m, v, param_bf16) after one step, and the initial bf16 params."""
+    S = sum(c for _, c, _, _ in segs)
+    G = sum(p * c for _, c, _, _ in segs)
+    grads = np.zeros((s, n, G), np.float32)
+    for t in range(s):
+        for r in range(n):
+            if grad_dtype == "bf16":
+                grads[t, r] = bf16_to_f32(oracle.gen_bf16(seed, r, t, 0, 0, G))
+            else:
+                grads[t, r] = oracle.gen_f32(seed, r, t, 0, 0, G)
+    acc = np.zeros((n, S), np.float32)
+    for r in range(n):
+        j, g = r % p, r // p
+        for t in range(s):
+            fold = np.zeros(S, np.float32)
+            for ln, c, so, go in segs:
+                e = np.arange(c)
+                valid = (j * c + e) < ln
+                if alternative:  # all-reduce over all n ranks, ascending rank
+                    f = grads[t, 0, go + j * c + e].copy()
+                    for i in range(1, n):
+                        f = f + grads[t, i, go + j * c + e]
+                else:  # reduce-scatter in the partition group, ascending position
+                    f = grads[t, g * p + 0, go + j * c + e].copy()
+                    for i in range(1, p):
+                        f = f + grads[t, g * p + i, go + j * c + e]
+                fold[so:so + c] = np.where(valid, f, np.float32(0))
+            acc[r] = (np.float32(0) + fold) if t == 0 else (acc[r] + fold)
+    red = np.zeros_like(acc)
+    for r in range(n):
+        if alternative:
+            red[r] = acc[r]
+        else:  # boundary all-reduce in the replication group, ascending position
+            j = r % p
+            f = acc[j].copy()
+            for q in range(1, n // p):
+                f = f + acc[j + q * p]
+            red[r] = f
+    out, init = [], []
+    for r in range(n):
+        m0 = oracle.gen_f32(seed ^ 0x5EED, r % p, 0, 255, 0, S)
+        init.append(m0)
+        out.append(oracle.adam(m0, np.zeros(S), np.zeros(S), red[r], opts.lr, opts.beta1, opts.beta2, opts.eps,
+                               opts.weight_decay, 1, 1.0 / (n * s), want_bf16=True))
+    return out, init
+
+
+@pytest.mark.parametrize("alternative,grad_dtype,hier_k,p", [
+    (False, "f32", 0, 2), (True, "f32", 0, 2), (False, "bf16", 0, 4), (False, "f32", 2, 4), (True, "bf16", 0, 8)])
+def test_step_matches_cpu_restatement(oracle, alternative, grad_dtype, hier_k, p):
+    from paper_2205_00119_b200.engine import Engine
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
+    n, s = 8, 3
+    layers = [10_000, 4_099, 777, 65_536]
+    wl = Workload("test", layers, p=p, s=s, grad_dtype=grad_dtype, hier_k=hier_k)
+    opts = StepOptions(resident_grads=not alternative, alternative=alternative, seed=77, lr=1e-3, weight_decay=0.01)
+    eng = Engine(n_ranks=n, device=0, arena_bytes=256 << 20)
+    step = MicsStep(eng, wl, opts)
+    info, segs = step.sync_info()
+    bufs = step.buffers()
+    S = info.shard_elems
+    step.run(1)
+    eng.synchronize()
+    want, init = expected_step(oracle, n, p, s, segs, grad_dtype, 77, alternative, opts)
+    for r in range(n):
+        wp, wm, wv, wb = want[r]
+        assert np.array_equal(u32(eng.d2h(bufs["master"], r, S)), u32(wp)), r
+        assert np.array_equal(u32(eng.d2h(bufs["exp_avg"], r, S)), u32(wm)), r
+        assert np.array_equal(u32(eng.d2h(bufs["exp_avg_sq"], r, S)), u32(wv)), r
+        assert np.array_equal(eng.d2h(bufs["param_bf16"], r, S, "bf16"), wb), r
+    # the last gathered layer (layer 0, backward pass) holds the pre-update bf16 params of the group
+    ln0, c0, so0, _ = segs[0]
+    for r in range(n):
+        g = r // p
+        got = eng.d2h(bufs["gathered"], r, p * c0, "bf16")
+        for i in range(p):
+            src = init[g * p + i][so0:so0 + c0]
+            want_bf = oracle.f32_to_bf16(src)
+            assert np.array_equal(got[i * c0:(i + 1) * c0], want_bf), (r, i)
+    stats = step.stats()
+    assert stats.launches > 0 and stats.ag_launches == 2 * s * len(layers) * (2 if hier_k and p > hier_k else 1)
+    step.close()
+    eng.close()
+
+
+def test_step_two_steps_deterministic(oracle):
+    """Two steps, twice: identical bits (the step is deterministic and replayable)."""
+    from paper_2205_00119_b200.engine import Engine
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
+    wl = Workload("det", [50_000, 12_345], p=2, s=2)
+    res = []
+    for _ in range(2):
+        eng = Engine(n_ranks=8, device=0, arena_bytes=128 << 20)
+        step = MicsStep(eng, wl, StepOptions(seed=5))
+        step.run(2)
+        eng.synchronize()
+        res.append(eng.d2h(step.buffers()["master"], 3, step.sync_info()[0].shard_elems))
+        step.close()
+        eng.close()
+    assert np.array_equal(u32(res[0]), u32(res[1]))
