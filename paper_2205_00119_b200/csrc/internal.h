@@ -136,6 +136,7 @@ struct mics_ctx {
   int blocks_per_sm = 4;
   // resident CTAs/SM per kernel: copy, adam, reduce by [input dtype][source class 2/4/8/9]
   int occ_copy = 2, occ_adam = 4, occ_reduce[4][4] = {};
+  int occ_copy_indep = 1;  // CTAs/SM of barrier-free gathers chained with PDL
   int reduce_occ(mics_dtype t, uint32_t max_p) const {
     const int pc = mics::reduce_class(max_p);
     return occ_reduce[t][pc == 2 ? 0 : pc == 4 ? 1 : pc == 8 ? 2 : 3];

@@ -65,6 +65,7 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l) {
     // reduce-scatter and Adam barriers order every write against these reads
     Launch l = make_copy_launch(ctx, plan, ctx->barrier(0, 0, 0), true);
     l.bar.dep_first = 0;  // independent of the previous layer's gather: overlaps its tail (PDL)
+    l.grid = ctx->grid_for(plan.tiles, ctx->occ_copy_indep);
     out.push_back(l);
     return out;
   }
