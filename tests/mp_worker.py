@@ -12,6 +12,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 
 def main():
@@ -141,6 +142,29 @@ def main():
 
     eng.synchronize()
     eng.close()
+
+    # ---- the MiCS step driver across processes: 2-hop (flat + hierarchical) and the
+    # alternative schedule, bit-exact against the CPU restatement of the step
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
+    from test_gpu_step import expected_step
+    for p, k, alt, gdt in ((2, 0, False, "f32"), (4, 2, False, "bf16"), (4, 0, True, "f32"), (8, 0, False, "f32")):
+        e2 = Engine(n_ranks=n, world=world, world_rank=rank, device=local, arena_bytes=256 << 20)
+        mdist.connect(e2)
+        wl = Workload("mp", [20_000, 4_099, 65_536], p=p, s=2, grad_dtype=gdt, hier_k=k)
+        opts = StepOptions(resident_grads=not alt, alternative=alt, seed=91, lr=1e-3)
+        step = MicsStep(e2, wl, opts)
+        info, segs = step.sync_info()
+        bufs = step.buffers()
+        step.run(1)
+        e2.synchronize()
+        want, _ = expected_step(ora, n, p, 2, segs, gdt, 91, alt, opts)
+        for r in e2.local_ranks:
+            got = e2.d2h(bufs["master"], r, info.shard_elems)
+            expect(np.array_equal(got.view(np.uint32), want[r][0].view(np.uint32)),
+                   f"step p={p} k={k} alt={alt} {gdt} r={r}")
+        step.close()
+        e2.close()
+
     dist.barrier()
     if fails:
         print(f"[rank {rank}] FAILED: {fails}", flush=True)
