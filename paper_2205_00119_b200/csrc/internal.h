@@ -85,6 +85,28 @@ struct AdamScalars {
   float b1, omb1, b2, omb2, eps, wd, step_size, bc2_sqrt, grad_scale;
 };
 
+// Fused boundary (K5): one local rank's replication-group reduce-scatter of its
+// slice, then Adam over its whole shard, pulling each slice as soon as its owner
+// has published that tile (per-tile flags), so NVLink pulls, the folds and Adam's
+// HBM traffic overlap inside one kernel.
+constexpr uint32_t kBndTile = kThreads * 4 * 4;  // 4096 fp32 elements
+constexpr uint32_t kBndBlockTiles = 32;            // tiles per published block (512 KiB): one flag per block
+constexpr uint64_t kBndBlock = uint64_t(kBndTile) * kBndBlockTiles;
+struct BndJob {
+  const void* const* ptrs;    // [0, r): member shard bases; [r, 2r): member flag arrays
+  float* own;                 // this rank's shard (its slice is reduced in place)
+  float* param;
+  float* m;
+  float* v;
+  uint16_t* pbf16;            // nullable
+  float* gout;                // nullable: also leave the reduced gradient in the shard
+  uint64_t* my_flags;         // [r][nblk], written by the slice owners
+  uint64_t elems;             // shard elements (Adam range)
+  uint64_t sub;               // slice length, a multiple of kBndTile
+  uint32_t r, pos, nblk;
+  uint32_t rs_tile0, ad_tile0, pad_;
+};
+
 // Flag barrier between processes: remote_flag[w] is the slot on process w's
 // arena reserved for this process; local_flag[w] is the slot process w writes
 // on ours.  Values are monotone barrier counts per process pair.
@@ -124,6 +146,8 @@ void launch_generate(cudaStream_t s, void* out, mics_dtype dtype, uint64_t seed,
                      uint64_t start, uint64_t count, int grid);
 void launch_cast_bf16(cudaStream_t s, const float* in, uint16_t* out, uint64_t count, int grid);
 void launch_barrier(cudaStream_t s, const BarrierArg& bar);
+void launch_boundary(cudaStream_t s, const BndJob* jobs, int njobs, uint32_t rs_tiles, uint32_t ntiles, int grid,
+                     const AdamScalars& sc, uint64_t epoch, const BarrierArg& bar);
 
 AdamScalars make_adam_scalars(double lr, double b1, double b2, double eps, double wd, int step, double grad_scale);
 
@@ -137,6 +161,7 @@ struct mics_ctx {
   // resident CTAs/SM per kernel: copy, adam, reduce by [input dtype][source class 2/4/8/9]
   int occ_copy = 2, occ_adam = 4, occ_reduce[4][4] = {};
   int occ_copy_indep = 1;  // CTAs/SM of barrier-free gathers chained with PDL
+  int occ_bnd = 1;         // CTAs/SM of the fused boundary (all CTAs must be co-resident)
   int reduce_occ(mics_dtype t, uint32_t max_p) const {
     const int pc = mics::reduce_class(max_p);
     return occ_reduce[t][pc == 2 ? 0 : pc == 4 ? 1 : pc == 8 ? 2 : 3];
@@ -225,7 +250,9 @@ struct AdamPlan {
 
 // A device-resident, replayable launch (built once, launched many times).
 struct Launch {
-  enum Kind { COPY, REDUCE, ADAM, BARRIER } kind = COPY;
+  enum Kind { COPY, REDUCE, ADAM, BARRIER, BOUNDARY } kind = COPY;
+  uint32_t rs_tiles = 0;   // BOUNDARY: tiles of the reduce-scatter phase
+  uint64_t epoch = 0;      // BOUNDARY: flag value of this launch (monotone per sync state)
   void* d_desc = nullptr;  // owned device table (cudaMalloc)
   uint64_t table_bytes = 0;
   uint32_t max_p = 1;
@@ -247,6 +274,9 @@ Launch make_reduce_launch(mics_ctx* ctx, const RedPlan& plan, mics_dtype in_t, m
                           const BarrierArg& bar, bool persistent);
 Launch make_adam_launch(mics_ctx* ctx, const AdamPlan& plan, const AdamScalars& sc, const BarrierArg& bar,
                         bool persistent);
+// jobs[i].ptrs is patched to point at ptrs[i] (2r entries) in the uploaded table
+Launch make_boundary_launch(mics_ctx* ctx, std::vector<BndJob> jobs, const std::vector<std::vector<const void*>>& ptrs,
+                            const AdamScalars& sc, const BarrierArg& bar, bool persistent);
 // dep_first: -1 = as planned, 0/1 = override BarrierArg::dep_first for this launch
 void enqueue(mics_ctx* ctx, const Launch& l, int dep_first = -1);
 

@@ -546,6 +546,147 @@ __global__ void __launch_bounds__(kThreads) k_cast_bf16(const float* in, uint16_
     out[i] = f32_to_bf16(in[i]);
 }
 
+// ---------------------------------------------------------------- K5': fused boundary
+// Data another GPU writes during this kernel (published by a flag) is read with a
+// coherent load, never through the non-coherent path.
+__device__ __forceinline__ uint4 ld_coherent(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+
+// Work items are blocks of kBndBlockTiles tiles.  Items [0, rs_items): the
+// reduce-scatter of each local rank's slice (fold over the r replication positions
+// in ascending order, stored in place), then one release flag per block into every
+// replica's flag array.  Items [rs_items, nitems): Adam over every local rank's
+// shard, each block waiting for its slice owner's flag.  All reduce-scatter items
+// precede all Adam items in every CTA's grid-stride order and the grid is one
+// resident wave, so every awaited flag is produced by a running CTA.
+__device__ __forceinline__ void bnd_reduce_tile(const BndJob& J, uint64_t e0) {
+  const uint32_t r = J.r;
+#pragma unroll 1
+  for (int h = 0; h < 4; h += 2) {  // 2 x (2 float4 per thread)
+    uint4 raw[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < int(r)) {
+        const float* s = static_cast<const float*>(J.ptrs[q]);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) raw[q][u] = ld_stream(s + e0 + (uint64_t(h + u) * kThreads + threadIdx.x) * 4);
+      }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      float a[4];
+      Codec<float, float>::unpack(raw[0][u], a);
+#pragma unroll
+      for (int q = 1; q < 8; ++q)
+        if (q < int(r)) {
+          float x[4];
+          Codec<float, float>::unpack(raw[q][u], x);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) a[k] = __fadd_rn(a[k], x[k]);
+        }
+      *reinterpret_cast<float4*>(J.own + e0 + (uint64_t(h + u) * kThreads + threadIdx.x) * 4) =
+          make_float4(a[0], a[1], a[2], a[3]);
+    }
+  }
+}
+
+__device__ __forceinline__ void bnd_adam_tile(const BndJob& J, const float* g, uint64_t e0, const AdamScalars& sc) {
+  if (e0 + kBndTile <= J.elems) {
+#pragma unroll 1
+    for (int h = 0; h < 4; h += 2) {
+      uint4 gr[2];
+      float4 p[2], m[2], v[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint64_t e = e0 + (uint64_t(h + u) * kThreads + threadIdx.x) * 4;
+        gr[u] = ld_coherent(g + e);
+        p[u] = *reinterpret_cast<const float4*>(J.param + e);
+        m[u] = *reinterpret_cast<const float4*>(J.m + e);
+        v[u] = *reinterpret_cast<const float4*>(J.v + e);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint64_t e = e0 + (uint64_t(h + u) * kThreads + threadIdx.x) * 4;
+        adam_one(__uint_as_float(gr[u].x), p[u].x, m[u].x, v[u].x, sc);
+        adam_one(__uint_as_float(gr[u].y), p[u].y, m[u].y, v[u].y, sc);
+        adam_one(__uint_as_float(gr[u].z), p[u].z, m[u].z, v[u].z, sc);
+        adam_one(__uint_as_float(gr[u].w), p[u].w, m[u].w, v[u].w, sc);
+        *reinterpret_cast<float4*>(J.param + e) = p[u];
+        *reinterpret_cast<float4*>(J.m + e) = m[u];
+        *reinterpret_cast<float4*>(J.v + e) = v[u];
+        if (J.pbf16) {
+          uint2 pk;
+          pk.x = uint32_t(f32_to_bf16(p[u].x)) | (uint32_t(f32_to_bf16(p[u].y)) << 16);
+          pk.y = uint32_t(f32_to_bf16(p[u].z)) | (uint32_t(f32_to_bf16(p[u].w)) << 16);
+          *reinterpret_cast<uint2*>(J.pbf16 + e) = pk;
+        }
+        if (J.gout) st_vec(J.gout + e, gr[u]);
+      }
+    }
+  } else {
+    for (uint64_t x = e0 + threadIdx.x; x < J.elems && x < e0 + kBndTile; x += kThreads) {
+      const float gx = *reinterpret_cast<const volatile float*>(g + x);
+      float p = J.param[x], m = J.m[x], v = J.v[x];
+      adam_one(gx, p, m, v, sc);
+      J.param[x] = p;
+      J.m[x] = m;
+      J.v[x] = v;
+      if (J.pbf16) J.pbf16[x] = f32_to_bf16(p);
+      if (J.gout) J.gout[x] = gx;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_boundary(const BndJob* __restrict__ jobs, int njobs,
+                                                          uint32_t rs_items, uint32_t nitems, AdamScalars sc,
+                                                          uint64_t epoch, BarrierArg bar) {
+  constexpr uint64_t kBlock = uint64_t(kBndTile) * kBndBlockTiles;
+  pdl_begin(bar);
+  bar_entry(bar);
+  for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    if (item < rs_items) {
+      int j = 0;
+      while (j + 1 < njobs && jobs[j + 1].rs_tile0 <= item) ++j;
+      const BndJob& J = jobs[j];
+      const uint32_t b = item - J.rs_tile0;
+      const uint64_t e0 = uint64_t(J.pos) * J.sub + uint64_t(b) * kBlock;
+#pragma unroll 1
+      for (uint32_t t = 0; t < kBndBlockTiles; ++t) bnd_reduce_tile(J, e0 + uint64_t(t) * kBndTile);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (uint32_t q = 0; q < J.r; ++q)
+          st_release_sys(static_cast<uint64_t*>(const_cast<void*>(J.ptrs[J.r + q])) + uint64_t(J.pos) * J.nblk + b,
+                         epoch);
+      }
+    } else {
+      const uint32_t a = item - rs_items;
+      int j = 0;
+      while (j + 1 < njobs && jobs[j + 1].ad_tile0 <= a) ++j;
+      const BndJob& J = jobs[j];
+      const uint32_t t = a - J.ad_tile0, q = t / J.nblk;
+      const uint64_t e0 = uint64_t(t) * kBlock;  // slices are whole blocks: block t of the shard
+      if (threadIdx.x == 0)
+        while (ld_acquire_sys(J.my_flags + t) < epoch) __nanosleep(256);
+      __syncthreads();
+      const float* g = static_cast<const float*>(J.ptrs[q]);
+#pragma unroll 1
+      for (uint32_t k = 0; k < kBndBlockTiles; ++k) {
+        const uint64_t e = e0 + uint64_t(k) * kBndTile;
+        if (e >= J.elems) break;
+        bnd_adam_tile(J, g, e, sc);
+      }
+    }
+  }
+  bar_exit(bar);
+  pdl_end(bar);
+}
+
 __global__ void k_barrier(BarrierArg bar) {
   pdl_begin(bar);
   bar_entry(bar);
@@ -619,6 +760,9 @@ int resident_ctas(int kind, mics_dtype in_t, int pc) {
       else if (in_t == MICS_I64) n = reduce_occupancy<long long, long long>(pc);
       else n = reduce_occupancy<float, float>(pc);
       break;
+    case 3:
+      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_boundary, kThreads, 0));
+      break;
     default:
       MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_adam, kThreads, 0));
       break;
@@ -678,6 +822,11 @@ void launch_cast_bf16(cudaStream_t s, const float* in, uint16_t* out, uint64_t c
 
 void launch_barrier(cudaStream_t s, const BarrierArg& bar) {
   launch_ex(k_barrier, 1, 32, 0, s, bar);
+}
+
+void launch_boundary(cudaStream_t s, const BndJob* jobs, int njobs, uint32_t rs_tiles, uint32_t ntiles, int grid,
+                     const AdamScalars& sc, uint64_t epoch, const BarrierArg& bar) {
+  launch_ex(k_boundary, grid, kThreads, 0, s, jobs, njobs, rs_tiles, ntiles, sc, epoch, bar);  // items, not tiles
 }
 
 }  // namespace mics

@@ -139,6 +139,7 @@ mics_ctx* create_ctx(const mics_init_args* a) {
     if (const char* e = std::getenv("MICS_COPY_CTAS_PER_SM"))  // tuning knob
       c->occ_copy_indep = std::max(1, std::min(c->occ_copy, std::atoi(e)));
     c->occ_adam = resident_ctas(2, MICS_F32);
+    c->occ_bnd = resident_ctas(3, MICS_F32);
     const int classes[4] = {2, 4, 8, 9};
     for (int t = 0; t < 4; ++t)
       for (int k = 0; k < 4; ++k) c->occ_reduce[t][k] = resident_ctas(1, mics_dtype(t), classes[k]);

@@ -124,6 +124,7 @@ void enqueue_boundary(mics_step* st) {
   if (st->bnd.has_ag) {
     st->bnd.ag.adam = make_adam_scalars(st->cfg.lr, st->cfg.beta1, st->cfg.beta2, st->cfg.eps, st->cfg.weight_decay,
                                         st->adam_step, st->adam.grad_scale);
+    st->bnd.ag.epoch = ++st->sync->epoch;
     enqueue(ctx, st->bnd.ag);
   }
 }

@@ -15,6 +15,11 @@ struct mics_sync {
   mics_buf shard{};
   int micro_step = 0;
   std::vector<std::array<int64_t, 4>> events;
+  // fused boundary: per-tile publication flags [r][nblk] per rank (lazily allocated), monotone epoch
+  bool fusable = false;
+  bool bflags_ready = false;
+  mics_buf bflags{};
+  uint64_t epoch = 0;
   // alternative schedule scratch (lazily allocated)
   bool alt_ready = false;
   mics_buf alt{};

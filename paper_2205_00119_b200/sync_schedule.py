@@ -70,6 +70,7 @@ class SyncStates:
         self.engine = engine
         self.layout = layout
         self.dtype = dtype
+        self._mark0 = engine.mark()  # arena is a bump allocator: close() pops our allocations if on top
         lens = (C.c_uint64 * len(seg_lens))(*seg_lens)
         h = C.c_void_p()
         check(lib.mics_sync_create(engine.ctx, layout.p, s, len(seg_lens), lens, dtype_code(dtype), align_elems,
@@ -85,11 +86,22 @@ class SyncStates:
             check(lib.mics_sync_seg(self.h, i, C.byref(ln), C.byref(ch), C.byref(so), C.byref(go)))
             self.segs.append((ln.value, ch.value, so.value, go.value))
         self._grads = {}  # dtype -> staging Buf for the host drop-in calls
+        self._mark1 = engine.mark()
+
+    def _track(self, top_before: int):
+        """Calls may allocate lazily (staging, scratch, flags).  Our allocations stay
+        poppable only while nobody else allocated on top of them."""
+        if top_before == self._mark1:
+            self._mark1 = self.engine.mark()
+        else:
+            self._mark1 = -1  # interleaved with foreign allocations: never pop
 
     def close(self):
         if getattr(self, "h", None):
             check(lib.mics_sync_destroy(self.h))
             self.h = None
+            if self.engine.ctx and self.engine.mark() == self._mark1:
+                self.engine.release(self._mark0)
 
     def __del__(self):
         try:
@@ -124,10 +136,14 @@ class SyncStates:
                                        scale, mode))
 
     def alt_step_device(self, grads: Buf, grad_dtype: str | None = None, off: int = 0, scale: float = 1.0) -> None:
+        top = self.engine.mark()
         check(lib.mics_sync_alt_step(self.engine.ctx, self.h, grads, off, dtype_code(grad_dtype or self.dtype), scale))
+        self._track(top)
 
     def boundary(self, adam: Adam | None = None) -> None:
+        top = self.engine.mark()
         check(lib.mics_sync_boundary(self.engine.ctx, self.h, C.byref(adam) if adam is not None else None))
+        self._track(top)
 
     def alt_boundary(self) -> None:
         check(lib.mics_sync_alt_boundary(self.engine.ctx, self.h))
@@ -147,7 +163,9 @@ class SyncStates:
     def stage_grads(self, grads, dtype: str | None = None) -> Buf:
         dtype = dtype or self.dtype
         if dtype not in self._grads:
+            top = self.engine.mark()
             self._grads[dtype] = self.engine.alloc(self.grad_elems * DTYPE_SIZE[dtype])
+            self._track(top)
         buf = self._grads[dtype]
         if len(grads) != self.layout.n:
             raise_error(Errc.SizeMismatch, "gradient count does not match rank count")

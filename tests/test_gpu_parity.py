@@ -363,10 +363,14 @@ def test_generator_matches_oracle(m, engines, oracle):
     assert np.array_equal(eng.d2h(b, 1, 100_003, "bf16"), oracle.gen_bf16(77, 1, 2, 5, 0, 100_003))
 
 
-@pytest.mark.parametrize("wd", [0.0, 0.01])
-def test_boundary_fused_adam_bitexact(m, engines, oracle, wd):
+@pytest.mark.parametrize("wd,single_kernel", [(0.0, False), (0.01, False), (0.01, True)])
+def test_boundary_fused_adam_bitexact(m, engines, oracle, wd, single_kernel, monkeypatch):
+    """Boundary AR's all-gather fused with Adam; single_kernel = the opt-in one-kernel
+    K5' (reduce-scatter tiles publish per-block flags, Adam tiles consume them)."""
     from paper_2205_00119_b200.sync_schedule import AdamConfig, make_adam
-    n, p, s, length = 8, 2, 2, 300_001
+    monkeypatch.setenv("MICS_FUSED_BOUNDARY", "1" if single_kernel else "0")
+    n, p, s = 8, 2, 2
+    length = 2_000_003 if single_kernel else 300_001  # K5' needs >= one 512 KiB block per slice
     eng = engines(n)
     lay = m.build_group_layout(n, p)
     g = oracle.random_f32(s * n * length, -1.0, 1.0, 5).reshape(s, n, length)
