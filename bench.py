@@ -118,6 +118,8 @@ def arena_bytes(wl, per, resident, n=N_RANKS, alternative=False):
     per_rank = r * sub * 4 + S * 2 + 3 * S * 4 + gathered + (s if resident else 1) * p * S * szg
     if alternative:  # all-n reduce-scatter scratch: n slices of ceil(p*chunk/n) per layer
         per_rank += sum(-(-p * c // n) * n for c in chunks) * 4
+    elif os.environ.get("MICS_PIPELINE") == "1":  # pipelined boundary: second gradient accumulator
+        per_rank += r * (sub + 131072) * 4
     return per * (per_rank + 8 * 4096) + (256 << 20)
 
 

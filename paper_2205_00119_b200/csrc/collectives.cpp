@@ -240,7 +240,8 @@ Launch make_boundary_launch(mics_ctx* ctx, std::vector<BndJob> jobs, const std::
   return l;
 }
 
-void enqueue(mics_ctx* ctx, const Launch& l, int dep_first) {
+void enqueue(mics_ctx* ctx, const Launch& l, int dep_first, cudaStream_t stream) {
+  cudaStream_t st = stream ? stream : ctx->stream;
   // A launch without local work still runs (one CTA) when it carries a barrier:
   // the peers count on this process's signals.
   if (l.ndesc == 0 && l.bar.mask == 0) return;
@@ -249,20 +250,20 @@ void enqueue(mics_ctx* ctx, const Launch& l, int dep_first) {
   if (bar.mask) bar.dep_first = 1;  // barrier tickets: never overlap the predecessor
   switch (l.kind) {
     case Launch::COPY:
-      launch_copy(ctx->stream, static_cast<const CopySeg*>(l.d_desc), l.ndesc, l.ntiles, l.grid, bar);
+      launch_copy(st, static_cast<const CopySeg*>(l.d_desc), l.ndesc, l.ntiles, l.grid, bar);
       break;
     case Launch::REDUCE:
-      launch_reduce(ctx->stream, l.in_t, l.acc_t, static_cast<const RedJob*>(l.d_desc), l.ndesc, l.table_bytes,
+      launch_reduce(st, l.in_t, l.acc_t, static_cast<const RedJob*>(l.d_desc), l.ndesc, l.table_bytes,
                     l.max_p, l.ntiles, l.grid, l.scale, l.mode, bar);
       break;
     case Launch::ADAM:
-      launch_adam(ctx->stream, static_cast<const AdamJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid, l.adam, bar);
+      launch_adam(st, static_cast<const AdamJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid, l.adam, bar);
       break;
     case Launch::BARRIER:
-      launch_barrier(ctx->stream, bar);
+      launch_barrier(st, bar);
       break;
     case Launch::BOUNDARY:
-      launch_boundary(ctx->stream, static_cast<const BndJob*>(l.d_desc), l.ndesc, l.rs_tiles, l.ntiles, l.grid,
+      launch_boundary(st, static_cast<const BndJob*>(l.d_desc), l.ndesc, l.rs_tiles, l.ntiles, l.grid,
                       l.adam, l.epoch, bar);
       break;
   }

@@ -167,13 +167,18 @@ struct mics_ctx {
     return occ_reduce[t][pc == 2 ? 0 : pc == 4 ? 1 : pc == 8 ? 2 : 3];
   }
   cudaStream_t stream = nullptr;
+  // Barrier channels: each has its own flag slots, pairwise counters and CTA
+  // tickets, so two streams can run barrier kernels concurrently (channel c is
+  // only ever used from one stream, in the same order on every process).
+  static constexpr int kChannels = 2;
+  cudaStream_t side_stream = nullptr;  // channel 1: the step's pipelined boundary
   char* base = nullptr;           // local arena (IPC-exportable)
   uint64_t cap = 0, used = 0;
   char* peer_base[MICS_MAX_WORLD] = {};
   bool ipc_ready = false;
-  mics::PeerTab* d_tab = nullptr;
-  uint64_t* d_nbar = nullptr;
-  unsigned* d_tickets = nullptr;
+  mics::PeerTab* d_tab = nullptr;   // [kChannels]
+  uint64_t* d_nbar = nullptr;       // [kChannels][MICS_MAX_WORLD]
+  unsigned* d_tickets = nullptr;    // [kChannels][2]
   // descriptor ring for ad-hoc calls
   char* ring = nullptr;
   uint64_t ring_cap = 0, ring_head = 0;
@@ -200,11 +205,11 @@ struct mics_ctx {
   void* ring_put(const void* host, uint64_t bytes);
   void* ring_reserve(uint64_t bytes);
   void ring_upload(void* dev, const void* host, uint64_t bytes);
-  mics::BarrierArg barrier(uint64_t mask, int entry, int exit) const {
+  mics::BarrierArg barrier(uint64_t mask, int entry, int exit, int chan = 0) const {
     mics::BarrierArg b;
-    b.tab = d_tab;
-    b.nbar = d_nbar;
-    b.tickets = d_tickets;
+    b.tab = d_tab + chan;
+    b.nbar = d_nbar + chan * MICS_MAX_WORLD;
+    b.tickets = d_tickets + 2 * chan;
     b.mask = ipc_ready ? mask : 0;
     b.entry = entry;
     b.exit = exit;
@@ -278,7 +283,7 @@ Launch make_adam_launch(mics_ctx* ctx, const AdamPlan& plan, const AdamScalars& 
 Launch make_boundary_launch(mics_ctx* ctx, std::vector<BndJob> jobs, const std::vector<std::vector<const void*>>& ptrs,
                             const AdamScalars& sc, const BarrierArg& bar, bool persistent);
 // dep_first: -1 = as planned, 0/1 = override BarrierArg::dep_first for this launch
-void enqueue(mics_ctx* ctx, const Launch& l, int dep_first = -1);
+void enqueue(mics_ctx* ctx, const Launch& l, int dep_first = -1, cudaStream_t stream = nullptr);
 
 void check_group(const mics_ctx* ctx, const int* ranks, int p);
 }  // namespace mics

@@ -144,18 +144,21 @@ mics_ctx* create_ctx(const mics_init_args* a) {
     for (int t = 0; t < 4; ++t)
       for (int k = 0; k < 4; ++k) c->occ_reduce[t][k] = resident_ctas(1, mics_dtype(t), classes[k]);
     MICS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    MICS_CUDA(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
     c->cap = (a->arena_bytes ? a->arena_bytes : (1ull << 30)) + kFlagsBytes;
     c->cap = round_up(c->cap, 2ull << 20);
     MICS_CUDA(cudaMalloc(&c->base, c->cap));
     MICS_CUDA(cudaMemset(c->base, 0, kFlagsBytes));
     c->used = kFlagsBytes;
     c->peer_base[c->wrank] = c->base;
-    MICS_CUDA(cudaMalloc(&c->d_tab, sizeof(PeerTab)));
-    MICS_CUDA(cudaMemset(c->d_tab, 0, sizeof(PeerTab)));
-    MICS_CUDA(cudaMalloc(&c->d_nbar, sizeof(uint64_t) * MICS_MAX_WORLD));
-    MICS_CUDA(cudaMemset(c->d_nbar, 0, sizeof(uint64_t) * MICS_MAX_WORLD));
-    MICS_CUDA(cudaMalloc(&c->d_tickets, 2 * sizeof(unsigned)));
-    MICS_CUDA(cudaMemset(c->d_tickets, 0, 2 * sizeof(unsigned)));
+    constexpr int K = mics_ctx::kChannels;
+    static_assert(K * MICS_MAX_WORLD * sizeof(uint64_t) <= kFlagsBytes, "flag slots of every channel fit");
+    MICS_CUDA(cudaMalloc(&c->d_tab, K * sizeof(PeerTab)));
+    MICS_CUDA(cudaMemset(c->d_tab, 0, K * sizeof(PeerTab)));
+    MICS_CUDA(cudaMalloc(&c->d_nbar, K * sizeof(uint64_t) * MICS_MAX_WORLD));
+    MICS_CUDA(cudaMemset(c->d_nbar, 0, K * sizeof(uint64_t) * MICS_MAX_WORLD));
+    MICS_CUDA(cudaMalloc(&c->d_tickets, K * 2 * sizeof(unsigned)));
+    MICS_CUDA(cudaMemset(c->d_tickets, 0, K * 2 * sizeof(unsigned)));
     c->ring_cap = kRingBytes;
     MICS_CUDA(cudaMalloc(&c->ring, c->ring_cap));
     MICS_CUDA(cudaDeviceSynchronize());
@@ -170,6 +173,7 @@ void destroy_ctx(mics_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->side_stream) cudaStreamSynchronize(c->side_stream);
   for (int w = 0; w < c->world; ++w)
     if (w != c->wrank && c->peer_base[w]) cudaIpcCloseMemHandle(c->peer_base[w]);
   cudaFree(c->ring);
@@ -178,6 +182,7 @@ void destroy_ctx(mics_ctx* c) {
   cudaFree(c->d_tab);
   cudaFree(c->base);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
   delete c;
 }
 
@@ -199,14 +204,15 @@ void ipc_import(mics_ctx* c, const void* handles) {
     MICS_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     c->peer_base[w] = static_cast<char*>(p);
   }
-  PeerTab tab;
-  std::memset(&tab, 0, sizeof(tab));
-  for (int w = 0; w < c->world; ++w) {
-    // slot w on our arena is written by process w; slot wrank on process w's arena is ours
-    tab.local_flag[w] = reinterpret_cast<uint64_t*>(c->base) + w;
-    tab.remote_flag[w] = reinterpret_cast<uint64_t*>(c->peer_base[w]) + c->wrank;
-  }
-  MICS_CUDA(cudaMemcpy(c->d_tab, &tab, sizeof(tab), cudaMemcpyHostToDevice));
+  PeerTab tab[mics_ctx::kChannels];
+  std::memset(tab, 0, sizeof(tab));
+  for (int ch = 0; ch < mics_ctx::kChannels; ++ch)
+    for (int w = 0; w < c->world; ++w) {
+      // channel ch, slot w on our arena is written by process w; slot wrank on process w's arena is ours
+      tab[ch].local_flag[w] = reinterpret_cast<uint64_t*>(c->base) + ch * MICS_MAX_WORLD + w;
+      tab[ch].remote_flag[w] = reinterpret_cast<uint64_t*>(c->peer_base[w]) + ch * MICS_MAX_WORLD + c->wrank;
+    }
+  MICS_CUDA(cudaMemcpy(c->d_tab, tab, sizeof(tab), cudaMemcpyHostToDevice));
   c->ipc_ready = c->world > 1;
 }
 

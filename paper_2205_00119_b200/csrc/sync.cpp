@@ -84,9 +84,10 @@ mics_sync* sync_create(mics_ctx* ctx, int p, int s, int nseg, const uint64_t* se
 
 // ---- micro-step: one reduce launch over all partition groups and segments
 Launch build_micro_launch(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode,
-                          bool persistent, bool record, int entry, int exit) {
+                          bool persistent, bool record, int entry, int exit, const mics_buf* shard_override) {
   mics_ctx* ctx = st->ctx;
   const int p = st->p;
+  const mics_buf shard = shard_override ? *shard_override : st->shard;
   const uint64_t szg = dtype_size(grad_t), sza = dtype_size(st->acc_t);
   RedPlan plan(grad_t);
   uint64_t mask = 0;
@@ -108,8 +109,7 @@ Launch build_micro_launch(mics_sync* st, mics_buf grads, uint64_t goff, mics_dty
         for (int i = 0; i < p; ++i)
           srcs[size_t(i)] = ctx->rank_ptr(grads, g * p + i) + goff + (st->grad_off[size_t(q)] + first) * szg;
         const uint64_t len = st->len[size_t(q)];
-        plan.add(srcs, ctx->rank_ptr(st->shard, rank) + st->shard_off[size_t(q)] * sza, c,
-                 len > first ? len - first : 0);
+        plan.add(srcs, ctx->rank_ptr(shard, rank) + st->shard_off[size_t(q)] * sza, c, len > first ? len - first : 0);
       }
     }
   }
@@ -253,6 +253,61 @@ BoundaryLaunches build_boundary(mics_sync* st, const mics_adam* adam, bool persi
     out.ag = make_copy_launch(ctx, ag, ctx->barrier(rmask, 0, 1), persistent);
     out.has_ag = true;
   }
+  return out;
+}
+
+// The boundary restricted to shard elements [lo, hi) — one layer group of the step
+// driver's pipelined boundary — on accumulator buffer `shard` and barrier channel
+// `chan`.  Same fold order and Adam as build_boundary: the range is split into r
+// slices of ceil(len/r) (rounded to 4) and position i reduces slice i in place.
+BoundaryLaunches build_boundary_range(mics_sync* st, const mics_adam* adam, mics_buf shard, uint64_t lo, uint64_t hi,
+                                      int chan) {
+  mics_ctx* ctx = st->ctx;
+  const int n = st->n, p = st->p, r = n / p;
+  const uint64_t len = hi - lo;
+  const uint64_t subg = round_up(ceil_div(len, uint64_t(r)), 4);
+  BoundaryLaunches out;
+  uint64_t rmask = 0, pmask = 0;
+  for (int j = 0; j < p; ++j) {
+    const std::vector<int> ranks = iota_ranks(j, r, p);
+    rmask |= ctx->peer_mask(ranks.data(), r);
+  }
+  for (int g = 0; g < n / p; ++g) {
+    const std::vector<int> ranks = iota_ranks(g * p, p, 1);
+    pmask |= ctx->peer_mask(ranks.data(), p);
+  }
+  if (r > 1) {
+    RedPlan rs(MICS_F32);
+    for (int rho = 0; rho < n; ++rho) {
+      if (!ctx->local(rho)) continue;
+      const int j = rho % p, i = rho / p;
+      const uint64_t start = lo + uint64_t(i) * subg;
+      const uint64_t elems = start < hi ? std::min(subg, hi - start) : 0;
+      std::vector<const void*> srcs(static_cast<size_t>(r));
+      for (int q = 0; q < r; ++q) srcs[size_t(q)] = ctx->rank_ptr(shard, j + q * p) + start * 4;
+      rs.add(srcs, ctx->rank_ptr(shard, rho) + start * 4, elems, elems);
+    }
+    out.rs = make_reduce_launch(ctx, rs, MICS_F32, MICS_F32, 1.0, MICS_RS_STORE, ctx->barrier(rmask, 1, 1, chan), true);
+    out.has_rs = true;
+  }
+  AdamPlan ap;
+  for (int rho = 0; rho < n; ++rho) {
+    if (!ctx->local(rho)) continue;
+    const int j = rho % p;
+    std::vector<const void*> srcs(static_cast<size_t>(r));
+    for (int q = 0; q < r; ++q) srcs[size_t(q)] = ctx->rank_ptr(shard, j + q * p) + lo * 4;
+    uint16_t* pb = adam->param_bf16.stride ? reinterpret_cast<uint16_t*>(ctx->rank_ptr(adam->param_bf16, rho)) + lo
+                                           : nullptr;
+    ap.add(srcs, reinterpret_cast<float*>(ctx->rank_ptr(adam->param, rho)) + lo,
+           reinterpret_cast<float*>(ctx->rank_ptr(adam->exp_avg, rho)) + lo,
+           reinterpret_cast<float*>(ctx->rank_ptr(adam->exp_avg_sq, rho)) + lo, pb, nullptr, len,
+           r > 1 ? subg : round_up(std::max<uint64_t>(len, 1), 4));
+  }
+  out.ag = make_adam_launch(ctx, ap,
+                            make_adam_scalars(adam->lr, adam->beta1, adam->beta2, adam->eps, adam->weight_decay,
+                                              adam->step, adam->grad_scale),
+                            ctx->barrier(rmask | pmask, 0, 1, chan), true);
+  out.has_ag = true;
   return out;
 }
 

@@ -40,8 +40,11 @@ void check_buf_rank(const mics_ctx* c, mics_buf b, int rank, uint64_t off, uint6
 mics_sync* sync_create(mics_ctx* ctx, int p, int s, int nseg, const uint64_t* seg_len, mics_dtype acc_t,
                        uint32_t align);
 Launch build_micro_launch(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode,
-                          bool persistent, bool record, int entry, int exit);
+                          bool persistent, bool record, int entry, int exit,
+                          const mics_buf* shard_override = nullptr);
 BoundaryLaunches build_boundary(mics_sync* st, const mics_adam* adam, bool persistent, bool record);
+BoundaryLaunches build_boundary_range(mics_sync* st, const mics_adam* adam, mics_buf shard, uint64_t lo, uint64_t hi,
+                                      int chan);
 void micro_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode);
 void boundary(mics_sync* st, const mics_adam* adam);
 void alt_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale);
@@ -68,4 +71,18 @@ struct mics_step {
   int adam_step = 0;
   mics_step_stats stats{};
   uint64_t host_result_elems = 4096;
+  // Pipelined boundary (2-hop): step k's boundary runs on the side stream (barrier
+  // channel 1), one layer group at a time, while step k+1's micro-steps proceed on
+  // the main stream; layer group g's first gather waits for its Adam.  The gradient
+  // accumulator is double buffered so step k+1's reduce-scatters never overwrite
+  // what step k's boundary is still reading.
+  bool pipelined = false;
+  mics_buf gacc1{};                                   // second accumulator buffer
+  std::vector<std::vector<mics::Launch>> micro1;      // micro-step launches into gacc1
+  std::vector<std::pair<uint64_t, uint64_t>> group_range;  // shard range of each boundary group
+  std::vector<int> group_first_layer;
+  std::vector<mics::BoundaryLaunches> bndg[2];        // [buffer][group]
+  cudaEvent_t ev_rs = nullptr, ev_done[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> ev_bnd;
+  uint64_t step_idx = 0;
 };

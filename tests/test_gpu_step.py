@@ -104,6 +104,28 @@ def test_step_matches_cpu_restatement(oracle, alternative, grad_dtype, hier_k, p
     eng.close()
 
 
+def test_pipelined_boundary_matches_sequential(monkeypatch):
+    """The pipelined boundary (side stream, layer groups, double-buffered accumulator)
+    gives the same bits as the in-order step, over several steps."""
+    from paper_2205_00119_b200.engine import Engine
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
+    wl = Workload("pipe", [70_000, 12_345, 40_000, 9_999, 33_333], p=2, s=2)
+    res = {}
+    for pipe in ("0", "1"):
+        monkeypatch.setenv("MICS_PIPELINE", pipe)
+        eng = Engine(n_ranks=8, device=0, arena_bytes=256 << 20)
+        step = MicsStep(eng, wl, StepOptions(seed=11, lr=1e-3))
+        step.run(3)
+        eng.synchronize()
+        S = step.sync_info()[0].shard_elems
+        b = step.buffers()
+        res[pipe] = [eng.d2h(b["master"], r, S) for r in range(8)] + [eng.d2h(b["param_bf16"], 5, S, "bf16")]
+        step.close()
+        eng.close()
+    for x, y in zip(res["0"], res["1"]):
+        assert np.array_equal(x.view(np.uint16), y.view(np.uint16))
+
+
 def test_step_two_steps_deterministic(oracle):
     """Two steps, twice: identical bits (the step is deterministic and replayable)."""
     from paper_2205_00119_b200.engine import Engine
