@@ -82,7 +82,7 @@ void AdamPlan::add(const std::vector<const void*>& src, float* param, float* m, 
   j.sub = sub;
   j.rr = uint32_t(src.size());
   j.tile0 = tiles;
-  tiles += uint32_t(ceil_div(elems, kAdamTile));
+  tiles += uint32_t(src.size() * ceil_div(sub, kAdamTile));  // rr slices, tiles interleaved (k_adam)
   jobs.push_back(j);
   srcs.push_back(src);
 }

@@ -440,8 +440,14 @@ __global__ void __launch_bounds__(kThreads) k_adam(const AdamJob* __restrict__ j
   bar_entry(bar);
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const AdamJob& J = jobs[find_desc(jobs, njobs, tile)];
-    const uint64_t e0 = uint64_t(tile - J.tile0) * kAdamTile;
-    if (e0 + kAdamTile <= J.elems) {
+    // tiles interleave the rr slices (tile a -> slice a % rr), so every owner's
+    // slice is pulled concurrently instead of all GPUs draining owner 0 first
+    const uint32_t a = tile - J.tile0, q = a % J.rr;
+    const uint64_t s0 = uint64_t(q) * J.sub;
+    const uint64_t send = s0 + J.sub < J.elems ? s0 + J.sub : J.elems;
+    const uint64_t e0 = s0 + uint64_t(a / J.rr) * kAdamTile;
+    if (e0 >= send) continue;
+    if (e0 + kAdamTile <= send) {
       // full tile: every load of the tile (the reduced gradient, mostly from NVLink
       // peers, and the local p, m, v) is issued before the first update
       uint4 gr[kAdamUnroll];
@@ -477,8 +483,8 @@ __global__ void __launch_bounds__(kThreads) k_adam(const AdamJob* __restrict__ j
 #pragma unroll 1
     for (int u = 0; u < kAdamUnroll; ++u) {
       const uint64_t e = e0 + uint64_t(u * kThreads + threadIdx.x) * 4;
-      if (e >= J.elems) continue;
-      if (e + 4 <= J.elems) {
+      if (e >= send) continue;
+      if (e + 4 <= send) {
         const uint32_t owner = uint32_t(e / J.sub);  // sub % 4 == 0: one owner per vector
         const uint4 gr = ld_stream(J.srcs[owner] + e);
         float4 p = *reinterpret_cast<const float4*>(J.param + e);
@@ -501,7 +507,7 @@ __global__ void __launch_bounds__(kThreads) k_adam(const AdamJob* __restrict__ j
         }
         if (J.gout) st_vec(J.gout + e, gr);
       } else {
-        for (uint64_t x = e; x < J.elems; ++x) {
+        for (uint64_t x = e; x < send; ++x) {
           const float g = J.srcs[x / J.sub][x];
           float p = J.param[x], m = J.m[x], v = J.v[x];
           adam_one(g, p, m, v, sc);
