@@ -18,6 +18,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import re
 import shutil
 import statistics
 import subprocess
@@ -46,6 +47,8 @@ def parse():
     ap.add_argument("--generated-grads", action="store_true", help="generate gradients inside the step (K6)")
     ap.add_argument("--schedule", default="two_hop", choices=["two_hop", "alternative"],
                     help="2-hop sync (MiCS) or the DeepSpeed-default all-reduce over all ranks every micro-step")
+    ap.add_argument("--p", type=int, default=0, help="override the workload's partition group size (ablation)")
+    ap.add_argument("--micro-steps", type=int, default=0, help="override s, micro-steps per step (ablation)")
     ap.add_argument("--sweep", action="store_true", help="C2 collective sweep instead of the step")
     return ap.parse_args()
 
@@ -460,6 +463,16 @@ def main():
         GLOO = dist.new_group(backend="gloo")
     from paper_2205_00119_b200.step import workloads
     wl = workloads()[args.workload]
+    if args.p or args.micro_steps:
+        import dataclasses
+        wl = dataclasses.replace(wl, p=args.p or wl.p, s=args.micro_steps or wl.s)
+        wl.name = re.sub(r"p=\d+", f"p={wl.p}", re.sub(r"s=\d+", f"s={wl.s}", wl.name))
+        if wl.p != wl.n:
+            wl.name = wl.name.replace(" (ZeRO-3)", "")
+        if f"p={wl.p}" not in wl.name:
+            wl.name += f", p={wl.p}"
+        if f"s={wl.s}" not in wl.name:
+            wl.name += f", s={wl.s}"
     if args.sweep:
         from tools.sweep import run_sweep
         run_sweep(args, rank, world, local)
