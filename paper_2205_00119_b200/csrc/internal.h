@@ -127,6 +127,9 @@ struct BarrierArg {
   // predecessor (barrier-free all-gathers of static shards): it waits only at its
   // end, so completion order — and every transitive dependency — is preserved.
   int dep_first;
+  // 1 = full system fences around every signal (the conservative protocol, kept
+  // for A/B runs: MICS_BAR_STRICT=1); 0 = relaxed signals, see bar_entry/bar_exit
+  int strict;
 };
 
 // --------------------------------------------------------------------------
@@ -161,6 +164,7 @@ struct mics_ctx {
   // resident CTAs/SM per kernel: copy, adam, reduce by [input dtype][source class 2/4/8/9]
   int occ_copy = 2, occ_adam = 4, occ_reduce[4][4] = {};
   int occ_copy_indep = 1;  // CTAs/SM of barrier-free gathers chained with PDL
+  int bar_strict = 0;      // BarrierArg::strict (MICS_BAR_STRICT)
   int occ_bnd = 1;         // CTAs/SM of the fused boundary (all CTAs must be co-resident)
   int reduce_occ(mics_dtype t, uint32_t max_p) const {
     const int pc = mics::reduce_class(max_p);
@@ -214,6 +218,7 @@ struct mics_ctx {
     b.entry = entry;
     b.exit = exit;
     b.dep_first = 1;
+    b.strict = bar_strict;
     return b;
   }
   // processes hosting any of `ranks`, minus self (0 when self hosts none)

@@ -51,31 +51,62 @@ __device__ __forceinline__ void st_vec(void* p, const uint4& v) { *reinterpret_c
 // descriptor staging overlap this kernel's tail).  A kernel that consumes its
 // predecessor's results waits for it up front; an independent one waits only
 // before exiting, which keeps completion in stream order.
+// A dependent kernel triggers its successor only once its own wait returned, so at
+// most one grid sits waiting behind a running one (triggering first let a whole
+// queue of replays become resident and cost 0.6 us per 1 MiB all-gather on 2 GPUs).
 __device__ __forceinline__ void pdl_begin(const BarrierArg& b) {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (b.dep_first) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void pdl_end(const BarrierArg& b) {
   if (!b.dep_first) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- barrier
+// Pairwise monotone flags: process w's slot on each peer counts the barriers w has
+// reached with that peer.  Why relaxed signals are enough (strict = 0):
+//  - entry announces "my inputs are ready"; they were written by kernels that
+//    completed before this one started (stream order, or griddepcontrol.wait),
+//    so they already sit in this GPU's L2, which is where peer loads are served.
+//  - exit announces "I finished reading your buffers": a CTA counts itself only
+//    after __syncthreads, when every load it issued has returned its value, and
+//    the last CTA's signal is issued after its ticket returns.
+//  - every data write of the collectives goes to this process's own memory.
+// The waiter polls relaxed and acquires once, so its L1 holds nothing stale.
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void bar_signal(const BarrierArg& b, uint64_t add) {
+  if (b.strict) __threadfence_system();
+  for (uint64_t m = b.mask; m; m &= m - 1) {
+    const int w = __ffsll(static_cast<long long>(m)) - 1;
+    uint64_t* f = b.tab->remote_flag[w];
+    const uint64_t v = b.nbar[w] + add;
+    if (b.strict) st_release_sys(f, v); else st_relaxed_sys(f, v);
+  }
+}
+
+__device__ __forceinline__ void bar_wait(const BarrierArg& b, uint64_t add) {
+  for (uint64_t m = b.mask; m; m &= m - 1) {
+    const int w = __ffsll(static_cast<long long>(m)) - 1;
+    const uint64_t* f = b.tab->local_flag[w];
+    const uint64_t target = b.nbar[w] + add;
+    while (ld_relaxed_sys(f) < target) __nanosleep(32);
+    (void)ld_acquire_sys(f);
+  }
+}
+
 __device__ void bar_entry(const BarrierArg& b) {
   if (b.mask == 0 || !b.entry) return;
   if (threadIdx.x == 0) {
-    const unsigned t = atomicAdd(&b.tickets[0], 1u);
-    if (t == 0) {  // first CTA on this GPU announces "inputs ready"
-      __threadfence_system();
-      for (uint64_t m = b.mask; m; m &= m - 1) {
-        const int w = __ffsll(static_cast<long long>(m)) - 1;
-        st_release_sys(b.tab->remote_flag[w], b.nbar[w] + 1);
-      }
-    }
-    for (uint64_t m = b.mask; m; m &= m - 1) {
-      const int w = __ffsll(static_cast<long long>(m)) - 1;
-      const uint64_t target = b.nbar[w] + 1;
-      while (ld_acquire_sys(b.tab->local_flag[w]) < target) __nanosleep(64);
-    }
+    if (atomicAdd(&b.tickets[0], 1u) == 0) bar_signal(b, 1);  // first CTA: "inputs ready"
+    bar_wait(b, 1);
   }
   __syncthreads();
 }
@@ -84,21 +115,13 @@ __device__ void bar_exit(const BarrierArg& b) {
   if (b.mask == 0) return;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    if (b.strict) __threadfence_system();
     const unsigned t = atomicAdd(&b.tickets[1], 1u);
     if (t == gridDim.x - 1) {  // last CTA: every CTA of this GPU finished its accesses
-      __threadfence_system();
       const uint64_t k = uint64_t(b.entry ? 1 : 0) + uint64_t(b.exit ? 1 : 0);
       if (b.exit) {
-        for (uint64_t m = b.mask; m; m &= m - 1) {
-          const int w = __ffsll(static_cast<long long>(m)) - 1;
-          st_release_sys(b.tab->remote_flag[w], b.nbar[w] + k);
-        }
-        for (uint64_t m = b.mask; m; m &= m - 1) {
-          const int w = __ffsll(static_cast<long long>(m)) - 1;
-          const uint64_t target = b.nbar[w] + k;
-          while (ld_acquire_sys(b.tab->local_flag[w]) < target) __nanosleep(64);
-        }
+        bar_signal(b, k);
+        bar_wait(b, k);
       }
       for (uint64_t m = b.mask; m; m &= m - 1) {
         const int w = __ffsll(static_cast<long long>(m)) - 1;

@@ -5,7 +5,7 @@ n/p groups concurrent — libmics (persistent plans) vs NCCL on split communicat
     torchrun --nproc-per-node N bench.py --gpus N --sweep [--steps K]
 
 busBW = (p-1) * M / p / t per rank; one JSON line per point, times are
-CUDA-event medians, max over ranks.
+CUDA-event averages over back-to-back calls (median of 3 trials), max over ranks.
 """
 from __future__ import annotations
 
@@ -16,17 +16,22 @@ import statistics
 NVLINK = 770.0
 
 
-def _time(fn, stream_ext, reps, world, gloo):
+def _time(fn, stream_ext, reps, world, gloo, trials=3):
+    """nccl-tests style: `reps` back-to-back calls between two events (per-call host
+    skew between ranks amortises), median over trials, max over ranks."""
     import torch
     import torch.distributed as dist
+
+    import bench
     ts = []
-    for _ in range(reps):
+    for _ in range(trials):
+        bench.barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream_ext)
-        fn()
+        fn(reps)
         e1.record(stream_ext)
         e1.synchronize()
-        ts.append(e0.elapsed_time(e1))
+        ts.append(e0.elapsed_time(e1) / reps)
     t = statistics.median(ts)
     if world > 1:
         x = torch.tensor([t], dtype=torch.float64)
@@ -75,7 +80,7 @@ def run_sweep(args, rank, world, local):
                 plan.run(3)
                 eng.synchronize()
                 bench.barrier(world)
-                us = _time(lambda: plan.run(1), ext, reps, world, gloo)
+                us = _time(plan.run, ext, reps, world, gloo)
                 if pg is not None:
                     a_in, a_out = t_in.view(torch.uint8)[:chunk], t_out.view(torch.uint8)[:m]
                     r_in, r_out = t_in[:m // 4], t_out[:m // 4 // p]
@@ -85,7 +90,7 @@ def run_sweep(args, rank, world, local):
                         nccl()
                     torch.cuda.synchronize()
                     bench.barrier(world)
-                    nus = _time(nccl, torch.cuda.current_stream(), reps, world, gloo)
+                    nus = _time(lambda k: [nccl() for _ in range(k)], torch.cuda.current_stream(), reps, world, gloo)
                 else:
                     nus = None
                 bus = (p - 1) * m / p / (us * 1e-6) / 1e9
