@@ -432,7 +432,9 @@ def run_mics(args, wl, rank, world, local):
                    "param_dtype": "bf16 (fp32 master, m, v)", "hierarchical_k": wl.hier_k,
                    "grads": "resident in HBM (generated before timing)" if resident else "generated in-step (K6)",
                    "l2": "inputs larger than L2 (gradient sets of %.2f GB/rank)" % (s * stats.grad_elems * szg / 1e9),
-                   "parallelism": f"MiCS p={wl.p} x {n // wl.p} replicas", "schedule": args.schedule},
+                   "parallelism": f"MiCS p={wl.p} x {n // wl.p} replicas", "schedule": args.schedule,
+                   "launch": "stream" if os.environ.get("MICS_GRAPH") == "0" or os.environ.get("MICS_PIPELINE") == "1"
+                             else "CUDA graph replay (one graph per step)"},
         "roofline": roof,
         "phases_ms": {k: v[0] for k, v in phases.items()},
         "per_rank_bytes": {"allgather_in": stats.ag_bytes_in, "reducescatter_in": stats.rs_bytes_in,

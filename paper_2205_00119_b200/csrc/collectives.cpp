@@ -257,14 +257,14 @@ void enqueue(mics_ctx* ctx, const Launch& l, int dep_first, cudaStream_t stream)
                     l.max_p, l.ntiles, l.grid, l.scale, l.mode, bar);
       break;
     case Launch::ADAM:
-      launch_adam(st, static_cast<const AdamJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid, l.adam, bar);
+      launch_adam(st, static_cast<const AdamJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid, l.adam, l.dyn, bar);
       break;
     case Launch::BARRIER:
       launch_barrier(st, bar);
       break;
     case Launch::BOUNDARY:
       launch_boundary(st, static_cast<const BndJob*>(l.d_desc), l.ndesc, l.rs_tiles, l.ntiles, l.grid,
-                      l.adam, l.epoch, bar);
+                      l.adam, l.epoch, l.dyn, bar);
       break;
   }
   ctx->launches++;

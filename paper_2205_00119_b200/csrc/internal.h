@@ -85,6 +85,15 @@ struct AdamScalars {
   float b1, omb1, b2, omb2, eps, wd, step_size, bc2_sqrt, grad_scale;
 };
 
+// Per-step values of a replayed (CUDA-graph) step, read by the boundary kernels
+// from device memory instead of their by-value parameters: the Adam scalars
+// (bias correction changes every step) and the fused boundary's flag epoch.
+struct DevScalars {
+  AdamScalars sc;
+  uint32_t pad_;
+  uint64_t epoch;
+};
+
 // Fused boundary (K5): one local rank's replication-group reduce-scatter of its
 // slice, then Adam over its whole shard, pulling each slice as soon as its owner
 // has published that tile (per-tile flags), so NVLink pulls, the folds and Adam's
@@ -143,14 +152,15 @@ uint32_t reduce_tile_elems(mics_dtype in_t);
 int reduce_class(uint32_t max_p);  // 2, 4, 8 or 9 (> 8 sources)
 int resident_ctas(int kind /* 0 copy, 1 reduce, 2 adam */, mics_dtype in_t, int pclass = 2);
 void launch_adam(cudaStream_t s, const AdamJob* jobs, int njobs, uint32_t ntiles, int grid, const AdamScalars& sc,
-                 const BarrierArg& bar);
+                 const DevScalars* dyn, const BarrierArg& bar);
+void launch_set_scalars(cudaStream_t s, DevScalars* dst, const DevScalars& v);
 constexpr uint32_t kAdamTile = kThreads * kAdamUnroll * 4;
 void launch_generate(cudaStream_t s, void* out, mics_dtype dtype, uint64_t seed, int rank, int step, int layer,
                      uint64_t start, uint64_t count, int grid);
 void launch_cast_bf16(cudaStream_t s, const float* in, uint16_t* out, uint64_t count, int grid);
 void launch_barrier(cudaStream_t s, const BarrierArg& bar);
 void launch_boundary(cudaStream_t s, const BndJob* jobs, int njobs, uint32_t rs_tiles, uint32_t ntiles, int grid,
-                     const AdamScalars& sc, uint64_t epoch, const BarrierArg& bar);
+                     const AdamScalars& sc, uint64_t epoch, const DevScalars* dyn, const BarrierArg& bar);
 
 AdamScalars make_adam_scalars(double lr, double b1, double b2, double eps, double wd, int step, double grad_scale);
 
@@ -273,6 +283,7 @@ struct Launch {
   double scale = 1.0;
   int mode = 0;
   AdamScalars adam{};
+  const DevScalars* dyn = nullptr;  // ADAM/BOUNDARY: per-step scalars in device memory (graph replay)
   BarrierArg bar{};
   // algorithmic bytes one launch moves on this GPU: pulled from peers over NVLink,
   // and local HBM reads + writes (the roofline numerators of bench.py)

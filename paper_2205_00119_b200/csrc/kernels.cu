@@ -458,7 +458,9 @@ __device__ __forceinline__ void adam_one(float g, float& p, float& m, float& v, 
 }
 
 __global__ void __launch_bounds__(kThreads) k_adam(const AdamJob* __restrict__ jobs, int njobs, uint32_t ntiles,
-                                                   AdamScalars sc, BarrierArg bar) {
+                                                   AdamScalars sc, const DevScalars* __restrict__ dyn,
+                                                   BarrierArg bar) {
+  if (dyn) sc = dyn->sc;  // written before the replayed step was launched (stream order)
   pdl_begin(bar);
   bar_entry(bar);
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -673,8 +675,13 @@ __device__ __forceinline__ void bnd_adam_tile(const BndJob& J, const float* g, u
 
 __global__ void __launch_bounds__(kThreads, 2) k_boundary(const BndJob* __restrict__ jobs, int njobs,
                                                           uint32_t rs_items, uint32_t nitems, AdamScalars sc,
-                                                          uint64_t epoch, BarrierArg bar) {
+                                                          uint64_t epoch, const DevScalars* __restrict__ dyn,
+                                                          BarrierArg bar) {
   constexpr uint64_t kBlock = uint64_t(kBndTile) * kBndBlockTiles;
+  if (dyn) {
+    sc = dyn->sc;
+    epoch = dyn->epoch;
+  }
   pdl_begin(bar);
   bar_entry(bar);
   for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
@@ -715,6 +722,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_boundary(const BndJob* __restri
   bar_exit(bar);
   pdl_end(bar);
 }
+
+__global__ void k_set_scalars(DevScalars* dst, DevScalars v) { *dst = v; }
 
 __global__ void k_barrier(BarrierArg bar) {
   pdl_begin(bar);
@@ -831,8 +840,13 @@ void launch_reduce(cudaStream_t s, mics_dtype in_t, mics_dtype acc_t, const RedJ
 }
 
 void launch_adam(cudaStream_t s, const AdamJob* jobs, int njobs, uint32_t ntiles, int grid, const AdamScalars& sc,
-                 const BarrierArg& bar) {
-  launch_ex(k_adam, grid, kThreads, 0, s, jobs, njobs, ntiles, sc, bar);
+                 const DevScalars* dyn, const BarrierArg& bar) {
+  launch_ex(k_adam, grid, kThreads, 0, s, jobs, njobs, ntiles, sc, dyn, bar);
+}
+
+void launch_set_scalars(cudaStream_t s, DevScalars* dst, const DevScalars& v) {
+  k_set_scalars<<<1, 1, 0, s>>>(dst, v);
+  MICS_CUDA(cudaGetLastError());
 }
 
 void launch_generate(cudaStream_t s, void* out, mics_dtype dtype, uint64_t seed, int rank, int step, int layer,
@@ -854,8 +868,8 @@ void launch_barrier(cudaStream_t s, const BarrierArg& bar) {
 }
 
 void launch_boundary(cudaStream_t s, const BndJob* jobs, int njobs, uint32_t rs_tiles, uint32_t ntiles, int grid,
-                     const AdamScalars& sc, uint64_t epoch, const BarrierArg& bar) {
-  launch_ex(k_boundary, grid, kThreads, 0, s, jobs, njobs, rs_tiles, ntiles, sc, epoch, bar);  // items, not tiles
+                     const AdamScalars& sc, uint64_t epoch, const DevScalars* dyn, const BarrierArg& bar) {
+  launch_ex(k_boundary, grid, kThreads, 0, s, jobs, njobs, rs_tiles, ntiles, sc, epoch, dyn, bar);  // items, not tiles
 }
 
 }  // namespace mics

@@ -49,6 +49,12 @@ void release(mics_step* st) {
   for (auto e : st->ev_done)
     if (e) cudaEventDestroy(e);
   for (auto e : st->ev_bnd) cudaEventDestroy(e);
+  if (st->gexec) cudaGraphExecDestroy(st->gexec);
+  for (auto e : st->ev_h2d) cudaEventDestroy(e);
+  for (auto e : st->ev_rs_slot) cudaEventDestroy(e);
+  if (st->ev_begin) cudaEventDestroy(st->ev_begin);
+  if (st->copy_stream) cudaStreamDestroy(st->copy_stream);
+  if (st->d_scalars) cudaFree(st->d_scalars);
 }
 
 // flat all-gather of layer l into gathered buffer (l % 2) of every local rank
@@ -139,10 +145,17 @@ void enqueue_boundary(mics_step* st, bool side) {
   const AdamScalars sc = make_adam_scalars(st->cfg.lr, st->cfg.beta1, st->cfg.beta2, st->cfg.eps,
                                            st->cfg.weight_decay, st->adam_step, st->adam.grad_scale);
   if (!st->pipelined) {
+    const uint64_t epoch = st->bnd.has_ag ? ++st->sync->epoch : 0;
+    if (st->d_scalars && !st->capturing) {  // boundary kernels read the device copy once a graph exists
+      DevScalars v{};
+      v.sc = sc;
+      v.epoch = epoch;
+      launch_set_scalars(ctx->stream, st->d_scalars, v);
+    }
     if (st->bnd.has_rs) enqueue(ctx, st->bnd.rs);
     if (st->bnd.has_ag) {
       st->bnd.ag.adam = sc;
-      st->bnd.ag.epoch = ++st->sync->epoch;
+      st->bnd.ag.epoch = epoch;
       enqueue(ctx, st->bnd.ag);
     }
     return;
@@ -386,7 +399,72 @@ void step_destroy(mics_step* st) {
   delete st;
 }
 
+namespace {
+bool graph_enabled(const mics_step* st) {
+  if (st->pipelined) return false;  // the pipelined boundary overlaps the next step: not one closed graph
+  const char* e = std::getenv("MICS_GRAPH");
+  return !(e && e[0] == '0');
+}
+
+// Capture one whole step (s micro-steps + boundary) into a CUDA graph.  The
+// boundary kernels read their per-step scalars from st->d_scalars, so the same
+// graph replays every step; programmatic-dependent-launch edges are kept by the
+// capture.  The capture itself launches nothing: the state it advanced (Adam
+// step, flag epoch) is rolled back and re-advanced per replay.
+void build_graph(mics_step* st) {
+  mics_ctx* ctx = st->ctx;
+  st->graph_tried = true;
+  MICS_CUDA(cudaMalloc(&st->d_scalars, sizeof(DevScalars)));
+  st->bnd.rs.dyn = st->bnd.ag.dyn = st->d_scalars;
+  const int adam_step0 = st->adam_step;
+  const uint64_t epoch0 = st->sync->epoch, launches0 = ctx->launches;
+  cudaGraph_t g = nullptr;
+  MICS_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  st->capturing = true;
+  try {
+    for (int t = 0; t < st->cfg.s; ++t) {
+      if (!st->cfg.resident_grads) enqueue_generate(st, t);
+      enqueue_micro(st, t, false);
+    }
+    enqueue_boundary(st, false);
+  } catch (...) {
+    st->capturing = false;
+    cudaStreamEndCapture(ctx->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  st->capturing = false;
+  MICS_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+  st->graph_launches = ctx->launches - launches0;
+  ctx->launches = launches0;
+  st->adam_step = adam_step0;
+  st->sync->epoch = epoch0;
+  const cudaError_t e = cudaGraphInstantiate(&st->gexec, g, 0);
+  cudaGraphDestroy(g);
+  MICS_CUDA(e);
+}
+
+void replay(mics_step* st) {
+  mics_ctx* ctx = st->ctx;
+  st->adam_step++;
+  DevScalars v{};
+  v.sc = make_adam_scalars(st->cfg.lr, st->cfg.beta1, st->cfg.beta2, st->cfg.eps, st->cfg.weight_decay,
+                           st->adam_step, st->adam.grad_scale);
+  if (st->bnd.has_ag) v.epoch = ++st->sync->epoch;
+  launch_set_scalars(ctx->stream, st->d_scalars, v);
+  MICS_CUDA(cudaGraphLaunch(st->gexec, ctx->stream));
+  ctx->launches += st->graph_launches + 1;
+  st->step_idx++;
+}
+}  // namespace
+
 void step_run(mics_step* st, int iters) {
+  if (iters > 0 && graph_enabled(st)) {
+    if (!st->graph_tried) build_graph(st);
+    for (int it = 0; it < iters; ++it) replay(st);
+    st->stats.adam_step = st->adam_step;
+    return;
+  }
   for (int it = 0; it < iters; ++it) {
     for (int t = 0; t < st->cfg.s; ++t) {
       if (!st->cfg.resident_grads) enqueue_generate(st, t);
@@ -448,15 +526,43 @@ void step_run_host(mics_step* st, const void* host_grads, int iters, void* host_
   mics_ctx* ctx = st->ctx;
   const uint64_t szg = dtype_size(st->cfg.grad_t), gb = st->sync->grad_elems * szg;
   const uint64_t rb = std::min(st->host_result_elems, st->sync->shard_elems) * 4;
+  const int s = st->cfg.s, nslot = st->cfg.resident_grads ? s : 1;
+  if (!st->copy_stream) {
+    MICS_CUDA(cudaStreamCreateWithFlags(&st->copy_stream, cudaStreamNonBlocking));
+    st->ev_h2d.resize(size_t(nslot));
+    st->ev_rs_slot.resize(size_t(nslot));
+    for (auto& e : st->ev_h2d) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : st->ev_rs_slot) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    MICS_CUDA(cudaEventCreateWithFlags(&st->ev_begin, cudaEventDisableTiming));
+  }
+  // slot k's copy waits until the reduce-scatter that last read slot k is done
+  auto copy_in = [&](int t) {
+    const int k = t % nslot;
+    MICS_CUDA(cudaStreamWaitEvent(st->copy_stream, st->ev_rs_slot[size_t(k)], 0));
+    for (int r = 0; r < ctx->n; ++r) {
+      if (!ctx->local(r)) continue;
+      MICS_CUDA(cudaMemcpyAsync(ctx->rank_ptr(st->grads, r) + uint64_t(k) * gb, host_grads, gb,
+                                cudaMemcpyHostToDevice, st->copy_stream));
+    }
+    MICS_CUDA(cudaEventRecord(st->ev_h2d[size_t(k)], st->copy_stream));
+  };
+  // nothing of this call starts before the work already on the main stream (e.g. a timing event)
+  MICS_CUDA(cudaEventRecord(st->ev_begin, ctx->stream));
+  MICS_CUDA(cudaStreamWaitEvent(st->copy_stream, st->ev_begin, 0));
   for (int it = 0; it < iters; ++it) {
-    for (int t = 0; t < st->cfg.s; ++t) {
-      const uint64_t off = st->cfg.resident_grads ? uint64_t(t) * gb : 0;
-      for (int r = 0; r < ctx->n; ++r) {
-        if (!ctx->local(r)) continue;
-        MICS_CUDA(cudaMemcpyAsync(ctx->rank_ptr(st->grads, r) + off, host_grads, gb, cudaMemcpyHostToDevice,
-                                  ctx->stream));
-      }
-      enqueue_micro(st, t, true);
+    // resident slots: every copy of the step can start at once (each waits only for
+    // its own slot's previous reader); one slot: copy t+1 follows the RS of t
+    if (nslot == s)
+      for (int t = 0; t < s; ++t) copy_in(t);
+    else
+      copy_in(0);
+    for (int t = 0; t < s; ++t) {
+      const int k = t % nslot;
+      enqueue_gathers(st, t, true);  // parameters only: overlaps the copies
+      MICS_CUDA(cudaStreamWaitEvent(ctx->stream, st->ev_h2d[size_t(k)], 0));
+      enqueue_sync(st, t, true);
+      MICS_CUDA(cudaEventRecord(st->ev_rs_slot[size_t(k)], ctx->stream));
+      if (nslot != s && t + 1 < s) copy_in(t + 1);
     }
     enqueue_boundary(st, true);
     st->step_idx++;

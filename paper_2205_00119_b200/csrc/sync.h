@@ -85,4 +85,16 @@ struct mics_step {
   cudaEvent_t ev_rs = nullptr, ev_done[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_bnd;
   uint64_t step_idx = 0;
+  // CUDA-graph replay (default; MICS_GRAPH=0 enqueues every kernel per step):
+  // one captured step whose boundary kernels read the per-step Adam scalars and
+  // flag epoch from d_scalars, set by one small kernel before each replay.
+  bool graph_tried = false, capturing = false;
+  cudaGraphExec_t gexec = nullptr;
+  mics::DevScalars* d_scalars = nullptr;
+  uint64_t graph_launches = 0;  // kernels in one replay (the capture's count)
+  // e2e (host gradients): H2D copies run on their own stream, one slot ahead of
+  // the reduce-scatter that consumes them, overlapping the gathers
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> ev_h2d, ev_rs_slot;
+  cudaEvent_t ev_begin = nullptr;
 };

@@ -141,3 +141,71 @@ def test_step_two_steps_deterministic(oracle):
         step.close()
         eng.close()
     assert np.array_equal(u32(res[0]), u32(res[1]))
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_graph_replay_matches_eager(monkeypatch, fused):
+    """The CUDA-graph replayed step (default) gives the same bits as enqueueing every
+    kernel per step, across replays, an interleaved profiled (eager) step and the
+    per-step Adam scalars / boundary epoch it reads from device memory."""
+    from paper_2205_00119_b200.engine import Engine
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
+    monkeypatch.setenv("MICS_FUSED_BOUNDARY", fused)
+    wl = Workload("graph", [70_000, 12_345, 40_000, 9_999], p=2, s=2)
+    res = {}
+    for graph in ("0", "1"):
+        monkeypatch.setenv("MICS_GRAPH", graph)
+        eng = Engine(n_ranks=8, device=0, arena_bytes=256 << 20)
+        step = MicsStep(eng, wl, StepOptions(seed=21, lr=1e-3, weight_decay=0.01))
+        l0 = eng.launches
+        step.run(2)
+        step.profile()
+        step.run(2)
+        eng.synchronize()
+        assert step.stats().adam_step == 5
+        if graph == "1":  # replays count every captured kernel (+ the scalar update)
+            assert eng.launches - l0 >= 5 * step.stats().launches
+        S = step.sync_info()[0].shard_elems
+        b = step.buffers()
+        res[graph] = [eng.d2h(b[k], r, S) for k in ("master", "exp_avg", "exp_avg_sq") for r in range(8)]
+        res[graph].append(eng.d2h(b["param_bf16"], 3, S, "bf16"))
+        step.close()
+        eng.close()
+    for x, y in zip(res["0"], res["1"]):
+        assert np.array_equal(x.view(np.uint16), y.view(np.uint16))
+
+
+@pytest.mark.parametrize("resident", [True, False])
+def test_run_host_matches_device_resident(resident):
+    """e2e path (H2D on a copy stream, overlapping the gathers): same bits as the
+    step run on the same gradients already resident in HBM."""
+    from paper_2205_00119_b200.engine import Engine, host_alloc, host_free
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
+    wl = Workload("host", [30_000, 12_345, 20_000], p=2, s=3)
+    eng = Engine(n_ranks=8, device=0, arena_bytes=256 << 20)
+    step = MicsStep(eng, wl, StepOptions(seed=3, lr=1e-3, resident_grads=resident))
+    G = step.stats().grad_elems
+    host, hptr = host_alloc(G * 4)
+    g = np.random.default_rng(7).uniform(-1, 1, G).astype(np.float32)
+    host[:] = g.view(np.uint8)
+    res, rptr = host_alloc(8 * 4096 * 4)
+    step.run_host(hptr, 2, rptr)
+    eng.synchronize()
+    S = step.sync_info()[0].shard_elems
+    got = [eng.d2h(step.buffers()["master"], r, S) for r in range(8)]
+    assert np.array_equal(res[:min(4096, S) * 4].view(np.float32), got[0][:min(4096, S)])
+    step.close()
+    # reference: the same gradients placed in every slot, then the device-resident step
+    step2 = MicsStep(eng, wl, StepOptions(seed=3, lr=1e-3, resident_grads=True))
+    b = step2.buffers()
+    for r in range(8):
+        for t in range(wl.s):
+            eng.h2d(b["grads"], r, g, off=t * G * 4)
+    step2.run(2)
+    eng.synchronize()
+    for r in range(8):
+        assert np.array_equal(u32(eng.d2h(b["master"], r, S)), u32(got[r])), r
+    step2.close()
+    host_free(hptr)
+    host_free(rptr)
+    eng.close()
