@@ -275,6 +275,17 @@ mics_status mics_sync_clear_events(mics_sync* st);
 /* ---------------------------------------------------------------- synthetic gradients (K6)
  * x = splitmix64(seed ^ rank<<40 ^ step<<32 ^ layer<<24 ^ idx) -> f32 in [-1,1) (24 bits) or an
  * exactly-representable bf16 (8 bits); idx runs from `start`.  dtype F32 or BF16. */
+/* K7: dense bf16 GEMM on the tcgen05 tensor cores (TMA + TMEM), the layer compute of
+ * the step with compute (the reference has no GEMM: unpinned, checked
+ * against an fp32 matmul).  C[m,n] (+)= sum_k A(m,k) B(k,n) on the ctx stream, device
+ * pointers, row-major storage:
+ *   A(m,k) = a[m*lda + k] (a_mn = 0, K-major) or a[k*lda + m] (a_mn = 1, M-major)
+ *   B(k,n) = b[n*ldb + k] (b_mn = 0, K-major) or b[k*ldb + n] (b_mn = 1, N-major)
+ *   C(m,n) = c[m*ldc + n], f32 or bf16 (RNE); accumulate = 1 adds into an f32 C.
+ * a, b 16-byte aligned, lda/ldb multiples of 8. */
+mics_status mics_gemm_bf16(mics_ctx* ctx, const void* a, uint64_t lda, int a_mn, const void* b, uint64_t ldb, int b_mn,
+                           void* c, uint64_t ldc, mics_dtype c_t, int m, int n, int k, int accumulate);
+
 mics_status mics_generate(mics_ctx* ctx, mics_buf buf, int rank, uint64_t off, mics_dtype dtype, uint64_t seed,
                           int step, int layer, uint64_t start, uint64_t count);
 

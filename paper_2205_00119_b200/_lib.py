@@ -150,6 +150,7 @@ _SIGS = [
     ("mics_step_buffers", I, [VP] + [C.POINTER(Buf)] * 6),
     ("mics_step_profile", I, [VP, VP] + [C.POINTER(D)] * 4),
     ("mics_step_run_host", I, [VP, VP, VP, I, VP]),
+    ("mics_gemm_bf16", I, [VP, VP, U64, I, VP, U64, I, VP, U64, I, I, I, I, I]),
 ]
 
 EXPORTS = [name for name, _, _ in _SIGS]

@@ -601,3 +601,14 @@ mics_status mics_step_run_host(mics_ctx* ctx, mics_step* st, const void* host_gr
 }
 
 }  // extern "C"
+
+mics_status mics_gemm_bf16(mics_ctx* ctx, const void* a, uint64_t lda, int a_mn, const void* b, uint64_t ldb, int b_mn,
+                           void* c, uint64_t ldc, mics_dtype c_t, int m, int n, int k, int accumulate) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (!a || !b || !c) mics::raise(MICS_OUT_OF_RANGE, "gemm: null operand");
+    const mics::GemmLaunch g = mics::plan_gemm(a, lda, a_mn, b, ldb, b_mn, c, ldc, c_t, m, n, k, accumulate);
+    mics::launch_gemm(ctx->stream, g);
+    ctx->launches++;
+  });
+}

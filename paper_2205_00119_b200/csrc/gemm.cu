@@ -1,0 +1,382 @@
+// K7: dense bf16 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA),
+// the layer compute of the MiCS step with compute (the
+// reference has no GEMM, so this is unpinned by it and checked
+// against a plain fp32 matmul).
+//
+//   C[M,N] (+)= A[M,K] · B[K,N]     bf16 operands, fp32 accumulation in TMEM
+//
+// Either operand may be K-major or MN-major in global memory, which covers the
+// three products of a linear layer without transposes (row-major storage):
+//   forward  Y  = X · Wᵀ   A = X  (K-major), B = W  (K-major)
+//   dgrad    dX = dY · W   A = dY (K-major), B = W  (N-major)
+//   wgrad    dW = dYᵀ · X  A = dY (M-major), B = X  (N-major)
+//
+// Structure (one CTA per SM, persistent over 128x256 output tiles):
+//   warp 0      TMA producer: 128B-swizzled boxes of A and B into a 4-stage ring
+//   warp 1      MMA issuer: one thread issues tcgen05.mma (M=128, N=256, K=16)
+//               into one of two TMEM accumulators (2 x 256 columns)
+//   warps 2..5  epilogue: tcgen05.ld accumulator rows -> registers -> fp32/bf16
+//               stores (optionally C += acc), overlapping the next tile's MMAs
+// Stage ring: full[s] (TMA bytes landed) / empty[s] (tcgen05.commit after the MMAs
+// that read it); accumulators: tmem_full[a] (commit) / tmem_empty[a] (epilogue).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "internal.h"
+
+namespace mics {
+namespace {
+
+constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4;
+constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KiB
+constexpr uint32_t kBBytes = kBN * kBK * 2;  // 32 KiB
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr int kGemmThreads = 192;
+constexpr uint32_t kTmemCols = 2 * kBN;  // double-buffered accumulator
+constexpr uint32_t kSmemBytes = kStages * kStageBytes + 1024 /* align */ + 256 /* barriers */;
+
+struct GemmParams {
+  void* c;
+  uint64_t ldc;
+  int M, N, K;
+  int c_bf16;   // output element type: 1 bf16, 0 fp32
+  int beta;     // 1: C += A·B (fp32 output only)
+  int a_mn;     // A is M-major (A(m,k) at a[k*lda + m])
+  int b_mn;     // B is N-major (B(n,k) at b[k*ldb + n])
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint32_t dst, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// shared-memory matrix descriptor, SWIZZLE_128B (layout type 2), version 1
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// instruction descriptor: fp32 accumulate, bf16 x bf16, M=128, N=256, majors
+__device__ __forceinline__ uint32_t idesc_bf16(int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
+         (uint32_t(kBN >> 3) << 17) | (uint32_t(kBM >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, GemmParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  // bars: full[kStages], empty[kStages], tmem_full[2], tmem_empty[2]; then the TMEM base address
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
+  const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8 * a, 1);
+      mbar_init(tempty0 + 8 * a, 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int tiles_m = (P.M + kBM - 1) / kBM, tiles_n = (P.N + kBN - 1) / kBN;
+  const int ntiles = tiles_m * tiles_n, nk = (P.K + kBK - 1) / kBK;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int m0 = (t % tiles_m) * kBM, n0 = (t / tiles_m) * kBN;
+        for (int kb = 0; kb < nk; ++kb) {
+          const uint32_t full = full0 + 8 * stage;
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          mbar_expect_tx(full, kStageBytes);
+          const uint32_t sa = smem_u32(smem + stage * kStageBytes), sb = sa + kABytes;
+          const int k0 = kb * kBK;
+          if (P.a_mn) {
+#pragma unroll
+            for (int j = 0; j < kBM / 64; ++j) tma_load_2d(&tma_a, sa + j * 8192, full, m0 + 64 * j, k0);
+          } else {
+            tma_load_2d(&tma_a, sa, full, k0, m0);
+          }
+          if (P.b_mn) {
+#pragma unroll
+            for (int j = 0; j < kBN / 64; ++j) tma_load_2d(&tma_b, sb + j * 8192, full, n0 + 64 * j, k0);
+          } else {
+            tma_load_2d(&tma_b, sb, full, k0, n0);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t idesc = idesc_bf16(P.a_mn, P.b_mn);
+      // K-major: the 16-element K slice advances 32 B inside the 128 B swizzle row;
+      // MN-major: it advances 16 rows of 128 B.  LBO = distance between 64-wide MN blocks.
+      const uint32_t a_step = P.a_mn ? 2048u : 32u, b_step = P.b_mn ? 2048u : 32u;
+      const uint32_t a_lbo = P.a_mn ? 8192u : 16u, b_lbo = P.b_mn ? 8192u : 16u;
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        fence_after();
+        const uint32_t d = tmem_base + uint32_t(acc * kBN);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(full0 + 8 * stage, phase);
+          fence_after();
+          const uint32_t sa = smem_u32(smem + stage * kStageBytes), sb = sa + kABytes;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t ad = umma_desc(sa + k * a_step, a_lbo, 1024);
+            const uint64_t bd = umma_desc(sb + k * b_step, b_lbo, 1024);
+            umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(empty0 + 8 * stage);  // frees the stage once these MMAs have read it
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(tfull0 + 8 * acc);  // accumulator complete
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {  // ---------------- epilogue: warps 2..5, TMEM lane quarter = warp % 4
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int m0 = (t % tiles_m) * kBM, n0 = (t / tiles_m) * kBN;
+      mbar_wait(tfull0 + 8 * acc, acc_phase);
+      fence_after();
+      const int m = m0 + row;
+#pragma unroll 1
+      for (int c = 0; c < kBN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * kBN + c * 32), v);
+        const int n = n0 + c * 32;
+        if (m >= P.M || n >= P.N) continue;
+        if (P.c_bf16) {
+          uint16_t* out = static_cast<uint16_t*>(P.c) + uint64_t(m) * P.ldc + n;
+          if (n + 32 <= P.N && (P.ldc % 8) == 0) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 w;
+              w.x = pack_bf16(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+              w.y = pack_bf16(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+              w.z = pack_bf16(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+              w.w = pack_bf16(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+              reinterpret_cast<uint4*>(out)[j] = w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n + j < P.N) {
+                const __nv_bfloat16 h = __float2bfloat16_rn(__uint_as_float(v[j]));
+                out[j] = *reinterpret_cast<const uint16_t*>(&h);
+              }
+          }
+        } else {
+          float* out = static_cast<float*>(P.c) + uint64_t(m) * P.ldc + n;
+          if (n + 32 <= P.N && (P.ldc % 4) == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 w = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                     __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+              if (P.beta) {
+                const float4 o = reinterpret_cast<const float4*>(out)[j];
+                w.x += o.x;
+                w.y += o.y;
+                w.z += o.z;
+                w.w += o.w;
+              }
+              reinterpret_cast<float4*>(out)[j] = w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n + j < P.N) out[j] = __uint_as_float(v[j]) + (P.beta ? out[j] : 0.0f);
+          }
+        }
+      }
+      fence_before();
+      mbar_arrive(tempty0 + 8 * acc);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols)
+                 : "memory");
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    MICS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) raise(MICS_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+// 2-D bf16 map over a row-major [outer, inner] matrix with leading dimension ld
+// (elements), box = 64 inner elements (one 128 B swizzle row) x box_outer rows.
+CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_outer) {
+  if (reinterpret_cast<uintptr_t>(base) % 16 || (ld * 2) % 16)
+    raise(MICS_OUT_OF_RANGE, "gemm: operands need 16-byte aligned base and leading dimension (multiple of 8)");
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {64, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(MICS_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return m;
+}
+
+int gemm_grid(int ntiles) {
+  static int nsm = [] {
+    int dev = 0, n = 0;
+    MICS_CUDA(cudaGetDevice(&dev));
+    MICS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    MICS_CUDA(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
+    return n;
+  }();
+  return ntiles < nsm ? ntiles : nsm;
+}
+
+}  // namespace
+
+GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint64_t ldb, int b_mn, void* c,
+                     uint64_t ldc, mics_dtype c_t, int M, int N, int K, int accumulate) {
+  if (M <= 0 || N <= 0 || K <= 0) raise(MICS_OUT_OF_RANGE, "gemm: M, N, K must be positive");
+  if (c_t != MICS_F32 && c_t != MICS_BF16) raise(MICS_TYPE_MISMATCH, "gemm: output must be f32 or bf16");
+  if (accumulate && c_t != MICS_F32) raise(MICS_TYPE_MISMATCH, "gemm: accumulate needs an f32 output");
+  if (ldc < uint64_t(N) || lda < uint64_t(a_mn ? M : K) || ldb < uint64_t(b_mn ? N : K))
+    raise(MICS_SIZE_MISMATCH, "gemm: leading dimension smaller than the row");
+  GemmLaunch g;
+  // A(m,k): K-major -> [M rows, K inner]; M-major -> [K rows, M inner]
+  g.ma = a_mn ? make_map(a, uint64_t(M), uint64_t(K), lda, 64) : make_map(a, uint64_t(K), uint64_t(M), lda, kBM);
+  g.mb = b_mn ? make_map(b, uint64_t(N), uint64_t(K), ldb, 64) : make_map(b, uint64_t(K), uint64_t(N), ldb, kBN);
+  GemmParams P{c, ldc, M, N, K, c_t == MICS_BF16, accumulate != 0, a_mn != 0, b_mn != 0};
+  static_assert(sizeof(GemmParams) <= sizeof(g.params), "GemmParams fits");
+  memcpy(g.params, &P, sizeof(P));
+  g.ntiles = ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN);
+  g.grid = gemm_grid(g.ntiles);
+  g.flops = 2.0 * double(M) * double(N) * double(K);
+  return g;
+}
+
+void launch_gemm(cudaStream_t s, const GemmLaunch& g) {
+  GemmParams P;
+  memcpy(&P, g.params, sizeof(P));
+  k_gemm<<<g.grid, kGemmThreads, kSmemBytes, s>>>(g.ma, g.mb, P);
+  MICS_CUDA(cudaGetLastError());
+}
+
+}  // namespace mics

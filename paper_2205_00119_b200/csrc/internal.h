@@ -1,6 +1,7 @@
 // Internal declarations of libmics (not part of the C-ABI).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -161,6 +162,18 @@ void launch_cast_bf16(cudaStream_t s, const float* in, uint16_t* out, uint64_t c
 void launch_barrier(cudaStream_t s, const BarrierArg& bar);
 void launch_boundary(cudaStream_t s, const BndJob* jobs, int njobs, uint32_t rs_tiles, uint32_t ntiles, int grid,
                      const AdamScalars& sc, uint64_t epoch, const DevScalars* dyn, const BarrierArg& bar);
+
+// K7 tcgen05 GEMM (gemm.cu): C[M,N] (+)= A[M,K]·B[K,N], bf16 operands K- or MN-major,
+// fp32 accumulation; planned once (TMA descriptors encoded), launched many times.
+struct GemmLaunch {
+  CUtensorMap ma, mb;
+  alignas(8) unsigned char params[64];
+  int ntiles = 0, grid = 1;
+  double flops = 0;
+};
+GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint64_t ldb, int b_mn, void* c,
+                     uint64_t ldc, mics_dtype c_t, int M, int N, int K, int accumulate);
+void launch_gemm(cudaStream_t s, const GemmLaunch& g);
 
 AdamScalars make_adam_scalars(double lr, double b1, double b2, double eps, double wd, int step, double grad_scale);
 
