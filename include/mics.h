@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define MICS_ABI_VERSION 1
+#define MICS_ABI_VERSION 2
 #define MICS_IPC_HANDLE_BYTES 64
 #define MICS_MAX_WORLD 64
 #define MICS_MAX_GROUP 1024
@@ -307,6 +307,18 @@ typedef struct {
   int alternative;               /* 1: DeepSpeed-default global all-reduce every micro-step */
   uint64_t seed;
   double lr, beta1, beta2, eps, weight_decay;
+  /* Step with compute (SURVEY 8f items 2+3; the reference has none).  Each layer l is a
+   * linear map W_l = its gathered bf16 parameters viewed as [E_l / hidden, hidden]; every
+   * layer reads the micro-step's input X [tokens, hidden] (bf16) and the loss is
+   * 1/2 sum_l ||X W_l^T||^2, so per rank and micro-step: forward Y_l = X W_l^T, backward
+   * dX += Y_l W_l and dW_l = Y_l^T X (tcgen05 GEMMs, K7), written as the layer's gradient
+   * that the micro-step reduce-scatter consumes.  The gather of layer l+1 runs on its own
+   * stream, overlapping layer l's GEMMs (prefetch depth 1, simulator.cpp:231-259); the
+   * reduce-scatter of micro-step t overlaps micro-step t+1's compute. */
+  int compute;                   /* 1: layer GEMMs in the step (gradients come from them) */
+  int recompute;                 /* 1: recompute Y_l in the backward pass instead of storing it */
+  uint64_t tokens;               /* rows of X per rank and micro-step (micro_batch * seq_len) */
+  uint64_t hidden;               /* columns of X; every E_l must be a multiple */
 } mics_step_cfg;
 
 typedef struct {
@@ -325,6 +337,9 @@ typedef struct {
   uint64_t ag_remote_bytes, ag_hbm_bytes, ag_launches;
   uint64_t rs_remote_bytes, rs_hbm_bytes, rs_launches;
   uint64_t bnd_remote_bytes, bnd_hbm_bytes, bnd_launches;
+  /* step with compute: tensor-core FLOPs and GEMM launches per step (this process) */
+  double compute_flops;
+  uint64_t gemm_launches;
 } mics_step_stats;
 
 mics_status mics_step_create(mics_ctx* ctx, const mics_step_cfg* cfg, mics_step** out);
@@ -337,7 +352,12 @@ mics_status mics_step_buffers(mics_step* st, mics_buf* param_bf16, mics_buf* mas
 /* per-phase kernel timing (CUDA events on the ctx stream) for the next run: ms per phase */
 mics_status mics_step_profile(mics_ctx* ctx, mics_step* st, double* ag_ms, double* rs_ms, double* boundary_ms,
                               double* gen_ms);
-/* e2e variant: gradients come from pinned HOST memory every micro-step (H2D in the step) */
+/* per-phase device times of one serialised step: ms[0] all-gather, [1] reduce-scatter,
+ * [2] boundary, [3] gradient generation, [4] layer GEMMs (step with compute) */
+mics_status mics_step_profile_ex(mics_ctx* ctx, mics_step* st, double* ms5);
+/* e2e variant: the step's inputs come from pinned HOST memory every micro-step (H2D in
+ * the step): the gradients (grad_elems, reused per rank and micro-step), or with compute
+ * the input X (tokens x hidden bf16) */
 mics_status mics_step_run_host(mics_ctx* ctx, mics_step* st, const void* host_grads /* grad_elems, reused per rank/micro-step */,
                                int iterations, void* host_result /* per local rank: shard fp32, or NULL */);
 

@@ -68,7 +68,7 @@ class Adam(C.Structure):
 class StepCfg(C.Structure):
     _fields_ = [("p", I), ("s", I), ("nlayers", I), ("layer_params", PU64), ("grad_t", I), ("hier_k", I),
                 ("resident_grads", I), ("alternative", I), ("seed", U64), ("lr", D), ("beta1", D), ("beta2", D),
-                ("eps", D), ("weight_decay", D)]
+                ("eps", D), ("weight_decay", D), ("compute", I), ("recompute", I), ("tokens", U64), ("hidden", U64)]
 
 
 class StepStats(C.Structure):
@@ -77,7 +77,8 @@ class StepStats(C.Structure):
                 ("grad_elems", U64), ("adam_step", I),
                 ("ag_remote_bytes", U64), ("ag_hbm_bytes", U64), ("ag_launches", U64),
                 ("rs_remote_bytes", U64), ("rs_hbm_bytes", U64), ("rs_launches", U64),
-                ("bnd_remote_bytes", U64), ("bnd_hbm_bytes", U64), ("bnd_launches", U64)]
+                ("bnd_remote_bytes", U64), ("bnd_hbm_bytes", U64), ("bnd_launches", U64),
+                ("compute_flops", D), ("gemm_launches", U64)]
 
 
 # (name, restype, argtypes); restype I is a mics_status
@@ -150,6 +151,7 @@ _SIGS = [
     ("mics_step_buffers", I, [VP] + [C.POINTER(Buf)] * 6),
     ("mics_step_profile", I, [VP, VP] + [C.POINTER(D)] * 4),
     ("mics_step_run_host", I, [VP, VP, VP, I, VP]),
+    ("mics_step_profile_ex", I, [VP, VP, C.POINTER(D)]),
     ("mics_gemm_bf16", I, [VP, VP, U64, I, VP, U64, I, VP, U64, I, I, I, I, I]),
 ]
 

@@ -45,7 +45,7 @@ Launch build_reduce_scatter(mics_ctx*, const int*, int, const void* const*, uint
 mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg);
 void step_destroy(mics_step* st);
 void step_run(mics_step* st, int iters);
-void step_profile(mics_step* st, double* ag_ms, double* rs_ms, double* bnd_ms, double* gen_ms);
+void step_profile(mics_step* st, double* ms5);
 void step_run_host(mics_step* st, const void* host_grads, int iters, void* host_result);
 }  // namespace mics
 
@@ -583,12 +583,20 @@ mics_status mics_step_profile(mics_ctx* ctx, mics_step* st, double* ag, double* 
   return guard([&] {
     need(ctx, "ctx");
     need(st, "step");
-    double a, r, b, g;
-    mics::step_profile(st, &a, &r, &b, &g);
-    if (ag) *ag = a;
-    if (rs) *rs = r;
-    if (bnd) *bnd = b;
-    if (gen) *gen = g;
+    double ms[5];
+    mics::step_profile(st, ms);
+    if (ag) *ag = ms[0];
+    if (rs) *rs = ms[1];
+    if (bnd) *bnd = ms[2];
+    if (gen) *gen = ms[3];
+  });
+}
+mics_status mics_step_profile_ex(mics_ctx* ctx, mics_step* st, double* ms5) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(st, "step");
+    need(ms5, "ms5");
+    mics::step_profile(st, ms5);
   });
 }
 mics_status mics_step_run_host(mics_ctx* ctx, mics_step* st, const void* host_grads, int iters, void* host_result) {

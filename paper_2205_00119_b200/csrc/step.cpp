@@ -53,12 +53,18 @@ void release(mics_step* st) {
   for (auto e : st->ev_h2d) cudaEventDestroy(e);
   for (auto e : st->ev_rs_slot) cudaEventDestroy(e);
   if (st->ev_begin) cudaEventDestroy(st->ev_begin);
+  for (cudaEvent_t e : {st->ev_g[0], st->ev_g[1], st->ev_free[0], st->ev_free[1], st->ev_fork, st->ev_jg, st->ev_jc})
+    if (e) cudaEventDestroy(e);
+  for (auto e : st->ev_wg) cudaEventDestroy(e);
+  for (auto e : st->ev_rsd) cudaEventDestroy(e);
+  if (st->gs) cudaStreamDestroy(st->gs);
+  if (st->cs) cudaStreamDestroy(st->cs);
   if (st->copy_stream) cudaStreamDestroy(st->copy_stream);
   if (st->d_scalars) cudaFree(st->d_scalars);
 }
 
 // flat all-gather of layer l into gathered buffer (l % 2) of every local rank
-std::vector<Launch> build_layer_ag(mics_step* st, int l) {
+std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan) {
   mics_ctx* ctx = st->ctx;
   mics_sync* sy = st->sync;
   const int p = sy->p, n = sy->n;
@@ -118,7 +124,7 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l) {
   // reads them.  Phase 2 needs no barrier of its own: the next overwrite of a
   // gathered buffer (phase 1 of layer l+2) sits behind layer l+1's phase-1
   // barrier, which every node peer only reaches after finishing phase 2 of l.
-  out.push_back(make_copy_launch(ctx, ph1, ctx->barrier(mask, 0, 1), true));
+  out.push_back(make_copy_launch(ctx, ph1, ctx->barrier(mask, 0, 1, chan), true));
   out.push_back(make_copy_launch(ctx, ph2, ctx->barrier(0, 0, 0), true));
   return out;
 }
@@ -126,7 +132,7 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l) {
 void enqueue_generate(mics_step* st, int t) {
   mics_ctx* ctx = st->ctx;
   const uint64_t szg = dtype_size(st->cfg.grad_t);
-  const uint64_t off = st->cfg.resident_grads ? uint64_t(t) * st->sync->grad_elems * szg : 0;
+  const uint64_t off = uint64_t(t % st->gslots) * st->sync->grad_elems * szg;
   for (int r = 0; r < ctx->n; ++r) {
     if (!ctx->local(r)) continue;
     launch_generate(ctx->stream, ctx->rank_ptr(st->grads, r) + off, st->cfg.grad_t, st->cfg.seed, r, t, 0, 0,
@@ -134,6 +140,8 @@ void enqueue_generate(mics_step* st, int t) {
     ctx->launches++;
   }
 }
+
+bool generated(const mics_step* st) { return !st->cfg.resident_grads && !st->compute; }
 
 int cur_buf(const mics_step* st) { return st->pipelined ? int(st->step_idx & 1) : 0; }
 
@@ -212,6 +220,154 @@ void enqueue_micro(mics_step* st, int t, bool side) {
   enqueue_sync(st, t, side);
 }
 
+// ---------------------------------------------------------------- step with compute
+// Layer l = W_l [rows_l, h] (its gathered bf16 parameters); per rank and micro-step t:
+//   forward   Y_l  = X_t · W_lᵀ                 (bf16, stored or recomputed)
+//   backward  dX  += Y_l · W_l                  (fp32; the input gradient of the branch sum)
+//             dW_l = Y_lᵀ · X_t -> grads slot    (the layer's gradient, f32/bf16)
+// i.e. the exact gradients of 1/2 sum_l ||X W_lᵀ||^2.  Plans are built once.
+void setup_compute(mics_step* st) {
+  mics_ctx* ctx = st->ctx;
+  mics_sync* sy = st->sync;
+  const mics_step_cfg& cfg = st->cfg;
+  const int L = cfg.nlayers, s = cfg.s;
+  st->T = cfg.tokens;
+  st->h = cfg.hidden;
+  st->recompute = cfg.recompute != 0;
+  uint64_t ytot = 0, ymax = 0;
+  for (int l = 0; l < L; ++l) {
+    const uint64_t E = st->layers[size_t(l)];
+    if (E % st->h) raise(MICS_SHAPE_ERROR, "step with compute: layer " + std::to_string(l) + " has " +
+                                                std::to_string(E) + " parameters, not a multiple of hidden " +
+                                                std::to_string(st->h));
+    const uint64_t rows = E / st->h;
+    st->rows.push_back(rows);
+    st->ldy.push_back(round_up(rows, 8));
+    st->yoff.push_back(st->recompute ? 0 : ytot);
+    ytot += st->T * round_up(rows, 8);
+    ymax = std::max(ymax, st->T * round_up(rows, 8));
+  }
+  const uint64_t xe = st->T * st->h;
+  st->x = alloc_sym(ctx, uint64_t(s) * xe * 2);
+  st->y = alloc_sym(ctx, (st->recompute ? ymax : ytot) * 2);
+  st->dx = alloc_sym(ctx, xe * 4);
+  const uint64_t szg = dtype_size(cfg.grad_t);
+  for (int r = 0; r < ctx->n; ++r) {  // inputs of every micro-step (the "batch"), generated once
+    if (!ctx->local(r)) continue;
+    for (int t = 0; t < s; ++t)
+      launch_generate(ctx->stream, ctx->rank_ptr(st->x, r) + uint64_t(t) * xe * 2, MICS_BF16, cfg.seed ^ 0xA11CEull,
+                      r, t, 254, 0, xe, ctx->nsm * 8);
+  }
+  const int T = int(st->T), h = int(st->h);
+  for (int t = 0; t < s; ++t)
+    for (int l = 0; l < L; ++l)
+      for (int r = 0; r < ctx->n; ++r) {
+        if (!ctx->local(r)) continue;
+        const int rows = int(st->rows[size_t(l)]);
+        const uint64_t ldy = st->ldy[size_t(l)];
+        char* W = ctx->rank_ptr(st->gathered, r) + uint64_t(l % 2) * st->gathered_half;
+        char* X = ctx->rank_ptr(st->x, r) + uint64_t(t) * xe * 2;
+        char* Y = ctx->rank_ptr(st->y, r) + st->yoff[size_t(l)] * 2;
+        char* dX = ctx->rank_ptr(st->dx, r);
+        char* dW = ctx->rank_ptr(st->grads, r) + (uint64_t(t % st->gslots) * sy->grad_elems + sy->grad_off[size_t(l)]) * szg;
+        st->gfwd.push_back(plan_gemm(X, st->h, 0, W, st->h, 0, Y, ldy, MICS_BF16, T, rows, h, 0));
+        st->gdgrad.push_back(plan_gemm(Y, ldy, 0, W, st->h, 1, dX, st->h, MICS_F32, T, h, rows, l != L - 1));
+        st->gwgrad.push_back(plan_gemm(Y, ldy, 1, X, st->h, 1, dW, st->h, cfg.grad_t, rows, h, T, 0));
+      }
+  MICS_CUDA(cudaStreamCreateWithFlags(&st->gs, cudaStreamNonBlocking));
+  MICS_CUDA(cudaStreamCreateWithFlags(&st->cs, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&st->ev_g[0], &st->ev_g[1], &st->ev_free[0], &st->ev_free[1], &st->ev_fork, &st->ev_jg,
+                         &st->ev_jc})
+    MICS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  st->ev_wg.resize(size_t(st->gslots));
+  st->ev_rsd.resize(size_t(st->gslots));
+  for (auto& e : st->ev_wg) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : st->ev_rsd) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+// Phase timing of a serialised step (profile): events around every gather and GEMM group.
+struct PhaseClock {
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> kind;  // phase of the interval ending at ev[i]
+  cudaStream_t s = nullptr;
+  void mark(int k) {
+    cudaEvent_t e;
+    MICS_CUDA(cudaEventCreate(&e));
+    MICS_CUDA(cudaEventRecord(e, s));
+    ev.push_back(e);
+    kind.push_back(k);
+  }
+};
+enum { PH_AG = 0, PH_RS = 1, PH_BND = 2, PH_GEN = 3, PH_GEMM = 4 };
+
+// One step with compute.  serial: everything on ctx->stream in order (profiling);
+// otherwise gathers on st->gs, GEMMs on st->cs, reduce-scatters + boundary on
+// ctx->stream:
+//   gather(l) waits ev_free[l%2] (the GEMMs that read that buffer last), GEMMs(l)
+//   wait ev_g[l%2]; RS(t) waits ev_wg[slot] (all dW of t); the first dW GEMM of t
+//   waits ev_rsd[slot] (the RS that read that gradient slot last).
+void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
+  mics_ctx* ctx = st->ctx;
+  const bool serial = clk != nullptr;
+  cudaStream_t M = ctx->stream, G = serial ? M : st->gs, C = serial ? M : st->cs;
+  const int L = st->cfg.nlayers, s = st->cfg.s, per = ctx->per;
+  auto rec = [&](cudaEvent_t e, cudaStream_t on) {
+    if (!serial) MICS_CUDA(cudaEventRecord(e, on));
+  };
+  auto wait = [&](cudaStream_t on, cudaEvent_t e) {
+    if (!serial) MICS_CUDA(cudaStreamWaitEvent(on, e, 0));
+  };
+  auto gemms = [&](const std::vector<GemmLaunch>& v, size_t base) {
+    for (int li = 0; li < per; ++li) {
+      launch_gemm(C, v[base + size_t(li)]);
+      ctx->launches++;
+    }
+  };
+  auto gather = [&](int l) {
+    wait(G, st->ev_free[l % 2]);
+    for (auto& x : st->ag[size_t(l)]) enqueue(ctx, x, -1, G);
+    if (clk) clk->mark(PH_AG);
+    rec(st->ev_g[l % 2], G);
+    wait(C, st->ev_g[l % 2]);
+  };
+  // gathers and GEMMs wait for everything before this step on the main stream (the
+  // previous boundary rewrote the parameter shards)
+  rec(st->ev_fork, M);
+  wait(G, st->ev_fork);
+  wait(C, st->ev_fork);
+  if (clk) clk->mark(-1);
+  for (int t = 0; t < s; ++t) {
+    const int slot = t % st->gslots;
+    for (int l = 0; l < L; ++l) {
+      gather(l);
+      gemms(st->gfwd, size_t(t * L + l) * size_t(per));
+      if (clk) clk->mark(PH_GEMM);
+      rec(st->ev_free[l % 2], C);
+    }
+    if (t >= st->gslots) wait(C, st->ev_rsd[size_t(slot)]);
+    for (int l = L; l-- > 0;) {
+      gather(l);
+      const size_t base = size_t(t * L + l) * size_t(per);
+      if (st->recompute) gemms(st->gfwd, base);
+      gemms(st->gdgrad, base);
+      gemms(st->gwgrad, base);
+      if (clk) clk->mark(PH_GEMM);
+      rec(st->ev_free[l % 2], C);
+    }
+    rec(st->ev_wg[size_t(slot)], C);
+    wait(M, st->ev_wg[size_t(slot)]);
+    for (auto& x : st->micro[size_t(t)]) enqueue(ctx, x, -1, M);
+    if (clk) clk->mark(PH_RS);
+    rec(st->ev_rsd[size_t(slot)], M);
+  }
+  enqueue_boundary(st, false);
+  if (clk) clk->mark(PH_BND);
+  rec(st->ev_jg, G);
+  rec(st->ev_jc, C);
+  wait(M, st->ev_jg);
+  wait(M, st->ev_jc);
+}
+
 // the main stream waits for the side stream, so a main-stream sync covers the step
 void join_side(mics_step* st) {
   if (st->pipelined && st->step_idx > 0)
@@ -244,7 +400,13 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     st->m = alloc_sym(ctx, S * 4);
     st->v = alloc_sym(ctx, S * 4);
     st->gathered = alloc_sym(ctx, 2 * st->gathered_half);
-    st->grads = alloc_sym(ctx, (cfg->resident_grads ? uint64_t(cfg->s) : 1) * sy->grad_elems * szg);
+    // gradient slots: s resident sets, 1 regenerated per micro-step, or with compute 2
+    // (the GEMMs of micro-step t+1 write one while the reduce-scatter of t reads the other)
+    st->compute = cfg->compute != 0;
+    st->gslots = st->compute ? std::min(2, cfg->s) : cfg->resident_grads ? cfg->s : 1;
+    if (st->compute && (cfg->alternative || cfg->tokens == 0 || cfg->hidden == 0 || cfg->hidden % 8 || cfg->tokens % 8))
+      raise(MICS_CONFIG_ERROR, "step with compute: 2-hop schedule, tokens and hidden multiples of 8");
+    st->grads = alloc_sym(ctx, uint64_t(st->gslots) * sy->grad_elems * szg);
     // initial state: master = generator(seed ^ 0x5eed, "rank" = partition position r % p, layer 255),
     // so every replica of a shard starts identical; m = v = 0; bf16 copy of master
     for (int r = 0; r < ctx->n; ++r) {
@@ -256,12 +418,17 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
       launch_cast_bf16(ctx->stream, reinterpret_cast<const float*>(ctx->rank_ptr(st->master, r)),
                        reinterpret_cast<uint16_t*>(ctx->rank_ptr(st->pbf16, r)), S, ctx->nsm * 8);
     }
-    if (cfg->resident_grads)
+    if (st->compute) {
+      for (int r = 0; r < ctx->n; ++r)  // padding past E_l stays zero: the GEMMs write [0, E_l) per layer
+        if (ctx->local(r))
+          MICS_CUDA(cudaMemsetAsync(ctx->rank_ptr(st->grads, r), 0, st->grads.stride, ctx->stream));
+    } else if (cfg->resident_grads) {
       for (int t = 0; t < cfg->s; ++t) enqueue_generate(st, t);
+    }
     // plans
-    for (int l = 0; l < cfg->nlayers; ++l) st->ag.push_back(build_layer_ag(st, l));
+    for (int l = 0; l < cfg->nlayers; ++l) st->ag.push_back(build_layer_ag(st, l, cfg->compute ? 1 : 0));
     for (int t = 0; t < cfg->s; ++t) {
-      const uint64_t goff = cfg->resident_grads ? uint64_t(t) * sy->grad_elems * szg : 0;
+      const uint64_t goff = uint64_t(t % st->gslots) * sy->grad_elems * szg;
       const int mode = t == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE;
       if (cfg->alternative)  // DeepSpeed default (sync_schedule.hpp:189-224): all-reduce over all n
         st->micro.push_back(build_alt(sy, st->grads, goff, cfg->grad_t, 1.0, true, mode));
@@ -285,12 +452,12 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     // forward gathers, so it measured no gain (10.24 vs 10.16 ms on 4 GPUs); it is
     // the hook for overlapping the optimizer with a real forward pass.
     const char* penv = std::getenv("MICS_PIPELINE");
-    st->pipelined = !cfg->alternative && penv && penv[0] == '1';
+    st->pipelined = !cfg->alternative && !st->compute && penv && penv[0] == '1';
     if (st->pipelined) {
       st->gacc1 = alloc_sym(ctx, sy->shard.stride);
       MICS_CUDA(cudaMemsetAsync(ctx->base + st->gacc1.offset, 0, st->gacc1.stride * uint64_t(ctx->per), ctx->stream));
       for (int t = 0; t < cfg->s; ++t) {
-        const uint64_t goff = cfg->resident_grads ? uint64_t(t) * sy->grad_elems * szg : 0;
+        const uint64_t goff = uint64_t(t % st->gslots) * sy->grad_elems * szg;
         st->micro1.push_back({build_micro_launch(sy, st->grads, goff, cfg->grad_t, 1.0,
                                                  t == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE, true, false, 1, 1,
                                                  &st->gacc1)});
@@ -338,6 +505,7 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
                                     ctx->barrier(pmask, 0, 1), true);
       st->bnd.has_ag = true;
     }
+    if (st->compute) setup_compute(st);
     // stats (per rank per step), algorithmic bytes of SURVEY §8(d)
     const int p = sy->p, r = sy->n / p;
     uint64_t csum = 0;
@@ -346,7 +514,7 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     st->stats.rs_bytes_in = uint64_t(cfg->s) * uint64_t(p - 1) * csum * szg;
     st->stats.ar_bytes_in = r > 1 ? 2ull * uint64_t(r - 1) * sy->sub * 4 : 0;
     st->stats.adam_hbm_bytes = S * 30;
-    st->stats.gen_bytes = cfg->resident_grads ? 0 : uint64_t(cfg->s) * sy->grad_elems * szg;
+    st->stats.gen_bytes = generated(st) ? uint64_t(cfg->s) * sy->grad_elems * szg : 0;
     st->stats.shard_elems = S;
     st->stats.gathered_max_bytes = maxl;
     st->stats.grad_elems = sy->grad_elems;
@@ -382,7 +550,20 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
         S2.bnd_hbm_bytes += x->hbm_bytes;
       }
     S2.launches = S2.ag_launches + S2.rs_launches + S2.bnd_launches +
-                  (cfg->resident_grads ? 0 : uint64_t(cfg->s) * uint64_t(ctx->per));
+                  (generated(st) ? uint64_t(cfg->s) * uint64_t(ctx->per) : 0);
+    if (st->compute) {
+      for (const auto* v : {&st->gfwd, &st->gdgrad, &st->gwgrad})
+        for (const GemmLaunch& g : *v) {
+          S2.compute_flops += g.flops;
+          S2.gemm_launches++;
+        }
+      if (st->recompute)
+        for (const GemmLaunch& g : st->gfwd) {
+          S2.compute_flops += g.flops;
+          S2.gemm_launches++;
+        }
+      S2.launches += S2.gemm_launches;
+    }
   } catch (...) {
     release(st);
     delete st;
@@ -422,11 +603,15 @@ void build_graph(mics_step* st) {
   MICS_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   st->capturing = true;
   try {
-    for (int t = 0; t < st->cfg.s; ++t) {
-      if (!st->cfg.resident_grads) enqueue_generate(st, t);
-      enqueue_micro(st, t, false);
+    if (st->compute) {
+      enqueue_compute_step(st, nullptr);
+    } else {
+      for (int t = 0; t < st->cfg.s; ++t) {
+        if (generated(st)) enqueue_generate(st, t);
+        enqueue_micro(st, t, false);
+      }
+      enqueue_boundary(st, false);
     }
-    enqueue_boundary(st, false);
   } catch (...) {
     st->capturing = false;
     cudaStreamEndCapture(ctx->stream, &g);
@@ -466,8 +651,13 @@ void step_run(mics_step* st, int iters) {
     return;
   }
   for (int it = 0; it < iters; ++it) {
+    if (st->compute) {
+      enqueue_compute_step(st, nullptr);
+      st->step_idx++;
+      continue;
+    }
     for (int t = 0; t < st->cfg.s; ++t) {
-      if (!st->cfg.resident_grads) enqueue_generate(st, t);
+      if (generated(st)) enqueue_generate(st, t);
       enqueue_micro(st, t, true);
     }
     enqueue_boundary(st, true);
@@ -477,16 +667,33 @@ void step_run(mics_step* st, int iters) {
   st->stats.adam_step = st->adam_step;
 }
 
-// One step with CUDA events around each phase; returns milliseconds per phase.
-void step_profile(mics_step* st, double* ag_ms, double* rs_ms, double* bnd_ms, double* gen_ms) {
+// One step with CUDA events around each phase; returns milliseconds per phase
+// (ms[0] all-gather, [1] reduce-scatter, [2] boundary, [3] generation, [4] GEMMs).
+void step_profile(mics_step* st, double* ms) {
   mics_ctx* ctx = st->ctx;
   const int s = st->cfg.s;
+  for (int i = 0; i < 5; ++i) ms[i] = 0;
+  if (st->compute) {  // serialised on the main stream, events around every gather / GEMM group
+    PhaseClock clk;
+    clk.s = ctx->stream;
+    enqueue_compute_step(st, &clk);
+    st->step_idx++;
+    MICS_CUDA(cudaEventSynchronize(clk.ev.back()));
+    for (size_t i = 1; i < clk.ev.size(); ++i) {
+      float x = 0;
+      MICS_CUDA(cudaEventElapsedTime(&x, clk.ev[i - 1], clk.ev[i]));
+      if (clk.kind[i] >= 0) ms[clk.kind[i]] += x;
+    }
+    for (auto e : clk.ev) cudaEventDestroy(e);
+    st->stats.adam_step = st->adam_step;
+    return;
+  }
   std::vector<cudaEvent_t> ev(size_t(4 * s + 2));
   for (auto& e : ev) MICS_CUDA(cudaEventCreate(&e));
   int k = 0;
   for (int t = 0; t < s; ++t) {
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
-    if (!st->cfg.resident_grads) enqueue_generate(st, t);
+    if (generated(st)) enqueue_generate(st, t);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
     enqueue_gathers(st, t, false);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
@@ -510,10 +717,10 @@ void step_profile(mics_step* st, double* ag_ms, double* rs_ms, double* bnd_ms, d
   MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * s)], ev[size_t(4 * s + 1)]));
   b = x;
   for (auto& e : ev) cudaEventDestroy(e);
-  *ag_ms = a;
-  *rs_ms = r;
-  *bnd_ms = b;
-  *gen_ms = g;
+  ms[0] = a;
+  ms[1] = r;
+  ms[2] = b;
+  ms[3] = g;
   st->stats.adam_step = st->adam_step;
 }
 
@@ -526,7 +733,29 @@ void step_run_host(mics_step* st, const void* host_grads, int iters, void* host_
   mics_ctx* ctx = st->ctx;
   const uint64_t szg = dtype_size(st->cfg.grad_t), gb = st->sync->grad_elems * szg;
   const uint64_t rb = std::min(st->host_result_elems, st->sync->shard_elems) * 4;
-  const int s = st->cfg.s, nslot = st->cfg.resident_grads ? s : 1;
+  if (st->compute) {  // inputs X of every micro-step and local rank (tokens x hidden bf16), then the step
+    const uint64_t xb = st->T * st->h * 2;
+    const uint64_t rb = std::min(st->host_result_elems, st->sync->shard_elems) * 4;
+    for (int it = 0; it < iters; ++it) {
+      for (int t = 0; t < st->cfg.s; ++t)
+        for (int r = 0; r < ctx->n; ++r)
+          if (ctx->local(r))
+            MICS_CUDA(cudaMemcpyAsync(ctx->rank_ptr(st->x, r) + uint64_t(t) * xb, host_grads, xb,
+                                      cudaMemcpyHostToDevice, ctx->stream));
+      enqueue_compute_step(st, nullptr);
+      st->step_idx++;
+      if (host_result) {
+        int li = 0;
+        for (int r = 0; r < ctx->n; ++r)
+          if (ctx->local(r))
+            MICS_CUDA(cudaMemcpyAsync(static_cast<char*>(host_result) + uint64_t(li++) * rb,
+                                      ctx->rank_ptr(st->master, r), rb, cudaMemcpyDeviceToHost, ctx->stream));
+      }
+    }
+    st->stats.adam_step = st->adam_step;
+    return;
+  }
+  const int s = st->cfg.s, nslot = st->gslots;
   if (!st->copy_stream) {
     MICS_CUDA(cudaStreamCreateWithFlags(&st->copy_stream, cudaStreamNonBlocking));
     st->ev_h2d.resize(size_t(nslot));

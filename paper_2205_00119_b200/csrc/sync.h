@@ -97,4 +97,17 @@ struct mics_step {
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> ev_h2d, ev_rs_slot;
   cudaEvent_t ev_begin = nullptr;
+  // ---- step with compute (cfg.compute): layer l is W_l = gathered[0, E_l) viewed as
+  // [rows_l = E_l / h, h]; X [T, h] per rank and micro-step slot; Y_l [T, ldy_l] stored
+  // (or one recomputed scratch); dX [T, h] fp32.  Three streams: gathers (gs), GEMMs
+  // (cs) and the reduce-scatters + boundary on ctx->stream, ordered by events.
+  bool compute = false, recompute = false;
+  uint64_t T = 0, h = 0;
+  std::vector<uint64_t> rows, ldy, yoff;
+  mics_buf x{}, y{}, dx{};
+  int gslots = 1;                                    // gradient slots (micro-step t -> t % gslots)
+  std::vector<mics::GemmLaunch> gfwd, gdgrad, gwgrad;  // [(t * L + l) * per + local rank]
+  cudaStream_t gs = nullptr, cs = nullptr;
+  cudaEvent_t ev_g[2] = {}, ev_free[2] = {}, ev_fork = nullptr, ev_jg = nullptr, ev_jc = nullptr;
+  std::vector<cudaEvent_t> ev_wg, ev_rsd;
 };

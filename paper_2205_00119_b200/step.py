@@ -25,6 +25,12 @@ class Workload:
     n: int = 8
     micro_batch: int = 8          # samples per rank per micro-step
     note: str = ""
+    hidden: int = 0               # step with compute: columns of X; layer l is W_l [E_l / hidden, hidden]
+    seq_len: int = 1              # tokens per sample (X has micro_batch * seq_len rows)
+
+    @property
+    def tokens(self) -> int:
+        return self.micro_batch * self.seq_len
 
     @property
     def params(self) -> int:
@@ -37,13 +43,16 @@ def workloads() -> dict:
     gpt2_xl = transformer_layer_params(1600, 6400, 48, 50257, 1024)
     bert_10b = transformer_layer_params(2560, 10240, 127, 32008, 512)
     return {
-        "C1": Workload("C1 4-layer MLP H=1024 (W+b), n=8, p=2, s=4, fp32", [1024 * 1024 + 1024] * 4, p=2, s=4),
-        "C3": Workload("C3 BERT-large-shaped 334M, n=8, p=2, s=4, fp32 grads", bert_large, p=2, s=4),
+        "C1": Workload("C1 4-layer MLP H=1024 (W+b), n=8, p=2, s=4, fp32", [1024 * 1024 + 1024] * 4, p=2, s=4,
+                       hidden=1024),
+        "C3": Workload("C3 BERT-large-shaped 334M, n=8, p=2, s=4, fp32 grads", bert_large, p=2, s=4, hidden=1024,
+                       seq_len=512),
         "C4": Workload("C4 GPT-2 1.5B-shaped, n=8, p=4, hierarchical k=2, bf16 grads", gpt2_xl, p=4, s=4,
-                       grad_dtype="bf16", hier_k=2),
-        "C5p2": Workload("C5 10B dense (BERT-10B), n=8, p=2, bf16 grads", bert_10b, p=2, s=4, grad_dtype="bf16"),
+                       grad_dtype="bf16", hier_k=2, hidden=1600, seq_len=1024),
+        "C5p2": Workload("C5 10B dense (BERT-10B), n=8, p=2, bf16 grads", bert_10b, p=2, s=4, grad_dtype="bf16",
+                         hidden=2560, seq_len=512),
         "C5p8": Workload("C5 10B dense (BERT-10B), n=8, p=8 (ZeRO-3), bf16 grads", bert_10b, p=8, s=4,
-                         grad_dtype="bf16"),
+                         grad_dtype="bf16", hidden=2560, seq_len=512),
     }
 
 
@@ -57,6 +66,8 @@ class StepOptions:
     beta2: float = 0.999
     eps: float = 1e-8
     weight_decay: float = 0.0
+    compute: bool = False         # layer GEMMs in the step (tcgen05, K7); gradients come from them
+    recompute: bool = False       # recompute Y_l in the backward pass instead of storing it
 
 
 class MicsStep:
@@ -70,7 +81,8 @@ class MicsStep:
         cfg = StepCfg(wl.p, wl.s, len(wl.layer_params), C.cast(self._layers, C.POINTER(C.c_uint64)),
                       DTYPE[wl.grad_dtype], wl.hier_k, int(opts.resident_grads), int(opts.alternative), opts.seed,
                       opts.lr, opts.beta1,
-                      opts.beta2, opts.eps, opts.weight_decay)
+                      opts.beta2, opts.eps, opts.weight_decay, int(opts.compute), int(opts.recompute),
+                      wl.tokens if opts.compute else 0, wl.hidden if opts.compute else 0)
         h = C.c_void_p()
         check(lib.mics_step_create(engine.ctx, C.byref(cfg), C.byref(h)))
         self.h = h
@@ -89,9 +101,11 @@ class MicsStep:
                                      C.c_void_p(host_result_ptr) if host_result_ptr else None))
 
     def profile(self) -> dict:
-        a, r, b, g = C.c_double(), C.c_double(), C.c_double(), C.c_double()
-        check(lib.mics_step_profile(self.engine.ctx, self.h, C.byref(a), C.byref(r), C.byref(b), C.byref(g)))
-        return {"allgather_ms": a.value, "reducescatter_ms": r.value, "boundary_ms": b.value, "generate_ms": g.value}
+        """One serialised step with CUDA events around every phase (ms)."""
+        ms = (C.c_double * 5)()
+        check(lib.mics_step_profile_ex(self.engine.ctx, self.h, ms))
+        return {"allgather_ms": ms[0], "reducescatter_ms": ms[1], "boundary_ms": ms[2], "generate_ms": ms[3],
+                "gemm_ms": ms[4]}
 
     def stats(self) -> StepStats:
         s = StepStats()
