@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--p", type=int, default=0, help="override the workload's partition group size (ablation)")
     ap.add_argument("--micro-steps", type=int, default=0, help="override s, micro-steps per step (ablation)")
     ap.add_argument("--sweep", action="store_true", help="C2 collective sweep instead of the step")
+    ap.add_argument("--compute", action="store_true",
+                    help="headline = the step with its layer GEMMs (tcgen05), gathers overlapped with compute")
+    ap.add_argument("--no-compute", action="store_true", help="skip the step-with-compute sub-measurement")
+    ap.add_argument("--compute-steps", type=int, default=3)
     return ap.parse_args()
 
 
@@ -109,8 +113,9 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- helpers
-def arena_bytes(wl, per, resident, n=N_RANKS, alternative=False):
-    """Per-process arena for `per` local ranks (mirrors csrc/step.cpp's allocations)."""
+def arena_bytes(wl, per, resident, n=N_RANKS, alternative=False, compute=None):
+    """Per-process arena for `per` local ranks (mirrors csrc/step.cpp's allocations).
+    compute: None (communication step) or "store" / "recompute" (step with compute)."""
     p, s = wl.p, wl.s
     chunks = [((e + p - 1) // p + 7) // 8 * 8 for e in wl.layer_params]
     S = sum(chunks)
@@ -118,7 +123,12 @@ def arena_bytes(wl, per, resident, n=N_RANKS, alternative=False):
     sub = ((S + r - 1) // r + 3) // 4 * 4
     szg = 2 if wl.grad_dtype == "bf16" else 4
     gathered = 2 * (((max(chunks) * p * 2) + 255) // 256 * 256)
-    per_rank = r * sub * 4 + S * 2 + 3 * S * 4 + gathered + (s if resident else 1) * p * S * szg
+    slots = min(2, s) if compute else (s if resident else 1)
+    per_rank = r * sub * 4 + S * 2 + 3 * S * 4 + gathered + slots * p * S * szg
+    if compute:
+        T, h = wl.tokens, wl.hidden
+        ldy = [(e // h + 7) // 8 * 8 for e in wl.layer_params]
+        per_rank += s * T * h * 2 + T * h * 4 + T * (max(ldy) if compute == "recompute" else sum(ldy)) * 2
     if alternative:  # all-n reduce-scatter scratch: n slices of ceil(p*chunk/n) per layer
         per_rank += sum(-(-p * c // n) * n for c in chunks) * 4
     elif os.environ.get("MICS_PIPELINE") == "1":  # pipelined boundary: second gradient accumulator
@@ -290,6 +300,104 @@ def nccl_step(wl, rank, world, steps, warmup):
                     "groups + torch.optim.Adam(fused=True), same shapes"}
 
 
+# ----------------------------------------------------------------------------- step with compute
+def measure_compute(args, wl, rank, world, local):
+    """The MiCS step with its layer GEMMs (tcgen05, K7): gradients come from the GEMMs,
+    gathers prefetch on their own stream under the GEMMs (SURVEY §8f items 2+3).
+    Returns the measurement dict (rank 0's view, times max over ranks)."""
+    import torch
+
+    from paper_2205_00119_b200 import dist as mdist
+    from paper_2205_00119_b200.engine import Engine, host_alloc, host_free
+    from paper_2205_00119_b200.step import MicsStep, StepOptions
+
+    n = args.ranks
+    per = n // world
+    free = torch.cuda.mem_get_info(local)[0]
+    mode = "store"
+    if arena_bytes(wl, per, False, n, compute="store") > 0.92 * free:
+        mode = "recompute"  # activations do not fit: recompute Y_l in the backward pass
+    need = arena_bytes(wl, per, False, n, compute=mode)
+    if need > 0.95 * free:
+        return {"error": f"{per} ranks/GPU need {need / 1e9:.1f} GB, {free / 1e9:.1f} GB free"}
+    eng = Engine(n_ranks=n, world=world, world_rank=rank, device=local, arena_bytes=need)
+    mdist.connect(eng, GLOO)
+    step = MicsStep(eng, wl, StepOptions(compute=True, recompute=mode == "recompute"))
+    stats = step.stats()
+    ext = torch.cuda.ExternalStream(eng.stream())
+    steps = max(2, args.compute_steps)
+    step.run(args.warmup)
+    eng.synchronize()
+    barrier(world)
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = eng.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eng.barrier()
+    eng.synchronize()
+    barrier(world)
+    e0.record(ext)
+    step.run(steps)
+    e1.record(ext)
+    e1.synchronize()
+    eng.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    launches = (eng.launches - l0) // steps
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    prof = step.profile()  # serialised: every phase timed alone
+    prof = {k: max_over_ranks(v, world) for k, v in prof.items()}
+    serial_ms = sum(prof[k] for k in ("allgather_ms", "reducescatter_ms", "boundary_ms", "gemm_ms"))
+    comm_ms = serial_ms - prof["gemm_ms"]
+    pk, pk_kind = peaks()
+    tf_peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    gemm_tflops = stats.compute_flops / (prof["gemm_ms"] / 1e3) / 1e12 if prof["gemm_ms"] > 0 else 0.0
+    samples = n * MICRO_BATCH * wl.s
+    out = {"value": samples / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms, "steps": steps,
+           "activations": mode, "tokens_per_micro_batch": wl.tokens, "hidden": wl.hidden,
+           "model": "parallel-branch linear proxy: layer l = its parameters as W_l [E_l/hidden, hidden], "
+                    "loss 1/2 sum_l ||X W_l^T||^2 (fwd Y=XW^T, bwd dX+=YW, dW=Y^T X; no attention/norms)",
+           "tflop_per_step_per_gpu": stats.compute_flops / 1e12,
+           "achieved_tflops_per_gpu": stats.compute_flops / (ms / 1e3) / 1e12,
+           "serialised_phases_ms": prof, "serialised_ms": serial_ms,
+           "overlap": {"comm_ms": comm_ms, "gemm_ms": prof["gemm_ms"],
+                       "hidden_comm_frac": max(0.0, min(1.0, (serial_ms - ms) / comm_ms)) if comm_ms > 0 else None},
+           "roofline": {"bound": "tensor", "kernel": "k_gemm (tcgen05 bf16, K7)", "achieved": gemm_tflops,
+                        "peak": tf_peak, "unit": "TFLOP/s", "frac": gemm_tflops / tf_peak,
+                        "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({pk_kind}; kernel inside a long "
+                                       "step)", "traffic": None,
+                        "launch_ms": prof["gemm_ms"] / max(1, stats.gemm_launches),
+                        "launches_per_step": stats.gemm_launches},
+           "gpu_launches": launches * steps, "clocks": clk}
+    if not args.no_e2e and args.e2e_steps > 0:
+        xb = wl.tokens * wl.hidden * 2
+        host, hptr = host_alloc(xb)
+        import numpy as np
+        host[:] = np.random.default_rng(rank).integers(0x3c00, 0x3f80, xb // 2, dtype=np.uint16).view(np.uint8)
+        res, rptr = host_alloc(per * 4096 * 4)
+        step.run_host(hptr, 1, rptr)
+        eng.synchronize()
+        barrier(world)
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        h0.record(ext)
+        step.run_host(hptr, args.e2e_steps, rptr)
+        h1.record(ext)
+        h1.synchronize()
+        wall = (time.perf_counter() - t0) / args.e2e_steps
+        ems = max_over_ranks(max(h0.elapsed_time(h1) / args.e2e_steps, wall * 1e3), world)
+        out["e2e"] = {"value": samples / (ems / 1e3), "unit": "samples/s", "ms_per_step": ems,
+                      "h2d_bytes_per_step": per * wl.s * xb, "d2h_bytes_per_step": per * 4096 * 4,
+                      "path": "mics_step_run_host (C-ABI): pinned host inputs X (tokens x hidden bf16) -> H2D every "
+                              "micro-step and rank, updated master slice D2H after the boundary"}
+        host_free(hptr)
+        host_free(rptr)
+    step.close()
+    eng.close()
+    return out
+
+
 # ----------------------------------------------------------------------------- main arm
 def run_mics(args, wl, rank, world, local):
     import torch
@@ -447,10 +555,40 @@ def run_mics(args, wl, rank, world, local):
         "cpu_baseline": cpu,
         "nccl_comparator": nccl,
     }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
     step.close()
     eng.close()
+    if not args.no_compute and wl.hidden and args.schedule == "two_hop":
+        try:
+            line["compute_step"] = measure_compute(args, wl, rank, world, local)
+        except Exception as e:  # noqa: BLE001  (the headline stays the communication step)
+            line["compute_step"] = {"error": str(e)[:300]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_compute_headline(args, wl, rank, world, local):
+    """`--compute`: the step with its layer GEMMs as the headline line."""
+    c = measure_compute(args, wl, rank, world, local)
+    if "error" in c:
+        raise SystemExit(c["error"])
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, os.cpu_count() or 1)
+    line = {"metric": "MiCS step samples/s (with layer GEMMs)", "value": c["value"], "unit": "samples/s",
+            "n_gpus": world, "steps": c["steps"], "warmup": args.warmup, "ms_per_step": c["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16 GEMMs, f32 sync",
+            "data": "synthetic",
+            "config": {"workload": wl.name + " + layer GEMMs", "n_ranks": args.ranks, "ranks_per_gpu":
+                       args.ranks // world, "p": wl.p, "s": wl.s, "micro_batch": MICRO_BATCH,
+                       "tokens_per_micro_batch": wl.tokens, "hidden": wl.hidden, "params": wl.params,
+                       "grad_dtype": wl.grad_dtype, "activations": c["activations"],
+                       "l2": "inputs larger than L2", "launch": "CUDA graph replay (gathers / GEMMs / sync streams)"},
+            "roofline": c["roofline"], "e2e": c.get("e2e"), "gpu_launches": c["gpu_launches"],
+            "clocks": c["clocks"], "cpu_baseline": cpu,
+            "detail": {k: c[k] for k in ("model", "tflop_per_step_per_gpu", "achieved_tflops_per_gpu",
+                                         "serialised_phases_ms", "serialised_ms", "overlap")}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 def main():
@@ -480,6 +618,8 @@ def main():
         run_sweep(args, rank, world, local)
     elif args.impl == "reference":
         run_reference(args, wl, rank)
+    elif args.compute:
+        run_compute_headline(args, wl, rank, world, local)
     else:
         run_mics(args, wl, rank, world, local)
     if world > 1:

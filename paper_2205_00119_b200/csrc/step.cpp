@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -274,8 +275,17 @@ void setup_compute(mics_step* st) {
         st->gdgrad.push_back(plan_gemm(Y, ldy, 0, W, st->h, 1, dX, st->h, MICS_F32, T, h, rows, l != L - 1));
         st->gwgrad.push_back(plan_gemm(Y, ldy, 1, X, st->h, 1, dW, st->h, cfg.grad_t, rows, h, T, 0));
       }
-  MICS_CUDA(cudaStreamCreateWithFlags(&st->gs, cudaStreamNonBlocking));
-  MICS_CUDA(cudaStreamCreateWithFlags(&st->cs, cudaStreamNonBlocking));
+  // Gathers are on the critical path (layer l+1's GEMMs wait for them): highest
+  // priority; GEMMs lowest, so a freed SM slot goes to a waiting gather first.
+  int prio_lo = 0, prio_hi = 0;
+  MICS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  MICS_CUDA(cudaStreamCreateWithPriority(&st->gs, cudaStreamNonBlocking, prio_hi));
+  MICS_CUDA(cudaStreamCreateWithPriority(&st->cs, cudaStreamNonBlocking, prio_lo));
+  // The micro-step reduce-scatters run under the next micro-step's GEMMs: one CTA per
+  // SM (its registers and shared-memory table fit beside a GEMM CTA), so they never
+  // keep the GEMMs' CTAs from becoming resident.
+  for (auto& v : st->micro)
+    for (auto& x : v) x.grid = std::min(x.grid, ctx->nsm);
   for (cudaEvent_t* e : {&st->ev_g[0], &st->ev_g[1], &st->ev_free[0], &st->ev_free[1], &st->ev_fork, &st->ev_jg,
                          &st->ev_jc})
     MICS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -306,9 +316,58 @@ enum { PH_AG = 0, PH_RS = 1, PH_BND = 2, PH_GEN = 3, PH_GEMM = 4 };
 //   gather(l) waits ev_free[l%2] (the GEMMs that read that buffer last), GEMMs(l)
 //   wait ev_g[l%2]; RS(t) waits ev_wg[slot] (all dW of t); the first dW GEMM of t
 //   waits ev_rsd[slot] (the RS that read that gradient slot last).
+// MICS_TRACE=<file>: eager compute steps record timing events around every gather,
+// GEMM group and reduce-scatter on their own streams and append a timeline
+// (op, t, l, start_ms, end_ms) to <file> — the overlap evidence without nsys.
+struct Trace {
+  struct Op {
+    std::string name;
+    int t, l;
+    cudaEvent_t a, b;
+  };
+  std::vector<Op> ops;
+  cudaEvent_t origin = nullptr;
+  void begin(cudaStream_t s, const char* name, int t, int l) {
+    Op o{name, t, l, nullptr, nullptr};
+    MICS_CUDA(cudaEventCreate(&o.a));
+    MICS_CUDA(cudaEventCreate(&o.b));
+    MICS_CUDA(cudaEventRecord(o.a, s));
+    ops.push_back(o);
+  }
+  void end(cudaStream_t s) { MICS_CUDA(cudaEventRecord(ops.back().b, s)); }
+};
+Trace* trace_for(mics_step* st) {
+  static const char* path = std::getenv("MICS_TRACE");
+  if (!path || st->capturing) return nullptr;
+  return new Trace();
+}
+void trace_flush(Trace* tr, mics_ctx* ctx) {
+  if (!tr) return;
+  static const char* path = std::getenv("MICS_TRACE");
+  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+  MICS_CUDA(cudaDeviceSynchronize());
+  FILE* f = std::fopen((std::string(path) + "." + std::to_string(ctx->wrank)).c_str(), "a");
+  for (auto& o : tr->ops) {
+    float a = 0, b = 0;
+    MICS_CUDA(cudaEventElapsedTime(&a, tr->origin, o.a));
+    MICS_CUDA(cudaEventElapsedTime(&b, tr->origin, o.b));
+    if (f) std::fprintf(f, "%d,%s,%d,%d,%.4f,%.4f\n", ctx->wrank, o.name.c_str(), o.t, o.l, a, b);
+    cudaEventDestroy(o.a);
+    cudaEventDestroy(o.b);
+  }
+  if (f) std::fclose(f);
+  cudaEventDestroy(tr->origin);
+  delete tr;
+}
+
 void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
   mics_ctx* ctx = st->ctx;
   const bool serial = clk != nullptr;
+  Trace* tr = serial ? nullptr : trace_for(st);
+  if (tr) {
+    MICS_CUDA(cudaEventCreate(&tr->origin));
+    MICS_CUDA(cudaEventRecord(tr->origin, ctx->stream));
+  }
   cudaStream_t M = ctx->stream, G = serial ? M : st->gs, C = serial ? M : st->cs;
   const int L = st->cfg.nlayers, s = st->cfg.s, per = ctx->per;
   auto rec = [&](cudaEvent_t e, cudaStream_t on) {
@@ -323,9 +382,12 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
       ctx->launches++;
     }
   };
+  int cur_t = 0;
   auto gather = [&](int l) {
     wait(G, st->ev_free[l % 2]);
+    if (tr) tr->begin(G, "gather", cur_t, l);
     for (auto& x : st->ag[size_t(l)]) enqueue(ctx, x, -1, G);
+    if (tr) tr->end(G);
     if (clk) clk->mark(PH_AG);
     rec(st->ev_g[l % 2], G);
     wait(C, st->ev_g[l % 2]);
@@ -338,9 +400,12 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
   if (clk) clk->mark(-1);
   for (int t = 0; t < s; ++t) {
     const int slot = t % st->gslots;
+    cur_t = t;
     for (int l = 0; l < L; ++l) {
       gather(l);
+      if (tr) tr->begin(C, "fwd", t, l);
       gemms(st->gfwd, size_t(t * L + l) * size_t(per));
+      if (tr) tr->end(C);
       if (clk) clk->mark(PH_GEMM);
       rec(st->ev_free[l % 2], C);
     }
@@ -348,24 +413,31 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
     for (int l = L; l-- > 0;) {
       gather(l);
       const size_t base = size_t(t * L + l) * size_t(per);
+      if (tr) tr->begin(C, "bwd", t, l);
       if (st->recompute) gemms(st->gfwd, base);
       gemms(st->gdgrad, base);
       gemms(st->gwgrad, base);
+      if (tr) tr->end(C);
       if (clk) clk->mark(PH_GEMM);
       rec(st->ev_free[l % 2], C);
     }
     rec(st->ev_wg[size_t(slot)], C);
     wait(M, st->ev_wg[size_t(slot)]);
+    if (tr) tr->begin(M, "rs", t, -1);
     for (auto& x : st->micro[size_t(t)]) enqueue(ctx, x, -1, M);
+    if (tr) tr->end(M);
     if (clk) clk->mark(PH_RS);
     rec(st->ev_rsd[size_t(slot)], M);
   }
+  if (tr) tr->begin(M, "boundary", s, -1);
   enqueue_boundary(st, false);
+  if (tr) tr->end(M);
   if (clk) clk->mark(PH_BND);
   rec(st->ev_jg, G);
   rec(st->ev_jc, C);
   wait(M, st->ev_jg);
   wait(M, st->ev_jc);
+  trace_flush(tr, ctx);
 }
 
 // the main stream waits for the side stream, so a main-stream sync covers the step
@@ -620,6 +692,20 @@ void build_graph(mics_step* st) {
   }
   st->capturing = false;
   MICS_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+  if (st->compute) {
+    // events recorded during the capture belong to the graph: eager steps (profile,
+    // run_host) after it need events that were never captured
+    for (cudaEvent_t* e : {&st->ev_g[0], &st->ev_g[1], &st->ev_free[0], &st->ev_free[1], &st->ev_fork, &st->ev_jg,
+                           &st->ev_jc}) {
+      MICS_CUDA(cudaEventDestroy(*e));
+      MICS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    for (auto* v : {&st->ev_wg, &st->ev_rsd})
+      for (auto& e : *v) {
+        MICS_CUDA(cudaEventDestroy(e));
+        MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+  }
   st->graph_launches = ctx->launches - launches0;
   ctx->launches = launches0;
   st->adam_step = adam_step0;

@@ -116,6 +116,13 @@ def test_compute_step(oracle, monkeypatch, recompute, grad_dtype, graph):
     per_layer = sum(6 * T * e for e in layers) * (4 / 3 if recompute else 1)
     assert abs(st.compute_flops - n * s * per_layer) < 1e-6 * st.compute_flops
     assert st.gemm_launches == n * s * len(layers) * (4 if recompute else 3)
+    # an eager host-input step after the graph was captured (fresh events), then a profile
+    from paper_2205_00119_b200.engine import host_alloc, host_free
+    host, hptr = host_alloc(T * h * 2)
+    host[:] = oracle.gen_bf16(5, 0, 0, 254, 0, T * h).view(np.uint8)
+    step.run_host(hptr, 1)
+    eng.synchronize()
+    host_free(hptr)
     prof = step.profile()
     assert prof["gemm_ms"] > 0 and prof["allgather_ms"] > 0 and prof["reducescatter_ms"] > 0
     step.close()
