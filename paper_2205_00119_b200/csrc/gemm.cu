@@ -11,14 +11,19 @@
 //   dgrad    dX = dY · W   A = dY (K-major), B = W  (N-major)
 //   wgrad    dW = dYᵀ · X  A = dY (M-major), B = X  (N-major)
 //
-// Structure (one CTA per SM, persistent over 128x256 output tiles):
-//   warp 0      TMA producer: 128B-swizzled boxes of A and B into a 4-stage ring
+// Structure (one CTA per SM, CTA pairs as thread-block clusters, persistent over
+// pairs of 128x256 output tiles that share their B tile):
+//   warp 0      TMA producer: 128B-swizzled boxes of A and B into a 4-stage ring;
+//               each CTA loads its own A tile and HALF of the shared B tile,
+//               multicast into both CTAs of the pair (L2->SM traffic 48 -> 32 KiB
+//               per k-block and CTA)
 //   warp 1      MMA issuer: one thread issues tcgen05.mma (M=128, N=256, K=16)
 //               into one of two TMEM accumulators (2 x 256 columns)
 //   warps 2..5  epilogue: tcgen05.ld accumulator rows -> registers -> fp32/bf16
 //               stores (optionally C += acc), overlapping the next tile's MMAs
-// Stage ring: full[s] (TMA bytes landed) / empty[s] (tcgen05.commit after the MMAs
-// that read it); accumulators: tmem_full[a] (commit) / tmem_empty[a] (epilogue).
+// Stage ring: full[s] (TMA bytes landed: own A + both B halves) / empty[s] (the
+// tcgen05.commit of BOTH CTAs' MMAs, multicast, since the peer's producer writes
+// into this CTA's stage); accumulators: tmem_full[a] (commit) / tmem_empty[a].
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -36,6 +41,8 @@ constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KiB
 constexpr uint32_t kBBytes = kBN * kBK * 2;  // 32 KiB
 constexpr uint32_t kStageBytes = kABytes + kBBytes;
 constexpr int kGemmThreads = 192;
+constexpr int kCluster = 2;                  // CTA pair sharing the B tile (multicast)
+constexpr uint32_t kBHalfBytes = kBBytes / kCluster;
 constexpr uint32_t kTmemCols = 2 * kBN;  // double-buffered accumulator
 constexpr uint32_t kSmemBytes = kStages * kStageBytes + 1024 /* align */ + 256 /* barriers */;
 
@@ -81,6 +88,22 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint32_t dst
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint32_t dst, uint32_t bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
@@ -102,6 +125,13 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint6
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+// arrive on the barrier at the same offset in every CTA of `mask`
+__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"(mask)
+      : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
@@ -136,11 +166,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
   const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int crank = int(cluster_rank());
+  constexpr uint16_t kMask = (1u << kCluster) - 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, kCluster);  // one commit from each CTA of the pair
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
@@ -157,19 +189,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   fence_before();
-  __syncthreads();
+  cluster_sync();  // the peer's barriers are initialised before any multicast reaches them
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // work unit = a pair of vertically adjacent tiles (same n0); CTA `crank` takes the
+  // m-block 2*mp + crank (possibly past M: zero-filled loads, masked stores)
   const int tiles_m = (P.M + kBM - 1) / kBM, tiles_n = (P.N + kBN - 1) / kBN;
-  const int ntiles = tiles_m * tiles_n, nk = (P.K + kBK - 1) / kBK;
+  const int tiles_mp = (tiles_m + 1) / 2;
+  const int ntiles = tiles_mp * tiles_n, nk = (P.K + kBK - 1) / kBK;
+  const int cid = blockIdx.x / kCluster, ncl = gridDim.x / kCluster;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int m0 = (t % tiles_m) * kBM, n0 = (t / tiles_m) * kBN;
+      for (int t = cid; t < ntiles; t += ncl) {
+        const int m0 = (2 * (t % tiles_mp) + crank) * kBM, n0 = (t / tiles_mp) * kBN;
         for (int kb = 0; kb < nk; ++kb) {
           const uint32_t full = full0 + 8 * stage;
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
@@ -182,11 +218,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           } else {
             tma_load_2d(&tma_a, sa, full, k0, m0);
           }
+          // this CTA's half of the shared B tile, multicast into both CTAs of the pair
           if (P.b_mn) {
 #pragma unroll
-            for (int j = 0; j < kBN / 64; ++j) tma_load_2d(&tma_b, sb + j * 8192, full, n0 + 64 * j, k0);
+            for (int j = 0; j < kBN / 64 / kCluster; ++j) {
+              const int jj = crank * (kBN / 64 / kCluster) + j;
+              tma_load_2d_mc(&tma_b, sb + jj * 8192, full, n0 + 64 * jj, k0, kMask);
+            }
           } else {
-            tma_load_2d(&tma_b, sb, full, k0, n0);
+            tma_load_2d_mc(&tma_b, sb + crank * kBHalfBytes, full, k0, n0 + crank * (kBN / kCluster), kMask);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -204,7 +244,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t a_lbo = P.a_mn ? 8192u : 16u, b_lbo = P.b_mn ? 8192u : 16u;
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = cid; t < ntiles; t += ncl) {
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         fence_after();
         const uint32_t d = tmem_base + uint32_t(acc * kBN);
@@ -218,7 +258,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint64_t bd = umma_desc(sb + k * b_step, b_lbo, 1024);
             umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
           }
-          umma_commit(empty0 + 8 * stage);  // frees the stage once these MMAs have read it
+          umma_commit_mc(empty0 + 8 * stage, kMask);  // frees the stage (both CTAs' copies) once read
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -236,8 +276,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int m0 = (t % tiles_m) * kBM, n0 = (t / tiles_m) * kBN;
+    for (int t = cid; t < ntiles; t += ncl) {
+      const int m0 = (2 * (t % tiles_mp) + crank) * kBM, n0 = (t / tiles_mp) * kBN;
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       fence_after();
       const int m = m0 + row;
@@ -299,7 +339,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   }
   fence_before();
-  __syncthreads();
+  cluster_sync();  // no CTA leaves while its peer may still multicast into it / arrive on it
   if (warp == 0) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols)
@@ -347,7 +387,8 @@ int gemm_grid(int ntiles) {
     MICS_CUDA(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
     return n;
   }();
-  return ntiles < nsm ? ntiles : nsm;
+  const int pairs = nsm / kCluster;
+  return kCluster * (ntiles < pairs ? ntiles : pairs);
 }
 
 }  // namespace
@@ -362,11 +403,12 @@ GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint6
   GemmLaunch g;
   // A(m,k): K-major -> [M rows, K inner]; M-major -> [K rows, M inner]
   g.ma = a_mn ? make_map(a, uint64_t(M), uint64_t(K), lda, 64) : make_map(a, uint64_t(K), uint64_t(M), lda, kBM);
-  g.mb = b_mn ? make_map(b, uint64_t(N), uint64_t(K), ldb, 64) : make_map(b, uint64_t(K), uint64_t(N), ldb, kBN);
+  g.mb = b_mn ? make_map(b, uint64_t(N), uint64_t(K), ldb, 64)
+              : make_map(b, uint64_t(K), uint64_t(N), ldb, kBN / kCluster);  // each CTA loads half the B rows
   GemmParams P{c, ldc, M, N, K, c_t == MICS_BF16, accumulate != 0, a_mn != 0, b_mn != 0};
   static_assert(sizeof(GemmParams) <= sizeof(g.params), "GemmParams fits");
   memcpy(g.params, &P, sizeof(P));
-  g.ntiles = ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN);
+  g.ntiles = (((M + kBM - 1) / kBM + 1) / 2) * ((N + kBN - 1) / kBN);  // tile pairs
   g.grid = gemm_grid(g.ntiles);
   g.flops = 2.0 * double(M) * double(N) * double(K);
   return g;
@@ -375,8 +417,19 @@ GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint6
 void launch_gemm(cudaStream_t s, const GemmLaunch& g) {
   GemmParams P;
   memcpy(&P, g.params, sizeof(P));
-  k_gemm<<<g.grid, kGemmThreads, kSmemBytes, s>>>(g.ma, g.mb, P);
-  MICS_CUDA(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(g.grid));
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kCluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm, g.ma, g.mb, P));
 }
 
 }  // namespace mics
