@@ -36,13 +36,16 @@
 namespace mics {
 namespace {
 
-constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4;
-constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KiB
-constexpr uint32_t kBBytes = kBN * kBK * 2;  // 32 KiB
-constexpr uint32_t kStageBytes = kABytes + kBBytes;
+// One CTA pair (cluster of 2, cta_group::2) computes a 256 x 256 tile: CTA r holds
+// rows [128r, 128r+128) of A and columns [128r, 128r+128) of B in its shared memory,
+// the leader issues M=256 N=256 MMAs that read both halves, and each CTA's TMEM
+// receives its 128 rows x 256 columns.  Per SM and k-block: 16 KiB of A + 16 KiB of B.
+constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 6;
+constexpr int kCluster = 2;
+constexpr uint32_t kABytes = kBM * kBK * 2;              // 16 KiB: this CTA's 128 rows of A
+constexpr uint32_t kBHalfBytes = kBN / kCluster * kBK * 2;  // 16 KiB: this CTA's 128 columns of B
+constexpr uint32_t kStageBytes = kABytes + kBHalfBytes;
 constexpr int kGemmThreads = 192;
-constexpr int kCluster = 2;                  // CTA pair sharing the B tile (multicast)
-constexpr uint32_t kBHalfBytes = kBBytes / kCluster;
 constexpr uint32_t kTmemCols = 2 * kBN;  // double-buffered accumulator
 constexpr uint32_t kSmemBytes = kStages * kStageBytes + 1024 /* align */ + 256 /* barriers */;
 
@@ -96,6 +99,40 @@ __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint32_t 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
 }
+// both CTAs load into their own shared memory; the bytes are counted on the LEADER's barrier
+__device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* map, uint32_t dst, uint32_t leader_bar, int c0,
+                                                int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void umma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_2sm_mc(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -145,10 +182,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// instruction descriptor: fp32 accumulate, bf16 x bf16, M=128, N=256, majors
+// instruction descriptor: fp32 accumulate, bf16 x bf16, M=256 (pair), N=256, majors
 __device__ __forceinline__ uint32_t idesc_bf16(int a_mn, int b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
-         (uint32_t(kBN >> 3) << 17) | (uint32_t(kBM >> 4) << 24);
+         (uint32_t(kBN >> 3) << 17) | (uint32_t((kCluster * kBM) >> 4) << 24);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -171,62 +208,60 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, kCluster);  // one commit from each CTA of the pair
+      mbar_init(full0 + 8 * s, 1);   // leader: its producer's expect_tx (both CTAs' bytes)
+      mbar_init(empty0 + 8 * s, 1);  // the leader's MMA commit, multicast to both CTAs
     }
     for (int a = 0; a < 2; ++a) {
-      mbar_init(tfull0 + 8 * a, 1);
-      mbar_init(tempty0 + 8 * a, 128);
+      mbar_init(tfull0 + 8 * a, 1);                 // the leader's commit, multicast
+      mbar_init(tempty0 + 8 * a, 4 * kCluster);     // leader: one arrival per epilogue warp of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
   }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+  if (warp == 0) {  // the same warp in both CTAs: one pair allocation
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "n"(kTmemCols)
                  : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
   fence_before();
-  cluster_sync();  // the peer's barriers are initialised before any multicast reaches them
+  cluster_sync();  // barriers and TMEM of both CTAs are ready before anything crosses the pair
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // work unit = a pair of vertically adjacent tiles (same n0); CTA `crank` takes the
-  // m-block 2*mp + crank (possibly past M: zero-filled loads, masked stores)
-  const int tiles_m = (P.M + kBM - 1) / kBM, tiles_n = (P.N + kBN - 1) / kBN;
-  const int tiles_mp = (tiles_m + 1) / 2;
-  const int ntiles = tiles_mp * tiles_n, nk = (P.K + kBK - 1) / kBK;
+  // work unit = one 256 x 256 tile per pair; CTA `crank` owns rows m0 + 128*crank
+  // (possibly past M: zero-filled loads, masked stores) and loads B columns
+  // n0 + 128*crank (possibly past N: zero-filled)
+  const int tiles_m = (P.M + kCluster * kBM - 1) / (kCluster * kBM), tiles_n = (P.N + kBN - 1) / kBN;
+  const int ntiles = tiles_m * tiles_n, nk = (P.K + kBK - 1) / kBK;
   const int cid = blockIdx.x / kCluster, ncl = gridDim.x / kCluster;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      const uint32_t leader_full0 = mapa(full0, 0);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < ntiles; t += ncl) {
-        const int m0 = (2 * (t % tiles_mp) + crank) * kBM, n0 = (t / tiles_mp) * kBN;
+        const int m0 = ((t % tiles_m) * kCluster + crank) * kBM;
+        const int nb = (t / tiles_m) * kBN + crank * (kBN / kCluster);
         for (int kb = 0; kb < nk; ++kb) {
-          const uint32_t full = full0 + 8 * stage;
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
-          mbar_expect_tx(full, kStageBytes);
+          const uint32_t lfull = leader_full0 + 8 * stage;
+          if (crank == 0) mbar_expect_tx(full0 + 8 * stage, kCluster * kStageBytes);
           const uint32_t sa = smem_u32(smem + stage * kStageBytes), sb = sa + kABytes;
           const int k0 = kb * kBK;
           if (P.a_mn) {
 #pragma unroll
-            for (int j = 0; j < kBM / 64; ++j) tma_load_2d(&tma_a, sa + j * 8192, full, m0 + 64 * j, k0);
+            for (int j = 0; j < kBM / 64; ++j) tma_load_2d_2sm(&tma_a, sa + j * 8192, lfull, m0 + 64 * j, k0);
           } else {
-            tma_load_2d(&tma_a, sa, full, k0, m0);
+            tma_load_2d_2sm(&tma_a, sa, lfull, k0, m0);
           }
-          // this CTA's half of the shared B tile, multicast into both CTAs of the pair
           if (P.b_mn) {
 #pragma unroll
-            for (int j = 0; j < kBN / 64 / kCluster; ++j) {
-              const int jj = crank * (kBN / 64 / kCluster) + j;
-              tma_load_2d_mc(&tma_b, sb + jj * 8192, full, n0 + 64 * jj, k0, kMask);
-            }
+            for (int j = 0; j < kBN / kCluster / 64; ++j) tma_load_2d_2sm(&tma_b, sb + j * 8192, lfull, nb + 64 * j, k0);
           } else {
-            tma_load_2d_mc(&tma_b, sb + crank * kBHalfBytes, full, k0, n0 + crank * (kBN / kCluster), kMask);
+            tma_load_2d_2sm(&tma_b, sb, lfull, k0, nb);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -236,7 +271,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    if (lane == 0 && crank == 0) {  // ---------------- MMA issuer (leader CTA only)
       const uint32_t idesc = idesc_bf16(P.a_mn, P.b_mn);
       // K-major: the 16-element K slice advances 32 B inside the 128 B swizzle row;
       // MN-major: it advances 16 rows of 128 B.  LBO = distance between 64-wide MN blocks.
@@ -256,28 +291,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ad = umma_desc(sa + k * a_step, a_lbo, 1024);
             const uint64_t bd = umma_desc(sb + k * b_step, b_lbo, 1024);
-            umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+            umma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0);
           }
-          umma_commit_mc(empty0 + 8 * stage, kMask);  // frees the stage (both CTAs' copies) once read
+          umma_commit_2sm_mc(empty0 + 8 * stage, kMask);  // frees this stage in both CTAs once read
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(tfull0 + 8 * acc);  // accumulator complete
+        umma_commit_2sm_mc(tfull0 + 8 * acc, kMask);  // both halves of the accumulator complete
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
     }
-  } else {  // ---------------- epilogue: warps 2..5, TMEM lane quarter = warp % 4
+  } else {  // ---------------- epilogue: warps 2..5 of both CTAs, TMEM lane quarter = warp % 4
     const int q = warp & 3;
     const int row = q * 32 + lane;
+    const uint32_t leader_tempty0 = mapa(tempty0, 0);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cid; t < ntiles; t += ncl) {
-      const int m0 = (2 * (t % tiles_mp) + crank) * kBM, n0 = (t / tiles_mp) * kBN;
+      const int m0 = ((t % tiles_m) * kCluster + crank) * kBM, n0 = (t / tiles_m) * kBN;
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       fence_after();
       const int m = m0 + row;
@@ -331,7 +367,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       fence_before();
-      mbar_arrive(tempty0 + 8 * acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty0 + 8 * acc);  // this warp drained its rows
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -339,10 +376,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   }
   fence_before();
-  cluster_sync();  // no CTA leaves while its peer may still multicast into it / arrive on it
+  cluster_sync();  // no CTA leaves while its pair may still signal or read it
   if (warp == 0) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols)
                  : "memory");
   }
 }
@@ -404,11 +441,11 @@ GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint6
   // A(m,k): K-major -> [M rows, K inner]; M-major -> [K rows, M inner]
   g.ma = a_mn ? make_map(a, uint64_t(M), uint64_t(K), lda, 64) : make_map(a, uint64_t(K), uint64_t(M), lda, kBM);
   g.mb = b_mn ? make_map(b, uint64_t(N), uint64_t(K), ldb, 64)
-              : make_map(b, uint64_t(K), uint64_t(N), ldb, kBN / kCluster);  // each CTA loads half the B rows
+              : make_map(b, uint64_t(K), uint64_t(N), ldb, kBN / kCluster);  // each CTA loads its 128 B rows
   GemmParams P{c, ldc, M, N, K, c_t == MICS_BF16, accumulate != 0, a_mn != 0, b_mn != 0};
   static_assert(sizeof(GemmParams) <= sizeof(g.params), "GemmParams fits");
   memcpy(g.params, &P, sizeof(P));
-  g.ntiles = (((M + kBM - 1) / kBM + 1) / 2) * ((N + kBN - 1) / kBN);  // tile pairs
+  g.ntiles = ((M + kCluster * kBM - 1) / (kCluster * kBM)) * ((N + kBN - 1) / kBN);  // 256 x 256 pair tiles
   g.grid = gemm_grid(g.ntiles);
   g.flops = 2.0 * double(M) * double(N) * double(K);
   return g;
