@@ -416,7 +416,7 @@ CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t 
   return m;
 }
 
-int gemm_grid(int ntiles) {
+int gemm_grid(int ntiles, int max_sms) {
   static int nsm = [] {
     int dev = 0, n = 0;
     MICS_CUDA(cudaGetDevice(&dev));
@@ -424,14 +424,15 @@ int gemm_grid(int ntiles) {
     MICS_CUDA(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
     return n;
   }();
-  const int pairs = nsm / kCluster;
+  const int sms = max_sms > 0 && max_sms < nsm ? max_sms : nsm;
+  const int pairs = sms / kCluster > 0 ? sms / kCluster : 1;
   return kCluster * (ntiles < pairs ? ntiles : pairs);
 }
 
 }  // namespace
 
 GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint64_t ldb, int b_mn, void* c,
-                     uint64_t ldc, mics_dtype c_t, int M, int N, int K, int accumulate) {
+                     uint64_t ldc, mics_dtype c_t, int M, int N, int K, int accumulate, int max_sms) {
   if (M <= 0 || N <= 0 || K <= 0) raise(MICS_OUT_OF_RANGE, "gemm: M, N, K must be positive");
   if (c_t != MICS_F32 && c_t != MICS_BF16) raise(MICS_TYPE_MISMATCH, "gemm: output must be f32 or bf16");
   if (accumulate && c_t != MICS_F32) raise(MICS_TYPE_MISMATCH, "gemm: accumulate needs an f32 output");
@@ -446,7 +447,7 @@ GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint6
   static_assert(sizeof(GemmParams) <= sizeof(g.params), "GemmParams fits");
   memcpy(g.params, &P, sizeof(P));
   g.ntiles = ((M + kCluster * kBM - 1) / (kCluster * kBM)) * ((N + kBN - 1) / kBN);  // 256 x 256 pair tiles
-  g.grid = gemm_grid(g.ntiles);
+  g.grid = gemm_grid(g.ntiles, max_sms);
   g.flops = 2.0 * double(M) * double(N) * double(K);
   return g;
 }

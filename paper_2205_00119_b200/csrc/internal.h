@@ -172,7 +172,7 @@ struct GemmLaunch {
   double flops = 0;
 };
 GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint64_t ldb, int b_mn, void* c,
-                     uint64_t ldc, mics_dtype c_t, int M, int N, int K, int accumulate);
+                     uint64_t ldc, mics_dtype c_t, int M, int N, int K, int accumulate, int max_sms = 0);
 void launch_gemm(cudaStream_t s, const GemmLaunch& g);
 
 AdamScalars make_adam_scalars(double lr, double b1, double b2, double eps, double wd, int step, double grad_scale);

@@ -259,6 +259,14 @@ void setup_compute(mics_step* st) {
       launch_generate(ctx->stream, ctx->rank_ptr(st->x, r) + uint64_t(t) * xe * 2, MICS_BF16, cfg.seed ^ 0xA11CEull,
                       r, t, 254, 0, xe, ctx->nsm * 8);
   }
+  // Optional SM split while gathers / reduce-scatters overlap the GEMMs: the GEMMs
+  // run on nsm - comm_sms SMs (whole CTA pairs), the collectives get comm_sms CTAs
+  // (MICS_COMM_SMS).  Default 0 = share every SM: measured on 2 B200 (C3, 1 rank per
+  // GPU) 37.1 ms/step shared vs 68.4 / 45.8 / 45.4 ms with 8 / 16 / 32 comm SMs — the
+  // pull kernels need many CTAs in flight to cover NVLink latency.
+  st->comm_sms = 0;
+  if (const char* e = std::getenv("MICS_COMM_SMS")) st->comm_sms = std::max(0, std::min(ctx->nsm - 2, std::atoi(e)));
+  const int gemm_sms = st->comm_sms ? ctx->nsm - st->comm_sms : 0;
   const int T = int(st->T), h = int(st->h);
   for (int t = 0; t < s; ++t)
     for (int l = 0; l < L; ++l)
@@ -271,9 +279,10 @@ void setup_compute(mics_step* st) {
         char* Y = ctx->rank_ptr(st->y, r) + st->yoff[size_t(l)] * 2;
         char* dX = ctx->rank_ptr(st->dx, r);
         char* dW = ctx->rank_ptr(st->grads, r) + (uint64_t(t % st->gslots) * sy->grad_elems + sy->grad_off[size_t(l)]) * szg;
-        st->gfwd.push_back(plan_gemm(X, st->h, 0, W, st->h, 0, Y, ldy, MICS_BF16, T, rows, h, 0));
-        st->gdgrad.push_back(plan_gemm(Y, ldy, 0, W, st->h, 1, dX, st->h, MICS_F32, T, h, rows, l != L - 1));
-        st->gwgrad.push_back(plan_gemm(Y, ldy, 1, X, st->h, 1, dW, st->h, cfg.grad_t, rows, h, T, 0));
+        st->gfwd.push_back(plan_gemm(X, st->h, 0, W, st->h, 0, Y, ldy, MICS_BF16, T, rows, h, 0, gemm_sms));
+        st->gdgrad.push_back(
+            plan_gemm(Y, ldy, 0, W, st->h, 1, dX, st->h, MICS_F32, T, h, rows, l != L - 1, gemm_sms));
+        st->gwgrad.push_back(plan_gemm(Y, ldy, 1, X, st->h, 1, dW, st->h, cfg.grad_t, rows, h, T, 0, gemm_sms));
       }
   // Gathers are on the critical path (layer l+1's GEMMs wait for them): highest
   // priority; GEMMs lowest, so a freed SM slot goes to a waiting gather first.
@@ -281,11 +290,20 @@ void setup_compute(mics_step* st) {
   MICS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   MICS_CUDA(cudaStreamCreateWithPriority(&st->gs, cudaStreamNonBlocking, prio_hi));
   MICS_CUDA(cudaStreamCreateWithPriority(&st->cs, cudaStreamNonBlocking, prio_lo));
-  // The micro-step reduce-scatters run under the next micro-step's GEMMs: one CTA per
-  // SM (its registers and shared-memory table fit beside a GEMM CTA), so they never
-  // keep the GEMMs' CTAs from becoming resident.
+  // Overlapped collectives: comm_sms CTAs (or, when sharing every SM, one CTA per SM,
+  // whose registers and shared-memory table fit beside a GEMM CTA).  The serialised
+  // profile step keeps the full grids.
+  const int lean = st->comm_sms ? st->comm_sms : ctx->nsm;
+  for (auto& v : st->ag)
+    for (auto& x : v) {
+      st->ag_grid_full.push_back(x.grid);
+      x.grid = std::min(x.grid, lean);
+    }
   for (auto& v : st->micro)
-    for (auto& x : v) x.grid = std::min(x.grid, ctx->nsm);
+    for (auto& x : v) {
+      st->micro_grid_full.push_back(x.grid);
+      x.grid = std::min(x.grid, lean);
+    }
   for (cudaEvent_t* e : {&st->ev_g[0], &st->ev_g[1], &st->ev_free[0], &st->ev_free[1], &st->ev_fork, &st->ev_jg,
                          &st->ev_jc})
     MICS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -383,10 +401,22 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
     }
   };
   int cur_t = 0;
+  // the serialised (profile) step runs the collectives with their full grids
+  auto ag_index = [&](int l) {
+    size_t i = 0;
+    for (int k = 0; k < l; ++k) i += st->ag[size_t(k)].size();
+    return i;
+  };
   auto gather = [&](int l) {
     wait(G, st->ev_free[l % 2]);
     if (tr) tr->begin(G, "gather", cur_t, l);
-    for (auto& x : st->ag[size_t(l)]) enqueue(ctx, x, -1, G);
+    size_t gi = ag_index(l);
+    for (auto& x : st->ag[size_t(l)]) {
+      Launch y = x;
+      if (serial) y.grid = st->ag_grid_full[gi];
+      ++gi;
+      enqueue(ctx, y, -1, G);
+    }
     if (tr) tr->end(G);
     if (clk) clk->mark(PH_AG);
     rec(st->ev_g[l % 2], G);
@@ -424,7 +454,14 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
     rec(st->ev_wg[size_t(slot)], C);
     wait(M, st->ev_wg[size_t(slot)]);
     if (tr) tr->begin(M, "rs", t, -1);
-    for (auto& x : st->micro[size_t(t)]) enqueue(ctx, x, -1, M);
+    size_t mi = 0;
+    for (int k = 0; k < t; ++k) mi += st->micro[size_t(k)].size();
+    for (auto& x : st->micro[size_t(t)]) {
+      Launch y = x;
+      if (serial) y.grid = st->micro_grid_full[mi];
+      ++mi;
+      enqueue(ctx, y, -1, M);
+    }
     if (tr) tr->end(M);
     if (clk) clk->mark(PH_RS);
     rec(st->ev_rsd[size_t(slot)], M);

@@ -106,6 +106,8 @@ struct mics_step {
   std::vector<uint64_t> rows, ldy, yoff;
   mics_buf x{}, y{}, dx{};
   int gslots = 1;                                    // gradient slots (micro-step t -> t % gslots)
+  int comm_sms = 0;                                  // SMs left to the overlapped collectives (GEMMs get the rest)
+  std::vector<int> ag_grid_full, micro_grid_full;    // grids of the serialised (profile) step
   std::vector<mics::GemmLaunch> gfwd, gdgrad, gwgrad;  // [(t * L + l) * per + local rank]
   cudaStream_t gs = nullptr, cs = nullptr;
   cudaEvent_t ev_g[2] = {}, ev_free[2] = {}, ev_fork = nullptr, ev_jg = nullptr, ev_jc = nullptr;
