@@ -182,6 +182,60 @@ def main():
     for x, y in zip(res["0"], res["1"]):
         expect(np.array_equal(x.view(np.uint32), y.view(np.uint32)), "pipelined boundary != in-order")
 
+    # ---- the step with compute across processes (gathers / GEMMs / sync on three
+    # streams, hierarchical gathers on barrier channel 1): GEMM gradients within
+    # tolerance of fp32, the sync + Adam bit-exact on the gradients the GEMMs produced
+    from test_gpu_step_compute import bf16_bits_to_f32, f32_to_bf16_bits, layer_weights, reduce_and_adam
+    for p, k, gdt in ((2, 0, "f32"), (4, 2, "bf16"), (8, 0, "f32")):
+        e4 = Engine(n_ranks=n, world=world, world_rank=rank, device=local, arena_bytes=256 << 20)
+        mdist.connect(e4)
+        h = 64
+        wl = Workload("mpc", [h * 40, h * 37, h * 56], p=p, s=2, grad_dtype=gdt, hier_k=k, hidden=h, seq_len=16)
+        opts = StepOptions(seed=91, lr=1e-3, compute=True)
+        step = MicsStep(e4, wl, opts)
+        info, segs = step.sync_info()
+        S, G, T = info.shard_elems, info.grad_elems, wl.tokens
+        b = step.buffers()
+        gsz = 2 if gdt == "bf16" else 4
+        for stepno in (1, 2):
+            pb_loc = {r: e4.d2h(b["param_bf16"], r, S, "bf16") for r in e4.local_ranks}
+            init_loc = {r: (e4.d2h(b["master"], r, S), e4.d2h(b["exp_avg"], r, S), e4.d2h(b["exp_avg_sq"], r, S))
+                        for r in e4.local_ranks}
+            step.run(1)
+            e4.synchronize()
+            g_loc = {}
+            for r in e4.local_ranks:
+                gr = np.zeros((2, G), np.float32)
+                for t in range(2):
+                    raw = e4.d2h(b["grads"], r, G, gdt, off=t * G * gsz)
+                    gr[t] = bf16_bits_to_f32(raw) if gdt == "bf16" else raw
+                g_loc[r] = gr
+            allg = [None] * world
+            dist.all_gather_object(allg, (pb_loc, g_loc, init_loc))
+            pb, grads, init = {}, np.zeros((2, n, G), np.float32), {}
+            for d_pb, d_g, d_init in allg:
+                pb.update(d_pb)
+                init.update(d_init)
+                for r, gr in d_g.items():
+                    grads[:, r] = gr
+            for r in e4.local_ranks:  # GEMM gradients vs fp32 (tolerance)
+                g = r // p
+                Ws = layer_weights(pb, segs, h, p, lambda i: g * p + i)
+                for t in range(2):
+                    X = bf16_bits_to_f32(ora.gen_bf16(91 ^ 0xA11CE, r, t, 254, 0, T * h)).reshape(T, h)
+                    for (ln, c, so, go), W in zip(segs, Ws):
+                        Y = bf16_bits_to_f32(f32_to_bf16_bits(X @ W.T))
+                        dW = (Y.T @ X).ravel()
+                        bound = 2e-2 * (np.abs(Y).T @ np.abs(X)).ravel() + 1e-5 + (np.abs(dW) * 2.0 ** -8 if gdt == "bf16" else 0)
+                        expect(bool(np.all(np.abs(grads[t, r, go:go + ln] - dW) <= bound)),
+                               f"compute step p={p} k={k} step={stepno} r={r} t={t}: dW")
+            want = reduce_and_adam(ora, n, p, 2, segs, grads, [init[r] for r in range(n)], opts, step=stepno)
+            for r in e4.local_ranks:
+                expect(np.array_equal(e4.d2h(b["master"], r, S).view(np.uint32), want[r][0].view(np.uint32)),
+                       f"compute step p={p} k={k} step={stepno} r={r}: master")
+        step.close()
+        e4.close()
+
     dist.barrier()
     if fails:
         print(f"[rank {rank}] FAILED: {fails}", flush=True)
