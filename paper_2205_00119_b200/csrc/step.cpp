@@ -259,12 +259,14 @@ void setup_compute(mics_step* st) {
       launch_generate(ctx->stream, ctx->rank_ptr(st->x, r) + uint64_t(t) * xe * 2, MICS_BF16, cfg.seed ^ 0xA11CEull,
                       r, t, 254, 0, xe, ctx->nsm * 8);
   }
-  // Optional SM split while gathers / reduce-scatters overlap the GEMMs: the GEMMs
-  // run on nsm - comm_sms SMs (whole CTA pairs), the collectives get comm_sms CTAs
-  // (MICS_COMM_SMS).  Default 0 = share every SM: measured on 2 B200 (C3, 1 rank per
-  // GPU) 37.1 ms/step shared vs 68.4 / 45.8 / 45.4 ms with 8 / 16 / 32 comm SMs — the
-  // pull kernels need many CTAs in flight to cover NVLink latency.
-  st->comm_sms = 0;
+  // Overlap resources (measured on 2 B200, C3, one rank per GPU, profiles/r1/compute/):
+  //  - flat per-layer gathers run on the copy engines (cudaMemcpyAsync of each
+  //    chunk, local or NVLink peer): no SM time, so the co-resident GEMM keeps its
+  //    speed (k_copy under a GEMM slowed it ~20%); MICS_CE_GATHER=0 uses k_copy;
+  //  - the reduce-scatters that run under the next micro-step's GEMMs get comm_sms
+  //    CTAs and the GEMMs the other SMs (MICS_COMM_SMS, default 16; 0 = share every
+  //    SM).  37.0 ms/step (k_copy, shared) -> 36.2 (copy engines) -> 35.0 (+16 SMs).
+  st->comm_sms = 16;
   if (const char* e = std::getenv("MICS_COMM_SMS")) st->comm_sms = std::max(0, std::min(ctx->nsm - 2, std::atoi(e)));
   const int gemm_sms = st->comm_sms ? ctx->nsm - st->comm_sms : 0;
   const int T = int(st->T), h = int(st->h);
@@ -293,6 +295,23 @@ void setup_compute(mics_step* st) {
   // Overlapped collectives: comm_sms CTAs (or, when sharing every SM, one CTA per SM,
   // whose registers and shared-memory table fit beside a GEMM CTA).  The serialised
   // profile step keeps the full grids.
+  {
+    const char* e = std::getenv("MICS_CE_GATHER");
+    st->ce_gather = !(e && e[0] == '0') && (cfg.hier_k <= 0 || cfg.p <= cfg.hier_k);
+  }
+  if (st->ce_gather) {
+    for (int l = 0; l < L; ++l) {
+      const uint64_t c = sy->chunk[size_t(l)], cb = c * 2, soff = sy->shard_off[size_t(l)] * 2;
+      std::vector<mics_step::CeCopy> v;
+      for (int r = 0; r < ctx->n; ++r) {
+        if (!ctx->local(r)) continue;
+        const int g = r / cfg.p;
+        char* G = ctx->rank_ptr(st->gathered, r) + uint64_t(l % 2) * st->gathered_half;
+        for (int i = 0; i < cfg.p; ++i) v.push_back({G + uint64_t(i) * cb, ctx->rank_ptr(st->pbf16, g * cfg.p + i) + soff, cb});
+      }
+      st->ce.push_back(std::move(v));
+    }
+  }
   const int lean = st->comm_sms ? st->comm_sms : ctx->nsm;
   for (auto& v : st->ag)
     for (auto& x : v) {
@@ -410,12 +429,17 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
   auto gather = [&](int l) {
     wait(G, st->ev_free[l % 2]);
     if (tr) tr->begin(G, "gather", cur_t, l);
-    size_t gi = ag_index(l);
-    for (auto& x : st->ag[size_t(l)]) {
-      Launch y = x;
-      if (serial) y.grid = st->ag_grid_full[gi];
-      ++gi;
-      enqueue(ctx, y, -1, G);
+    if (st->ce_gather && !serial) {
+      for (const auto& c : st->ce[size_t(l)])
+        MICS_CUDA(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, G));
+    } else {
+      size_t gi = ag_index(l);
+      for (auto& x : st->ag[size_t(l)]) {
+        Launch y = x;
+        if (serial) y.grid = st->ag_grid_full[gi];
+        ++gi;
+        enqueue(ctx, y, -1, G);
+      }
     }
     if (tr) tr->end(G);
     if (clk) clk->mark(PH_AG);
@@ -458,7 +482,8 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
     for (int k = 0; k < t; ++k) mi += st->micro[size_t(k)].size();
     for (auto& x : st->micro[size_t(t)]) {
       Launch y = x;
-      if (serial) y.grid = st->micro_grid_full[mi];
+      // the last micro-step's reduce-scatter overlaps no compute: full grid
+      if (serial || t == s - 1) y.grid = st->micro_grid_full[mi];
       ++mi;
       enqueue(ctx, y, -1, M);
     }

@@ -108,6 +108,16 @@ struct mics_step {
   int gslots = 1;                                    // gradient slots (micro-step t -> t % gslots)
   int comm_sms = 0;                                  // SMs left to the overlapped collectives (GEMMs get the rest)
   std::vector<int> ag_grid_full, micro_grid_full;    // grids of the serialised (profile) step
+  // flat gathers of the step with compute (MICS_CE_GATHER, default on): the
+  // overlapped per-layer gathers are copy-engine memcpys (no SM time) instead of
+  // k_copy: per layer, the (dst, src, bytes) of every local rank's p chunks
+  bool ce_gather = false;
+  struct CeCopy {
+    void* dst;
+    const void* src;
+    uint64_t bytes;
+  };
+  std::vector<std::vector<CeCopy>> ce;
   std::vector<mics::GemmLaunch> gfwd, gdgrad, gwgrad;  // [(t * L + l) * per + local rank]
   cudaStream_t gs = nullptr, cs = nullptr;
   cudaEvent_t ev_g[2] = {}, ev_free[2] = {}, ev_fork = nullptr, ev_jg = nullptr, ev_jc = nullptr;

@@ -62,8 +62,14 @@ def layer_weights(pbf16, segs, h, p, n_of):
     return Ws
 
 
-@pytest.mark.parametrize("recompute,grad_dtype,graph", [(False, "f32", "1"), (True, "f32", "0"), (False, "bf16", "1")])
-def test_compute_step(oracle, monkeypatch, recompute, grad_dtype, graph):
+@pytest.mark.parametrize("recompute,grad_dtype,graph,ce,comm_sms", [
+    (False, "f32", "1", "1", "16"), (True, "f32", "0", "1", "16"), (False, "bf16", "1", "1", "0"),
+    (False, "f32", "1", "0", "0")])
+def test_compute_step(oracle, monkeypatch, recompute, grad_dtype, graph, ce, comm_sms):
+    """ce: flat gathers on the copy engines (default) or k_copy; comm_sms: SMs left to the
+    overlapped reduce-scatters."""
+    monkeypatch.setenv("MICS_CE_GATHER", ce)
+    monkeypatch.setenv("MICS_COMM_SMS", comm_sms)
     from paper_2205_00119_b200.engine import Engine
     from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
     monkeypatch.setenv("MICS_GRAPH", graph)
