@@ -384,6 +384,7 @@ void trace_flush(Trace* tr, mics_ctx* ctx) {
   MICS_CUDA(cudaStreamSynchronize(ctx->stream));
   MICS_CUDA(cudaDeviceSynchronize());
   FILE* f = std::fopen((std::string(path) + "." + std::to_string(ctx->wrank)).c_str(), "a");
+  if (f) std::fprintf(f, "%d,step,-1,-1,0,0\n", ctx->wrank);  // one block per step
   for (auto& o : tr->ops) {
     float a = 0, b = 0;
     MICS_CUDA(cudaEventElapsedTime(&a, tr->origin, o.a));

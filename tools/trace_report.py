@@ -1,4 +1,5 @@
-"""Summarise a MICS_TRACE timeline (one compute step per block of rows).
+"""Summarise a MICS_TRACE timeline (`<path>.<process>`: a `step` marker row, then one
+row per gather / GEMM group / reduce-scatter / boundary of that step).
 
     python tools/trace_report.py trace.csv [rank]
 
@@ -17,9 +18,11 @@ def main():
         rk, op, t, l, a, b = ln.strip().split(",")
         if int(rk) != want:
             continue
-        if op == "gather" and t == "0" and l == "0" and cur:
-            steps.append(cur)
+        if op == "step":  # csrc/step.cpp writes one marker row per traced step
+            if cur:
+                steps.append(cur)
             cur = []
+            continue
         cur.append((op, int(t), int(l), float(a), float(b)))
     steps.append(cur)
     ops = steps[-1]
