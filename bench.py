@@ -113,6 +113,32 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- helpers
+def bind_to_gpu_numa(local):
+    """Pin this process to the CPUs of the GPU's own NUMA node (sysfs local_cpulist)
+    so the pinned host buffers of the e2e path are allocated next to its PCIe root
+    (MICS_NUMA=0 disables).  Returns the CPU list used, or None."""
+    if os.environ.get("MICS_NUMA") == "0":
+        return None
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(local)
+        bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/local_cpulist") as fh:
+            spec = fh.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return spec
+    except (OSError, AttributeError, ValueError):
+        return None
+    return None
+
+
+
 def arena_bytes(wl, per, resident, n=N_RANKS, alternative=False, compute=None):
     """Per-process arena for `per` local ranks (mirrors csrc/step.cpp's allocations).
     compute: None (communication step) or "store" / "recompute" (step with compute)."""
@@ -407,6 +433,7 @@ def run_mics(args, wl, rank, world, local):
     from paper_2205_00119_b200.engine import Engine, host_alloc, host_free
 
     torch.cuda.set_device(local)
+    numa = bind_to_gpu_numa(local)
     n = args.ranks
     if n % world:
         raise SystemExit(f"--gpus {world} must divide the {n} ranks")
@@ -516,7 +543,8 @@ def run_mics(args, wl, rank, world, local):
         e2e = {"value": samples / (ems / 1e3), "unit": "samples/s", "ms_per_step": ems,
                "h2d_bytes_per_step": per * s * gbytes, "d2h_bytes_per_step": per * min(4096, S) * 4,
                "path": "mics_step_run_host (C-ABI): pinned host gradients -> H2D every micro-step, "
-                       "result slice D2H after the boundary"}
+                       "result slice D2H after the boundary",
+               "host_cpus": numa}
         host_free(hptr)
         host_free(rptr)
 
