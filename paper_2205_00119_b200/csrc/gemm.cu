@@ -29,6 +29,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
 #include <string>
 
 #include "internal.h"
@@ -47,7 +51,10 @@ constexpr uint32_t kBHalfBytes = kBN / kCluster * kBK * 2;  // 16 KiB: this CTA'
 constexpr uint32_t kStageBytes = kABytes + kBHalfBytes;
 constexpr int kGemmThreads = 192;
 constexpr uint32_t kTmemCols = 2 * kBN;  // double-buffered accumulator
-constexpr uint32_t kSmemBytes = kStages * kStageBytes + 1024 /* align */ + 256 /* barriers */;
+// epilogue staging for TMA stores: per epilogue warp two 32 x 32 chunks (fp32 worst case)
+constexpr uint32_t kEpiChunkBytes = 32 * 32 * 4;
+constexpr uint32_t kEpiBytes = 4 * 2 * kEpiChunkBytes;  // 32 KiB
+constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /* align */ + 256 /* barriers */;
 
 struct GemmParams {
   void* c;
@@ -57,6 +64,8 @@ struct GemmParams {
   int beta;     // 1: C += A·B (fp32 output only)
   int a_mn;     // A is M-major (A(m,k) at a[k*lda + m])
   int b_mn;     // B is N-major (B(n,k) at b[k*ldb + n])
+  unsigned long long* probe;  // MICS_GEMM_PROBE: per-CTA stall cycles [8] (debug), else null
+  int tma_store;              // 1: epilogue stores through shared memory with TMA (C map valid)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -193,11 +202,40 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+// TMA store of a staged 32 x 32 chunk (clipped to the tensor bounds by the hardware);
+// `add` reduces into global memory instead (C += chunk, fp32)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1, int add) {
+  if (add)
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1)
+                 : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// wait and, when probing, add the cycles spent to *acc
+__device__ __forceinline__ void mbar_wait_probe(uint32_t bar, uint32_t parity, unsigned long long* acc) {
+  if (!acc) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  const long long t0 = clock64();
+  mbar_wait(bar, parity);
+  *acc += static_cast<unsigned long long>(clock64() - t0);
+}
+
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    k_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, GemmParams P) {
+    k_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+           const __grid_constant__ CUtensorMap tma_c, GemmParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint8_t* epi_smem = smem + kStages * kStageBytes;  // [4 warps][2 buffers][32 x 32 chunk]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
   // bars: full[kStages], empty[kStages], tmem_full[2], tmem_empty[2]; then the TMEM base address
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
@@ -205,6 +243,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int crank = int(cluster_rank());
   constexpr uint16_t kMask = (1u << kCluster) - 1;
+  const long long t_start = P.probe ? clock64() : 0;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -240,13 +279,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       const uint32_t leader_full0 = mapa(full0, 0);
+      unsigned long long w_empty = 0, *pw = P.probe ? &w_empty : nullptr;
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < ntiles; t += ncl) {
         const int m0 = ((t % tiles_m) * kCluster + crank) * kBM;
         const int nb = (t / tiles_m) * kBN + crank * (kBN / kCluster);
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          mbar_wait_probe(empty0 + 8 * stage, phase ^ 1, pw);
           const uint32_t lfull = leader_full0 + 8 * stage;
           if (crank == 0) mbar_expect_tx(full0 + 8 * stage, kCluster * kStageBytes);
           const uint32_t sa = smem_u32(smem + stage * kStageBytes), sb = sa + kABytes;
@@ -269,6 +309,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
+      if (P.probe) P.probe[blockIdx.x * 8 + 2] = w_empty;
     }
   } else if (warp == 1) {
     if (lane == 0 && crank == 0) {  // ---------------- MMA issuer (leader CTA only)
@@ -279,12 +320,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t a_lbo = P.a_mn ? 8192u : 16u, b_lbo = P.b_mn ? 8192u : 16u;
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
+      unsigned long long w_te = 0, w_full = 0;
+      unsigned long long *pte = P.probe ? &w_te : nullptr, *pfu = P.probe ? &w_full : nullptr;
       for (int t = cid; t < ntiles; t += ncl) {
-        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        mbar_wait_probe(tempty0 + 8 * acc, acc_phase ^ 1, pte);
         fence_after();
         const uint32_t d = tmem_base + uint32_t(acc * kBN);
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(full0 + 8 * stage, phase);
+          mbar_wait_probe(full0 + 8 * stage, phase, pfu);
           fence_after();
           const uint32_t sa = smem_u32(smem + stage * kStageBytes), sb = sa + kABytes;
 #pragma unroll
@@ -305,6 +348,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           acc_phase ^= 1;
         }
       }
+      if (P.probe) {
+        P.probe[blockIdx.x * 8 + 0] = w_te;
+        P.probe[blockIdx.x * 8 + 1] = w_full;
+      }
     }
   } else {  // ---------------- epilogue: warps 2..5 of both CTAs, TMEM lane quarter = warp % 4
     const int q = warp & 3;
@@ -312,9 +359,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t leader_tempty0 = mapa(tempty0, 0);
     int acc = 0;
     uint32_t acc_phase = 0;
+    unsigned long long w_tf = 0, busy = 0, *ptf = (P.probe && warp == 2 && lane == 0) ? &w_tf : nullptr;
     for (int t = cid; t < ntiles; t += ncl) {
       const int m0 = ((t % tiles_m) * kCluster + crank) * kBM, n0 = (t / tiles_m) * kBN;
-      mbar_wait(tfull0 + 8 * acc, acc_phase);
+      mbar_wait_probe(tfull0 + 8 * acc, acc_phase, ptf);
+      const long long tb0 = ptf ? clock64() : 0;
       fence_after();
       const int m = m0 + row;
 #pragma unroll 1
@@ -322,6 +371,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         uint32_t v[32];
         tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * kBN + c * 32), v);
         const int n = n0 + c * 32;
+        if (P.tma_store) {
+          // stage this warp's 32 rows x 32 columns in shared memory in the TMA
+          // swizzled layout (16-byte chunk j of row r at j ^ swizzle(r): conflict-free
+          // stores), then one lane stores it to global with TMA (bounds clipped)
+          if (n >= P.N || m0 >= P.M) continue;  // whole chunk outside C (warp-uniform)
+          const int buf = c & 1;
+          uint8_t* stg = epi_smem + (uint32_t(q) * 2 + uint32_t(buf)) * kEpiChunkBytes;
+          if (c >= 2) {  // the store issued from this buffer two chunks ago has read it
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+          }
+          if (P.c_bf16) {  // 64 B rows, SWIZZLE_64B: chunk j -> j ^ ((row >> 1) & 3)
+            uint8_t* row = stg + lane * 64;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 w;
+              w.x = pack_bf16(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+              w.y = pack_bf16(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+              w.z = pack_bf16(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+              w.w = pack_bf16(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+              *reinterpret_cast<uint4*>(row + ((j ^ ((lane >> 1) & 3)) * 16)) = w;
+            }
+          } else {  // 128 B rows, SWIZZLE_128B: chunk j -> j ^ (row & 7)
+            uint8_t* row = stg + lane * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<uint4*>(row + ((j ^ (lane & 7)) * 16)) =
+                  make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
+          __syncwarp();
+          if (lane == 0) tma_store_2d(&tma_c, smem_u32(stg), n, m0 + q * 32, P.beta);
+          continue;
+        }
         if (m >= P.M || n >= P.N) continue;
         if (P.c_bf16) {
           uint16_t* out = static_cast<uint16_t*>(P.c) + uint64_t(m) * P.ldc + n;
@@ -368,15 +451,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       fence_before();
       __syncwarp();
+      if (ptf) busy += static_cast<unsigned long long>(clock64() - tb0);
       if (lane == 0) mbar_arrive_cluster(leader_tempty0 + 8 * acc);  // this warp drained its rows
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (ptf) {
+      P.probe[blockIdx.x * 8 + 3] = busy;
+      P.probe[blockIdx.x * 8 + 5] = w_tf;
+    }
+    // staged chunks must be read (and the stores complete) before the CTA exits
+    if (P.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   fence_before();
   cluster_sync();  // no CTA leaves while its pair may still signal or read it
+  if (P.probe && threadIdx.x == 0) P.probe[blockIdx.x * 8 + 4] = static_cast<unsigned long long>(clock64() - t_start);
   if (warp == 0) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols)
@@ -416,6 +507,23 @@ CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t 
   return m;
 }
 
+// 2-D map over the output C [M rows, N inner] for the epilogue's TMA stores: 32 x 32
+// boxes, 64 B (bf16, SWIZZLE_64B) or 128 B (fp32, SWIZZLE_128B) rows.  Returns false
+// when C is not TMA-aligned (the epilogue then stores from registers).
+bool make_c_map(CUtensorMap* m, void* c, uint64_t ldc, int M, int N, bool bf16) {
+  const uint64_t esz = bf16 ? 2 : 4;
+  if (reinterpret_cast<uintptr_t>(c) % 16 || (ldc * esz) % 16) return false;
+  const cuuint64_t dims[2] = {uint64_t(N), uint64_t(M)};
+  const cuuint64_t strides[1] = {ldc * esz};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encoder()(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, c,
+                               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 int gemm_grid(int ntiles, int max_sms) {
   static int nsm = [] {
     int dev = 0, n = 0;
@@ -443,7 +551,10 @@ GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint6
   g.ma = a_mn ? make_map(a, uint64_t(M), uint64_t(K), lda, 64) : make_map(a, uint64_t(K), uint64_t(M), lda, kBM);
   g.mb = b_mn ? make_map(b, uint64_t(N), uint64_t(K), ldb, 64)
               : make_map(b, uint64_t(K), uint64_t(N), ldb, kBN / kCluster);  // each CTA loads its 128 B rows
-  GemmParams P{c, ldc, M, N, K, c_t == MICS_BF16, accumulate != 0, a_mn != 0, b_mn != 0};
+  const char* te = std::getenv("MICS_GEMM_TMA_STORE");  // 0: register stores (A/B runs)
+  const bool tma_store = !(te && te[0] == '0') && make_c_map(&g.mc, c, ldc, M, N, c_t == MICS_BF16);
+  if (!tma_store) g.mc = g.ma;  // unused placeholder
+  GemmParams P{c, ldc, M, N, K, c_t == MICS_BF16, accumulate != 0, a_mn != 0, b_mn != 0, nullptr, tma_store};
   static_assert(sizeof(GemmParams) <= sizeof(g.params), "GemmParams fits");
   memcpy(g.params, &P, sizeof(P));
   g.ntiles = ((M + kCluster * kBM - 1) / (kCluster * kBM)) * ((N + kBN - 1) / kBN);  // 256 x 256 pair tiles
@@ -455,6 +566,17 @@ GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint6
 void launch_gemm(cudaStream_t s, const GemmLaunch& g) {
   GemmParams P;
   memcpy(&P, g.params, sizeof(P));
+  // MICS_GEMM_PROBE=1 (debugging, synchronous): per-role stall cycles of this launch
+  static const bool probe = [] {
+    const char* e = std::getenv("MICS_GEMM_PROBE");
+    return e && e[0] == '1';
+  }();
+  static unsigned long long* d_probe = nullptr;
+  if (probe) {
+    if (!d_probe) MICS_CUDA(cudaMalloc(&d_probe, 1024 * 8 * sizeof(unsigned long long)));
+    MICS_CUDA(cudaMemsetAsync(d_probe, 0, 1024 * 8 * sizeof(unsigned long long), s));
+    P.probe = d_probe;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(g.grid));
   cfg.blockDim = dim3(kGemmThreads);
@@ -467,7 +589,23 @@ void launch_gemm(cudaStream_t s, const GemmLaunch& g) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm, g.ma, g.mb, P));
+  MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm, g.ma, g.mb, g.mc, P));
+  if (probe) {
+    std::vector<unsigned long long> h(size_t(g.grid) * 8);
+    MICS_CUDA(cudaMemcpyAsync(h.data(), d_probe, h.size() * 8, cudaMemcpyDeviceToHost, s));
+    MICS_CUDA(cudaStreamSynchronize(s));
+    double a[8] = {};
+    int nl = 0;
+    for (int b = 0; b < g.grid; ++b) {
+      for (int k = 0; k < 8; ++k) a[k] += double(h[size_t(b) * 8 + k]);
+      nl += (b % 2 == 0);
+    }
+    std::fprintf(stderr,
+                 "[gemm probe] M=%d N=%d K=%d grid=%d tiles=%d: total %.0f cyc/CTA; MMA wait tmem_empty %.0f, "
+                 "full %.0f (leaders); producer wait empty %.0f; epilogue busy %.0f, wait tmem_full %.0f\n",
+                 P.M, P.N, P.K, g.grid, g.ntiles, a[4] / g.grid, a[0] / nl, a[1] / nl, a[2] / g.grid, a[3] / g.grid,
+                 a[5] / g.grid);
+  }
 }
 
 }  // namespace mics

@@ -166,7 +166,7 @@ void launch_boundary(cudaStream_t s, const BndJob* jobs, int njobs, uint32_t rs_
 // K7 tcgen05 GEMM (gemm.cu): C[M,N] (+)= A[M,K]·B[K,N], bf16 operands K- or MN-major,
 // fp32 accumulation; planned once (TMA descriptors encoded), launched many times.
 struct GemmLaunch {
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   alignas(8) unsigned char params[64];
   int ntiles = 0, grid = 1;
   double flops = 0;
