@@ -326,6 +326,106 @@ def nccl_step(wl, rank, world, steps, warmup):
                     "groups + torch.optim.Adam(fused=True), same shapes"}
 
 
+def nccl_compute_step(wl, rank, world, steps, warmup):
+    """Comparator for the step with compute, one rank per GPU: the same model and
+    schedule on the stock stack — torch.matmul (cuBLAS) for the layer GEMMs, NCCL
+    all_gather_into_tensor on a side stream one layer ahead (prefetch), NCCL
+    reduce_scatter_tensor per micro-step, all_reduce at the boundary, fused Adam.
+    Timing only (random data).  Like the K7 path it pads every layer's row count to
+    a multiple of 8: cuBLAS on the unpadded, 2-byte-misaligned shapes (12301 rows)
+    ran at 130-160 TF/s (tools/probe_stock.py)."""
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device())
+    p, s, n, T, h = wl.p, wl.s, world, wl.tokens, wl.hidden
+    pg = {g: dist.new_group(list(range(g * p, (g + 1) * p))) for g in range(n // p)}
+    rg = {j: dist.new_group(list(range(j, n, p))) for j in range(p)}
+    my_pg, my_rg = pg[rank // p], rg[rank % p]
+    ldy = [(e // h + 7) // 8 * 8 for e in wl.layer_params]
+    # per layer: a gradient region of R_l (>= the padded dW, divisible by p) and a shard of R_l / p
+    R = [(max(((e + p - 1) // p + 7) // 8 * 8 * p, r * h) + p - 1) // p * p for e, r in zip(wl.layer_params, ldy)]
+    offs, goffs = [0], [0]
+    for r_ in R:
+        offs.append(offs[-1] + r_ // p)
+        goffs.append(goffs[-1] + r_)
+    S, G = offs[-1], goffs[-1]
+    gdt = torch.bfloat16 if wl.grad_dtype == "bf16" else torch.float32
+    shard = (torch.randn(S, device=dev) * 0.02).to(torch.bfloat16)
+    gathered = [torch.zeros(max(R), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    X = [torch.randn(T, h, device=dev).to(torch.bfloat16) for _ in range(s)]
+    Y = [torch.empty(T, r, dtype=torch.bfloat16, device=dev) for r in ldy]
+    dX = torch.zeros(T, h, dtype=torch.float32, device=dev)
+    grads = [torch.zeros(G, dtype=gdt, device=dev) for _ in range(2)]
+    acc = torch.zeros(S, dtype=torch.float32, device=dev)
+    tmp = torch.empty(S, dtype=gdt, device=dev)
+    master = torch.nn.Parameter(shard.float())
+    opt = torch.optim.Adam([master], lr=1e-4, fused=True)
+    side = torch.cuda.Stream()
+    ev_g = [torch.cuda.Event() for _ in range(2)]
+    ev_free = [torch.cuda.Event() for _ in range(2)]
+    main = torch.cuda.current_stream()
+    L = len(ldy)
+
+    def gather(l):
+        b = l % 2
+        with torch.cuda.stream(side):
+            side.wait_event(ev_free[b])
+            dist.all_gather_into_tensor(gathered[b][:R[l]], shard[offs[l]:offs[l + 1]], group=my_pg)
+            ev_g[b].record(side)
+
+    def W(l):
+        return gathered[l % 2][:ldy[l] * h].view(ldy[l], h)
+
+    def one():
+        for t in range(s):
+            g = grads[t % 2]
+            gather(0)
+            for l in range(L):  # forward, prefetching layer l+1
+                if l + 1 < L:
+                    gather(l + 1)
+                main.wait_event(ev_g[l % 2])
+                torch.matmul(X[t], W(l).t(), out=Y[l])
+                ev_free[l % 2].record(main)
+            gather(L - 1)
+            for l in range(L - 1, -1, -1):  # backward
+                if l > 0:
+                    gather(l - 1)
+                main.wait_event(ev_g[l % 2])
+                Wl = W(l)
+                if l == L - 1:  # bf16 cuBLAS products, accumulated / stored in the step's dtypes
+                    dX.copy_(torch.matmul(Y[l], Wl))
+                else:
+                    dX.add_(torch.matmul(Y[l], Wl))
+                dW = g[goffs[l]:goffs[l] + ldy[l] * h].view(ldy[l], h)
+                if gdt == torch.bfloat16:
+                    torch.matmul(Y[l].t(), X[t], out=dW)
+                else:
+                    dW.copy_(torch.matmul(Y[l].t(), X[t]))
+                ev_free[l % 2].record(main)
+            dist.reduce_scatter_tensor(tmp, g, group=my_pg)
+            acc.add_(tmp.float()) if t else acc.copy_(tmp.float())
+        if n // p > 1:
+            dist.all_reduce(acc, group=my_rg)
+        master.grad = acc
+        opt.step()
+        shard.copy_(master.detach().to(torch.bfloat16))
+
+    for _ in range(warmup):
+        one()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        one()
+    e1.record()
+    e1.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    return {"value": n * MICRO_BATCH * s / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
+            "what": "same model and schedule on torch.matmul (cuBLAS, rows padded to 8) + NCCL all_gather (side "
+                    "stream, one layer ahead) / reduce_scatter / all_reduce + torch.optim.Adam(fused=True)"}
+
+
 # ----------------------------------------------------------------------------- step with compute
 def measure_compute(args, wl, rank, world, local):
     """The MiCS step with its layer GEMMs (tcgen05, K7): gradients come from the GEMMs,
@@ -421,6 +521,11 @@ def measure_compute(args, wl, rank, world, local):
         host_free(rptr)
     step.close()
     eng.close()
+    if world > 1 and per == 1:
+        try:
+            out["nccl_cublas_comparator"] = nccl_compute_step(wl, rank, world, max(2, args.compute_steps), 1)
+        except Exception as e:  # noqa: BLE001
+            out["nccl_cublas_comparator"] = {"error": str(e)[:200]}
     return out
 
 
@@ -613,6 +718,7 @@ def run_compute_headline(args, wl, rank, world, local):
                        "l2": "inputs larger than L2", "launch": "CUDA graph replay (gathers / GEMMs / sync streams)"},
             "roofline": c["roofline"], "e2e": c.get("e2e"), "gpu_launches": c["gpu_launches"],
             "clocks": c["clocks"], "cpu_baseline": cpu,
+            "nccl_cublas_comparator": c.get("nccl_cublas_comparator"),
             "detail": {k: c[k] for k in ("model", "tflop_per_step_per_gpu", "achieved_tflops_per_gpu",
                                          "serialised_phases_ms", "serialised_ms", "overlap")}}
     if rank == 0:
