@@ -51,6 +51,13 @@ void release(mics_step* st) {
     if (e) cudaEventDestroy(e);
   for (auto e : st->ev_bnd) cudaEventDestroy(e);
   if (st->gexec) cudaGraphExecDestroy(st->gexec);
+  for (auto& l : st->tail_rs) l.release();
+  for (auto& b : st->tail_bnd) {
+    b.rs.release();
+    b.ag.release();
+  }
+  for (auto e : st->ev_tail) cudaEventDestroy(e);
+  if (st->ev_tail_done) cudaEventDestroy(st->ev_tail_done);
   for (auto e : st->ev_h2d) cudaEventDestroy(e);
   for (auto e : st->ev_rs_slot) cudaEventDestroy(e);
   if (st->ev_begin) cudaEventDestroy(st->ev_begin);
@@ -183,6 +190,71 @@ void enqueue_boundary(mics_step* st, bool side) {
     if (side) MICS_CUDA(cudaEventRecord(st->ev_bnd[g], s));
   }
   if (side) MICS_CUDA(cudaEventRecord(st->ev_done[b], s));
+}
+
+// Up to 4 layer groups of about equal shard size, in forward order: layer l joins
+// the group its shard midpoint falls in (empty groups vanish).
+void plan_layer_groups(mics_step* st) {
+  if (!st->group_range.empty()) return;
+  mics_sync* sy = st->sync;
+  const int L = st->cfg.nlayers;
+  const uint64_t G = uint64_t(std::min(4, L)), S = sy->shard_elems;
+  int prev = -1;
+  for (int l = 0; l < L; ++l) {
+    const uint64_t mid = sy->shard_off[size_t(l)] + sy->chunk[size_t(l)] / 2;
+    const int g = int(std::min(G - 1, mid * G / std::max<uint64_t>(S, 1)));
+    if (g != prev) {
+      st->group_first_layer.push_back(l);
+      st->group_range.push_back({sy->shard_off[size_t(l)], 0});
+      prev = g;
+    }
+    st->group_range.back().second = sy->shard_off[size_t(l)] + sy->chunk[size_t(l)];
+  }
+}
+
+// The overlapped tail: the last micro-step's reduce-scatter group by group on the main
+// stream (channel 0); once group g is reduced, its boundary reduce-scatter + Adam run on
+// the side stream (channel 1) while the main stream reduces group g+1.  Same fold order
+// and Adam as the in-order boundary (build_boundary_range), so the bits are identical.
+// clk (profile): everything in order on the main stream, events around each launch
+// (even entries: reduce-scatter, odd: boundary).
+void enqueue_tail(mics_step* st, std::vector<cudaEvent_t>* clk) {
+  mics_ctx* ctx = st->ctx;
+  const bool serial = clk != nullptr;
+  cudaStream_t M = ctx->stream, S = serial ? M : ctx->side_stream;
+  st->adam_step++;
+  const AdamScalars sc = make_adam_scalars(st->cfg.lr, st->cfg.beta1, st->cfg.beta2, st->cfg.eps,
+                                           st->cfg.weight_decay, st->adam_step, st->adam.grad_scale);
+  if (st->d_scalars && !st->capturing) {
+    DevScalars v{};
+    v.sc = sc;
+    launch_set_scalars(M, st->d_scalars, v);
+  }
+  auto mark = [&]() {
+    if (!clk) return;
+    cudaEvent_t e;
+    MICS_CUDA(cudaEventCreate(&e));
+    MICS_CUDA(cudaEventRecord(e, M));
+    clk->push_back(e);
+  };
+  mark();
+  for (size_t g = 0; g < st->tail_rs.size(); ++g) {
+    enqueue(ctx, st->tail_rs[g], -1, M);
+    mark();
+    if (!serial) {
+      MICS_CUDA(cudaEventRecord(st->ev_tail[g], M));
+      MICS_CUDA(cudaStreamWaitEvent(S, st->ev_tail[g], 0));
+    }
+    BoundaryLaunches& b = st->tail_bnd[g];
+    if (b.has_rs) enqueue(ctx, b.rs, -1, S);
+    b.ag.adam = sc;
+    enqueue(ctx, b.ag, -1, S);
+    mark();
+  }
+  if (!serial) {
+    MICS_CUDA(cudaEventRecord(st->ev_tail_done, S));
+    MICS_CUDA(cudaStreamWaitEvent(M, st->ev_tail_done, 0));
+  }
 }
 
 // forward then backward per-layer gathers.  The first gather of a window follows
@@ -597,20 +669,7 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
                                                  t == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE, true, false, 1, 1,
                                                  &st->gacc1)});
       }
-      // up to 4 layer groups of about equal shard size, in forward order: layer l
-      // joins the group its shard midpoint falls in (empty groups vanish)
-      const uint64_t G = uint64_t(std::min(4, cfg->nlayers));
-      int prev = -1;
-      for (int l = 0; l < cfg->nlayers; ++l) {
-        const uint64_t mid = sy->shard_off[size_t(l)] + sy->chunk[size_t(l)] / 2;
-        const int g = int(std::min(G - 1, mid * G / std::max<uint64_t>(S, 1)));
-        if (g != prev) {
-          st->group_first_layer.push_back(l);
-          st->group_range.push_back({sy->shard_off[size_t(l)], 0});
-          prev = g;
-        }
-        st->group_range.back().second = sy->shard_off[size_t(l)] + sy->chunk[size_t(l)];
-      }
+      plan_layer_groups(st);
       for (const auto& [lo, hi] : st->group_range) {
         st->bndg[0].push_back(build_boundary_range(sy, &st->adam, sy->shard, lo, hi, 1));
         st->bndg[1].push_back(build_boundary_range(sy, &st->adam, st->gacc1, lo, hi, 1));
@@ -621,6 +680,28 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
       for (auto& e : st->ev_bnd) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     } else if (!cfg->alternative) {
       st->bnd = build_boundary(sy, &st->adam, true, false);
+      // overlapped tail: worth it when the micro-step reduce-scatter stays inside a GPU
+      // (HBM) and the boundary crosses GPUs (NVLink); MICS_TAIL_OVERLAP=0/1 forces it
+      const char* te = std::getenv("MICS_TAIL_OVERLAP");
+      const bool auto_on = ctx->world > 1 && ctx->per >= cfg->p && sy->n / sy->p > 1;
+      st->tail = !st->compute && sy->n / sy->p > 1 && (te ? te[0] == '1' : auto_on);
+      if (st->tail) {
+        plan_layer_groups(st);
+        const int s_last = cfg->s - 1;
+        const uint64_t goff = uint64_t(s_last % st->gslots) * sy->grad_elems * szg;
+        for (size_t g = 0; g < st->group_range.size(); ++g) {
+          const int l0 = st->group_first_layer[g];
+          const int l1 = g + 1 < st->group_first_layer.size() ? st->group_first_layer[g + 1] : cfg->nlayers;
+          st->tail_rs.push_back(build_micro_launch(sy, st->grads, goff, cfg->grad_t, 1.0,
+                                                   s_last == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE, true, false,
+                                                   1, 1, nullptr, l0, l1));
+          st->tail_bnd.push_back(
+              build_boundary_range(sy, &st->adam, sy->shard, st->group_range[g].first, st->group_range[g].second, 1));
+        }
+        st->ev_tail.resize(st->group_range.size());
+        for (auto& e : st->ev_tail) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        MICS_CUDA(cudaEventCreateWithFlags(&st->ev_tail_done, cudaEventDisableTiming));
+      }
     } else {  // shards already hold the global sum: the boundary is Adam on the own shard
       AdamPlan ap;
       uint64_t pmask = 0;
@@ -666,15 +747,24 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
         S2.ag_remote_bytes += 2 * uint64_t(cfg->s) * x.remote_bytes;
         S2.ag_hbm_bytes += 2 * uint64_t(cfg->s) * x.hbm_bytes;
       }
-    for (auto& v : st->micro)
-      for (auto& x : v) {
+    for (size_t t = 0; t < st->micro.size(); ++t) {
+      if (st->tail && t + 1 == st->micro.size()) continue;  // replaced by the per-group tail launches
+      for (auto& x : st->micro[t]) {
         S2.rs_launches += runs(x);
         S2.rs_remote_bytes += x.remote_bytes;
         S2.rs_hbm_bytes += x.hbm_bytes;
       }
+    }
+    for (auto& x : st->tail_rs) {
+      S2.rs_launches += runs(x);
+      S2.rs_remote_bytes += x.remote_bytes;
+      S2.rs_hbm_bytes += x.hbm_bytes;
+    }
     std::vector<const BoundaryLaunches*> bl;
     if (st->pipelined)
       for (const auto& x : st->bndg[0]) bl.push_back(&x);
+    else if (st->tail)
+      for (const auto& x : st->tail_bnd) bl.push_back(&x);
     else
       bl.push_back(&st->bnd);
     for (const BoundaryLaunches* b : bl)
@@ -732,6 +822,7 @@ void build_graph(mics_step* st) {
   st->graph_tried = true;
   MICS_CUDA(cudaMalloc(&st->d_scalars, sizeof(DevScalars)));
   st->bnd.rs.dyn = st->bnd.ag.dyn = st->d_scalars;
+  for (auto& b : st->tail_bnd) b.ag.dyn = st->d_scalars;
   const int adam_step0 = st->adam_step;
   const uint64_t epoch0 = st->sync->epoch, launches0 = ctx->launches;
   cudaGraph_t g = nullptr;
@@ -743,9 +834,14 @@ void build_graph(mics_step* st) {
     } else {
       for (int t = 0; t < st->cfg.s; ++t) {
         if (generated(st)) enqueue_generate(st, t);
-        enqueue_micro(st, t, false);
+        if (st->tail && t == st->cfg.s - 1) {
+          enqueue_gathers(st, t, false);
+          enqueue_tail(st, nullptr);
+        } else {
+          enqueue_micro(st, t, false);
+        }
       }
-      enqueue_boundary(st, false);
+      if (!st->tail) enqueue_boundary(st, false);
     }
   } catch (...) {
     st->capturing = false;
@@ -807,9 +903,14 @@ void step_run(mics_step* st, int iters) {
     }
     for (int t = 0; t < st->cfg.s; ++t) {
       if (generated(st)) enqueue_generate(st, t);
-      enqueue_micro(st, t, true);
+      if (st->tail && t == st->cfg.s - 1) {
+        enqueue_gathers(st, t, true);
+        enqueue_tail(st, nullptr);
+      } else {
+        enqueue_micro(st, t, true);
+      }
     }
-    enqueue_boundary(st, true);
+    if (!st->tail) enqueue_boundary(st, true);
     st->step_idx++;
   }
   join_side(st);
@@ -846,11 +947,15 @@ void step_profile(mics_step* st, double* ms) {
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
     enqueue_gathers(st, t, false);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
-    enqueue_sync(st, t, false);
+    if (!(st->tail && t == s - 1)) enqueue_sync(st, t, false);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
   }
   MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
-  enqueue_boundary(st, false);
+  std::vector<cudaEvent_t> tclk;  // overlapped tail, serialised: RS / boundary per layer group
+  if (st->tail)
+    enqueue_tail(st, &tclk);
+  else
+    enqueue_boundary(st, false);
   st->step_idx++;
   MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
   MICS_CUDA(cudaEventSynchronize(ev[size_t(k - 1)]));
@@ -865,6 +970,14 @@ void step_profile(mics_step* st, double* ms) {
   }
   MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * s)], ev[size_t(4 * s + 1)]));
   b = x;
+  if (st->tail) {
+    b = 0;
+    for (size_t i = 1; i < tclk.size(); ++i) {
+      MICS_CUDA(cudaEventElapsedTime(&x, tclk[i - 1], tclk[i]));
+      (i % 2 ? r : b) += x;
+    }
+    for (auto e : tclk) cudaEventDestroy(e);
+  }
   for (auto& e : ev) cudaEventDestroy(e);
   ms[0] = a;
   ms[1] = r;
@@ -938,11 +1051,14 @@ void step_run_host(mics_step* st, const void* host_grads, int iters, void* host_
       const int k = t % nslot;
       enqueue_gathers(st, t, true);  // parameters only: overlaps the copies
       MICS_CUDA(cudaStreamWaitEvent(ctx->stream, st->ev_h2d[size_t(k)], 0));
-      enqueue_sync(st, t, true);
+      if (st->tail && t == s - 1)
+        enqueue_tail(st, nullptr);  // last reduce-scatter + boundary, overlapped per layer group
+      else
+        enqueue_sync(st, t, true);
       MICS_CUDA(cudaEventRecord(st->ev_rs_slot[size_t(k)], ctx->stream));
       if (nslot != s && t + 1 < s) copy_in(t + 1);
     }
-    enqueue_boundary(st, true);
+    if (!st->tail) enqueue_boundary(st, true);
     st->step_idx++;
     if (host_result) {
       join_side(st);

@@ -84,7 +84,9 @@ mics_sync* sync_create(mics_ctx* ctx, int p, int s, int nseg, const uint64_t* se
 
 // ---- micro-step: one reduce launch over all partition groups and segments
 Launch build_micro_launch(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode,
-                          bool persistent, bool record, int entry, int exit, const mics_buf* shard_override) {
+                          bool persistent, bool record, int entry, int exit, const mics_buf* shard_override,
+                          int seg_lo, int seg_hi) {
+  if (seg_hi < 0) seg_hi = st->nseg;  // segments [seg_lo, seg_hi) (a layer group of the step driver)
   mics_ctx* ctx = st->ctx;
   const int p = st->p;
   const mics_buf shard = shard_override ? *shard_override : st->shard;
@@ -97,13 +99,13 @@ Launch build_micro_launch(mics_sync* st, mics_buf grads, uint64_t goff, mics_dty
       for (int i = 0; i < p; ++i)
         for (int j = 0; j < p; ++j)
           if (i != j)
-            for (int q = 0; q < st->nseg; ++q) ctx->record(g * p + i, g * p + j, st->chunk[size_t(q)] * szg);
+            for (int q = seg_lo; q < seg_hi; ++q) ctx->record(g * p + i, g * p + j, st->chunk[size_t(q)] * szg);
     }
     mask |= ctx->peer_mask(ranks.data(), p);
     for (int j = 0; j < p; ++j) {
       const int rank = g * p + j;
       if (!ctx->local(rank)) continue;
-      for (int q = 0; q < st->nseg; ++q) {
+      for (int q = seg_lo; q < seg_hi; ++q) {
         const uint64_t c = st->chunk[size_t(q)], first = uint64_t(j) * c;
         std::vector<const void*> srcs(static_cast<size_t>(p));
         for (int i = 0; i < p; ++i)

@@ -41,7 +41,7 @@ mics_sync* sync_create(mics_ctx* ctx, int p, int s, int nseg, const uint64_t* se
                        uint32_t align);
 Launch build_micro_launch(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode,
                           bool persistent, bool record, int entry, int exit,
-                          const mics_buf* shard_override = nullptr);
+                          const mics_buf* shard_override = nullptr, int seg_lo = 0, int seg_hi = -1);
 BoundaryLaunches build_boundary(mics_sync* st, const mics_adam* adam, bool persistent, bool record);
 BoundaryLaunches build_boundary_range(mics_sync* st, const mics_adam* adam, mics_buf shard, uint64_t lo, uint64_t hi,
                                       int chan);
@@ -85,6 +85,15 @@ struct mics_step {
   cudaEvent_t ev_rs = nullptr, ev_done[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_bnd;
   uint64_t step_idx = 0;
+  // Overlapped tail (2-hop, partition groups inside a GPU, replication groups across
+  // GPUs — N=2/4 of the 8-rank job): the last micro-step's reduce-scatter (HBM) runs
+  // per layer group on the main stream (channel 0) while each finished group's
+  // boundary all-reduce + Adam (NVLink) runs on the side stream (channel 1).
+  bool tail = false;
+  std::vector<mics::Launch> tail_rs;
+  std::vector<mics::BoundaryLaunches> tail_bnd;
+  std::vector<cudaEvent_t> ev_tail;
+  cudaEvent_t ev_tail_done = nullptr;
   // CUDA-graph replay (default; MICS_GRAPH=0 enqueues every kernel per step):
   // one captured step whose boundary kernels read the per-step Adam scalars and
   // flag epoch from d_scalars, set by one small kernel before each replay.

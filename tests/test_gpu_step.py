@@ -209,3 +209,43 @@ def test_run_host_matches_device_resident(resident):
     host_free(hptr)
     host_free(rptr)
     eng.close()
+
+
+@pytest.mark.parametrize("graph", ["1", "0"])
+def test_overlapped_tail_matches_in_order(monkeypatch, graph):
+    """Overlapped tail (last reduce-scatter per layer group on the main stream, each
+    group's boundary all-reduce + Adam on the side stream): same bits as the in-order
+    step over several steps, with a profiled (serialised) step and a host-input step
+    in between."""
+    from paper_2205_00119_b200.engine import Engine, host_alloc, host_free
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
+    monkeypatch.setenv("MICS_GRAPH", graph)
+    wl = Workload("tail", [70_000, 12_345, 40_000, 9_999, 33_333, 4_096], p=2, s=3)
+    res = {}
+    for tail in ("0", "1"):
+        monkeypatch.setenv("MICS_TAIL_OVERLAP", tail)
+        eng = Engine(n_ranks=8, device=0, arena_bytes=256 << 20)
+        step = MicsStep(eng, wl, StepOptions(seed=13, lr=1e-3, weight_decay=0.01))
+        G = step.stats().grad_elems
+        host, hptr = host_alloc(G * 4)
+        host[:] = np.random.default_rng(1).uniform(-1, 1, G).astype(np.float32).view(np.uint8)
+        step.run(2)
+        prof = step.profile()
+        step.run_host(hptr, 1)
+        step.run(1)
+        eng.synchronize()
+        assert prof["boundary_ms"] > 0 and prof["reducescatter_ms"] > 0
+        S = step.sync_info()[0].shard_elems
+        b = step.buffers()
+        res[tail] = [eng.d2h(b[k], r, S) for k in ("master", "exp_avg", "exp_avg_sq") for r in range(8)]
+        st = step.stats()
+        res[tail + "launch"] = (st.rs_launches, st.bnd_launches, st.rs_hbm_bytes + st.rs_remote_bytes,
+                                st.bnd_hbm_bytes + st.bnd_remote_bytes)
+        step.close()
+        host_free(hptr)
+        eng.close()
+    for x, y in zip(res["0"], res["1"]):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    # same reduce-scatter bytes; the tail splits the last reduce-scatter and the boundary per layer group
+    assert res["1launch"][2] == res["0launch"][2]
+    assert res["1launch"][0] > res["0launch"][0] and res["1launch"][1] > res["0launch"][1]
