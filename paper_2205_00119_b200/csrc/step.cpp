@@ -340,6 +340,11 @@ void setup_compute(mics_step* st) {
   //    SM).  37.0 ms/step (k_copy, shared) -> 36.2 (copy engines) -> 35.0 (+16 SMs).
   st->comm_sms = 16;
   if (const char* e = std::getenv("MICS_COMM_SMS")) st->comm_sms = std::max(0, std::min(ctx->nsm - 2, std::atoi(e)));
+  {
+    const char* e = std::getenv("MICS_RS_OVERLAP");
+    st->rs_overlap = !(e && e[0] == '0');
+    if (!st->rs_overlap) st->comm_sms = 0;  // nothing runs beside the GEMMs but copy-engine gathers
+  }
   const int gemm_sms = st->comm_sms ? ctx->nsm - st->comm_sms : 0;
   const int T = int(st->T), h = int(st->h);
   for (int t = 0; t < s; ++t)
@@ -551,18 +556,20 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
     rec(st->ev_wg[size_t(slot)], C);
     wait(M, st->ev_wg[size_t(slot)]);
     if (tr) tr->begin(M, "rs", t, -1);
+    const bool rs_under_compute = st->rs_overlap && t != s - 1;
     size_t mi = 0;
     for (int k = 0; k < t; ++k) mi += st->micro[size_t(k)].size();
     for (auto& x : st->micro[size_t(t)]) {
       Launch y = x;
       // the last micro-step's reduce-scatter overlaps no compute: full grid
-      if (serial || t == s - 1) y.grid = st->micro_grid_full[mi];
+      if (serial || !rs_under_compute) y.grid = st->micro_grid_full[mi];
       ++mi;
       enqueue(ctx, y, -1, M);
     }
     if (tr) tr->end(M);
     if (clk) clk->mark(PH_RS);
     rec(st->ev_rsd[size_t(slot)], M);
+    if (!st->rs_overlap) wait(C, st->ev_rsd[size_t(slot)]);  // next micro-step's GEMMs after the RS
   }
   if (tr) tr->begin(M, "boundary", s, -1);
   enqueue_boundary(st, false);

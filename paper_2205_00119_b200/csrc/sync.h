@@ -116,6 +116,7 @@ struct mics_step {
   mics_buf x{}, y{}, dx{};
   int gslots = 1;                                    // gradient slots (micro-step t -> t % gslots)
   int comm_sms = 0;                                  // SMs left to the overlapped collectives (GEMMs get the rest)
+  bool rs_overlap = true;                            // micro-step RS under the next micro-step's GEMMs
   std::vector<int> ag_grid_full, micro_grid_full;    // grids of the serialised (profile) step
   // flat gathers of the step with compute (MICS_CE_GATHER, default on): the
   // overlapped per-layer gathers are copy-engine memcpys (no SM time) instead of
