@@ -1,0 +1,73 @@
+"""Full-size parity (BASELINE.json C3: BERT-large-shaped 334,088,192 parameters, n=8,
+p=2, s=4, fp32 gradients) through properties that do not need the whole job on the
+CPU.  The gradients come from the counter-based generator (K6), so the CPU can
+evaluate any element of any rank's gradient directly; for a random sample of shard
+elements it replays the 2-hop folds (reduce-scatter over the partition group per
+micro-step, accumulation over micro-steps, boundary fold over the replication group)
+and Adam, and the device result must match BIT-EXACTLY.  Same for the gathered
+bf16 parameters (all-gather = concatenation of the group's shards)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_c3_full_size_sampled_bitexact(oracle):
+    from paper_2205_00119_b200.engine import Engine
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, workloads
+    import bench
+    wl = workloads()["C3"]
+    n, p, s = wl.n, wl.p, wl.s
+    opts = StepOptions(seed=2205, lr=1e-4)
+    eng = Engine(n_ranks=n, device=0, arena_bytes=bench.arena_bytes(wl, n, True, n))
+    step = MicsStep(eng, wl, opts)
+    info, segs = step.sync_info()
+    S = info.shard_elems
+    assert sum(ln for ln, _, _, _ in segs) == 334_088_192
+    b = step.buffers()
+    step.run(1)
+    eng.synchronize()
+    rng = np.random.default_rng(7)
+    samples = np.sort(rng.choice(S, 400, replace=False))
+    # include both ends and the layer boundaries' neighbourhood
+    samples = np.unique(np.concatenate([samples, [0, S - 1]] + [[so, so + c - 1] for _, c, so, _ in segs]))
+    seg_of = np.searchsorted([so for _, _, so, _ in segs], samples, side="right") - 1
+    seed_m = 2205 ^ 0x5EED
+    for x, q in zip(samples, seg_of):
+        ln, c, so, go = segs[q]
+        e = int(x - so)
+        for r in range(n):
+            j, g = r % p, r // p
+            # expected reduced gradient of element x at replication position j
+            acc_by_member = []
+            for qq in range(n // p):  # replication group members j, j+p, ...
+                gg = qq  # member rank j + qq*p sits in partition group qq at position j
+                acc = np.float32(0)
+                for t in range(s):
+                    gi = go + j * c + e
+                    if j * c + e < ln:
+                        f = oracle.gen_f32(2205, gg * p + 0, t, 0, gi, 1)[0]
+                        for i in range(1, p):
+                            f = np.float32(f + oracle.gen_f32(2205, gg * p + i, t, 0, gi, 1)[0])
+                    else:
+                        f = np.float32(0)
+                    acc = np.float32(acc + f) if t else np.float32(np.float32(0) + f)
+                acc_by_member.append(acc)
+            red = acc_by_member[0]
+            for a in acc_by_member[1:]:
+                red = np.float32(red + a)
+            p0 = oracle.gen_f32(seed_m, j, 0, 255, int(x), 1)
+            wp, _, _, wb = oracle.adam(p0, np.zeros(1), np.zeros(1), np.array([red], np.float32), opts.lr, opts.beta1,
+                                       opts.beta2, opts.eps, opts.weight_decay, 1, 1.0 / (n * s), want_bf16=True)
+            got = eng.d2h(b["master"], r, 1, off=int(x) * 4)
+            assert got.view(np.uint32)[0] == wp.view(np.uint32)[0], (int(x), r)
+            assert eng.d2h(b["param_bf16"], r, 1, "bf16", off=int(x) * 2)[0] == wb[0], (int(x), r)
+    # all-gather: the last gathered layer (layer 0, backward pass) = the group's pre-update bf16 shards
+    ln0, c0, so0, _ = segs[0]
+    for pos_e in rng.choice(p * c0, 200, replace=False):
+        pos, e = divmod(int(pos_e), c0)
+        want = oracle.f32_to_bf16(oracle.gen_f32(seed_m, pos, 0, 255, so0 + e, 1))[0]
+        for r in (0, 5):
+            assert eng.d2h(b["gathered"], r, 1, "bf16", off=int(pos_e) * 2)[0] == want, (r, pos, e)
+    step.close()
+    eng.close()
