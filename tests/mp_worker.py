@@ -165,6 +165,25 @@ def main():
         step.close()
         e2.close()
 
+    # ---- full-size C3 step across processes: sampled elements bit-exact (test_gpu_fullsize)
+    from test_gpu_fullsize import check_sampled
+    import bench
+    from paper_2205_00119_b200.step import workloads
+    wl3 = workloads()["C3"]
+    opts3 = StepOptions(seed=2205, lr=1e-4)
+    e6 = Engine(n_ranks=n, world=world, world_rank=rank, device=local,
+                arena_bytes=bench.arena_bytes(wl3, n // world, True, n))
+    mdist.connect(e6)
+    step = MicsStep(e6, wl3, opts3)
+    step.run(1)
+    e6.synchronize()
+    try:
+        check_sampled(ora, e6, step, wl3, opts3, e6.local_ranks, nsamples=150, seed=rank)
+    except AssertionError as ex:
+        expect(False, f"full-size C3 sampled check: {ex}")
+    step.close()
+    e6.close()
+
     # ---- overlapped tail (auto-on when partition groups stay inside a GPU) vs in order
     res = {}
     for tail in ("0", "1"):

@@ -12,50 +12,39 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def test_c3_full_size_sampled_bitexact(oracle):
-    from paper_2205_00119_b200.engine import Engine
-    from paper_2205_00119_b200.step import MicsStep, StepOptions, workloads
-    import bench
-    wl = workloads()["C3"]
+def check_sampled(oracle, eng, step, wl, opts, ranks, nsamples=400, seed=7):
+    """Bit-exact check of sampled shard elements of `ranks` after one step (see module doc)."""
     n, p, s = wl.n, wl.p, wl.s
-    opts = StepOptions(seed=2205, lr=1e-4)
-    eng = Engine(n_ranks=n, device=0, arena_bytes=bench.arena_bytes(wl, n, True, n))
-    step = MicsStep(eng, wl, opts)
     info, segs = step.sync_info()
     S = info.shard_elems
-    assert sum(ln for ln, _, _, _ in segs) == 334_088_192
     b = step.buffers()
-    step.run(1)
-    eng.synchronize()
-    rng = np.random.default_rng(7)
-    samples = np.sort(rng.choice(S, 400, replace=False))
-    # include both ends and the layer boundaries' neighbourhood
+    rng = np.random.default_rng(seed)
+    samples = np.sort(rng.choice(S, nsamples, replace=False))
+    # include both ends and every layer boundary
     samples = np.unique(np.concatenate([samples, [0, S - 1]] + [[so, so + c - 1] for _, c, so, _ in segs]))
     seg_of = np.searchsorted([so for _, _, so, _ in segs], samples, side="right") - 1
-    seed_m = 2205 ^ 0x5EED
+    seed_m = opts.seed ^ 0x5EED
     for x, q in zip(samples, seg_of):
         ln, c, so, go = segs[q]
         e = int(x - so)
-        for r in range(n):
-            j, g = r % p, r // p
-            # expected reduced gradient of element x at replication position j
-            acc_by_member = []
-            for qq in range(n // p):  # replication group members j, j+p, ...
-                gg = qq  # member rank j + qq*p sits in partition group qq at position j
+        for r in ranks:
+            j = r % p
+            members = []  # accumulated gradient of every replication-group member (j, j+p, ...)
+            for gg in range(n // p):
                 acc = np.float32(0)
                 for t in range(s):
                     gi = go + j * c + e
-                    if j * c + e < ln:
-                        f = oracle.gen_f32(2205, gg * p + 0, t, 0, gi, 1)[0]
+                    if j * c + e < ln:  # partition-group fold, ascending position
+                        f = oracle.gen_f32(opts.seed, gg * p + 0, t, 0, gi, 1)[0]
                         for i in range(1, p):
-                            f = np.float32(f + oracle.gen_f32(2205, gg * p + i, t, 0, gi, 1)[0])
+                            f = np.float32(f + oracle.gen_f32(opts.seed, gg * p + i, t, 0, gi, 1)[0])
                     else:
                         f = np.float32(0)
                     acc = np.float32(acc + f) if t else np.float32(np.float32(0) + f)
-                acc_by_member.append(acc)
-            red = acc_by_member[0]
-            for a in acc_by_member[1:]:
-                red = np.float32(red + a)
+                members.append(acc)
+            red = members[0]
+            for a_ in members[1:]:
+                red = np.float32(red + a_)
             p0 = oracle.gen_f32(seed_m, j, 0, 255, int(x), 1)
             wp, _, _, wb = oracle.adam(p0, np.zeros(1), np.zeros(1), np.array([red], np.float32), opts.lr, opts.beta1,
                                        opts.beta2, opts.eps, opts.weight_decay, 1, 1.0 / (n * s), want_bf16=True)
@@ -67,7 +56,21 @@ def test_c3_full_size_sampled_bitexact(oracle):
     for pos_e in rng.choice(p * c0, 200, replace=False):
         pos, e = divmod(int(pos_e), c0)
         want = oracle.f32_to_bf16(oracle.gen_f32(seed_m, pos, 0, 255, so0 + e, 1))[0]
-        for r in (0, 5):
+        for r in ranks[:2]:
             assert eng.d2h(b["gathered"], r, 1, "bf16", off=int(pos_e) * 2)[0] == want, (r, pos, e)
+
+
+def test_c3_full_size_sampled_bitexact(oracle):
+    from paper_2205_00119_b200.engine import Engine
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, workloads
+    import bench
+    wl = workloads()["C3"]
+    opts = StepOptions(seed=2205, lr=1e-4)
+    eng = Engine(n_ranks=wl.n, device=0, arena_bytes=bench.arena_bytes(wl, wl.n, True, wl.n))
+    step = MicsStep(eng, wl, opts)
+    assert sum(ln for ln, _, _, _ in step.sync_info()[1]) == 334_088_192
+    step.run(1)
+    eng.synchronize()
+    check_sampled(oracle, eng, step, wl, opts, list(range(wl.n)))
     step.close()
     eng.close()
