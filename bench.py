@@ -155,6 +155,8 @@ def arena_bytes(wl, per, resident, n=N_RANKS, alternative=False, compute=None):
         T, h = wl.tokens, wl.hidden
         ldy = [(e // h + 7) // 8 * 8 for e in wl.layer_params]
         per_rank += s * T * h * 2 + T * h * 4 + T * (max(ldy) if compute == "recompute" else sum(ldy)) * 2
+        if per < p:  # partition groups span GPUs: copy-engine staging of the peers' chunks (csrc/step.cpp ce_rs)
+            per_rank += p * S * szg
     if alternative:  # all-n reduce-scatter scratch: n slices of ceil(p*chunk/n) per layer
         per_rank += sum(-(-p * c // n) * n for c in chunks) * 4
     elif os.environ.get("MICS_PIPELINE") == "1":  # pipelined boundary: second gradient accumulator

@@ -65,6 +65,8 @@ void release(mics_step* st) {
     if (e) cudaEventDestroy(e);
   for (auto e : st->ev_wg) cudaEventDestroy(e);
   for (auto e : st->ev_rsd) cudaEventDestroy(e);
+  for (auto e : st->ev_copied) cudaEventDestroy(e);
+  for (auto& l : st->rs_local) l.release();
   if (st->gs) cudaStreamDestroy(st->gs);
   if (st->cs) cudaStreamDestroy(st->cs);
   if (st->copy_stream) cudaStreamDestroy(st->copy_stream);
@@ -345,6 +347,17 @@ void setup_compute(mics_step* st) {
     st->rs_overlap = !(e && e[0] == '0');
     if (!st->rs_overlap) st->comm_sms = 0;  // nothing runs beside the GEMMs but copy-engine gathers
   }
+  {
+    // partition groups that span processes: the reduce-scatter pulls over NVLink, so
+    // stage it through the copy engines instead (see mics_step::ce_rs)
+    bool remote_peers = false;
+    for (int r = 0; r < ctx->n; ++r)
+      if (ctx->local(r))
+        for (int i = 0; i < cfg.p; ++i) remote_peers |= !ctx->local(r / cfg.p * cfg.p + i);
+    const char* e = std::getenv("MICS_CE_RS");
+    st->ce_rs = remote_peers && cfg.s > 1 && !(e && e[0] == '0');
+    if (st->ce_rs) st->comm_sms = 0;  // only a short local fold runs beside the GEMMs
+  }
   const int gemm_sms = st->comm_sms ? ctx->nsm - st->comm_sms : 0;
   const int T = int(st->T), h = int(st->h);
   for (int t = 0; t < s; ++t)
@@ -388,6 +401,70 @@ void setup_compute(mics_step* st) {
       }
       st->ce.push_back(std::move(v));
     }
+  }
+  if (st->ce_rs) {
+    const int p = cfg.p;
+    uint64_t csum = 0;
+    std::vector<uint64_t> cum;
+    for (uint64_t c : sy->chunk) {
+      cum.push_back(csum);
+      csum += c;
+    }
+    st->stage = alloc_sym(ctx, uint64_t(p) * csum * szg);
+    auto stage_ptr = [&](int r, int i, int q) {
+      return ctx->rank_ptr(st->stage, r) + (uint64_t(i) * csum + cum[size_t(q)]) * szg;
+    };
+    for (int slot = 0; slot < st->gslots; ++slot) {
+      const uint64_t goff = uint64_t(slot) * sy->grad_elems * szg;
+      std::vector<std::vector<mics_step::CeCopy>> per_layer(static_cast<size_t>(L));
+      for (int r = 0; r < ctx->n; ++r) {
+        if (!ctx->local(r)) continue;
+        const int g = r / p, j = r % p;
+        for (int i = 0; i < p; ++i) {
+          if (ctx->local(g * p + i)) continue;
+          for (int q = 0; q < L; ++q) {
+            const uint64_t c = sy->chunk[size_t(q)];
+            per_layer[size_t(q)].push_back(
+                {stage_ptr(r, i, q),
+                 ctx->rank_ptr(st->grads, g * p + i) + goff + (sy->grad_off[size_t(q)] + uint64_t(j) * c) * szg,
+                 c * szg});
+          }
+        }
+      }
+      st->ce_rs_copies.push_back(std::move(per_layer));
+    }
+    const uint64_t sza = dtype_size(sy->acc_t);
+    for (int t = 0; t < s; ++t) {
+      const uint64_t goff = uint64_t(t % st->gslots) * sy->grad_elems * szg;
+      RedPlan plan(cfg.grad_t);
+      for (int r = 0; r < ctx->n; ++r) {
+        if (!ctx->local(r)) continue;
+        const int g = r / p, j = r % p;
+        for (int q = 0; q < L; ++q) {
+          const uint64_t c = sy->chunk[size_t(q)], first = uint64_t(j) * c, len = sy->len[size_t(q)];
+          std::vector<const void*> srcs(static_cast<size_t>(p));
+          for (int i = 0; i < p; ++i)  // ascending position, local or staged: the same fold as the pull RS
+            srcs[size_t(i)] = ctx->local(g * p + i)
+                                  ? static_cast<const void*>(ctx->rank_ptr(st->grads, g * p + i) + goff +
+                                                             (sy->grad_off[size_t(q)] + first) * szg)
+                                  : static_cast<const void*>(stage_ptr(r, i, q));
+          plan.add(srcs, ctx->rank_ptr(sy->shard, r) + sy->shard_off[size_t(q)] * sza, c, len > first ? len - first : 0);
+        }
+      }
+      st->rs_local.push_back(make_reduce_launch(ctx, plan, cfg.grad_t, sy->acc_t, 1.0,
+                                                t == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE,
+                                                ctx->barrier(0, 0, 0), true));
+    }
+    uint64_t pmask = 0;
+    for (int g = 0; g < ctx->n / p; ++g) {
+      std::vector<int> ranks(static_cast<size_t>(p));
+      for (int i = 0; i < p; ++i) ranks[size_t(i)] = g * p + i;
+      pmask |= ctx->peer_mask(ranks.data(), p);
+    }
+    st->rs_bar.kind = Launch::BARRIER;
+    st->rs_bar.bar = ctx->barrier(pmask, 1, 0, 2);
+    st->ev_copied.resize(size_t(st->gslots));
+    for (auto& e : st->ev_copied) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   const int lean = st->comm_sms ? st->comm_sms : ctx->nsm;
   for (auto& v : st->ag)
@@ -530,6 +607,7 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
   wait(G, st->ev_fork);
   wait(C, st->ev_fork);
   if (clk) clk->mark(-1);
+  int pending = -1;  // micro-step whose copy-engine-staged reduce-scatter is still to do
   for (int t = 0; t < s; ++t) {
     const int slot = t % st->gslots;
     cur_t = t;
@@ -542,8 +620,24 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
       rec(st->ev_free[l % 2], C);
     }
     if (t >= st->gslots) wait(C, st->ev_rsd[size_t(slot)]);
+    // the copy-engine-staged reduce-scatter of the previous micro-step rides on this
+    // backward pass (gather stream, one layer's chunks after each layer's gather)
+    const bool carry = st->ce_rs && !serial && pending >= 0;
+    const int ps = carry ? pending % st->gslots : 0;
+    if (carry) {
+      MICS_CUDA(cudaStreamWaitEvent(G, st->ev_wg[size_t(ps)], 0));
+      if (pending > 0)  // one staging buffer: the fold of micro-step pending-1 has read it
+        MICS_CUDA(cudaStreamWaitEvent(G, st->ev_rsd[size_t((pending - 1) % st->gslots)], 0));
+      enqueue(ctx, st->rs_bar, -1, G);  // peers' micro-step gradients are complete
+    }
     for (int l = L; l-- > 0;) {
       gather(l);
+      if (carry) {
+        if (tr) tr->begin(G, "rs_copy", pending, l);
+        for (const auto& c : st->ce_rs_copies[size_t(ps)][size_t(l)])
+          MICS_CUDA(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, G));
+        if (tr) tr->end(G);
+      }
       const size_t base = size_t(t * L + l) * size_t(per);
       if (tr) tr->begin(C, "bwd", t, l);
       if (st->recompute) gemms(st->gfwd, base);
@@ -553,7 +647,21 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
       if (clk) clk->mark(PH_GEMM);
       rec(st->ev_free[l % 2], C);
     }
+    if (carry) {
+      enqueue(ctx, st->rs_bar, -1, G);  // finished reading the peers' gradients
+      MICS_CUDA(cudaEventRecord(st->ev_copied[size_t(ps)], G));
+      MICS_CUDA(cudaStreamWaitEvent(M, st->ev_copied[size_t(ps)], 0));
+      if (tr) tr->begin(M, "rs", pending, -1);
+      enqueue(ctx, st->rs_local[size_t(pending)], -1, M);
+      if (tr) tr->end(M);
+      rec(st->ev_rsd[size_t(ps)], M);
+      pending = -1;
+    }
     rec(st->ev_wg[size_t(slot)], C);
+    if (st->ce_rs && !serial && t != s - 1) {
+      pending = t;  // carried by the next micro-step's backward pass
+      continue;
+    }
     wait(M, st->ev_wg[size_t(slot)]);
     if (tr) tr->begin(M, "rs", t, -1);
     const bool rs_under_compute = st->rs_overlap && t != s - 1;
@@ -866,7 +974,7 @@ void build_graph(mics_step* st) {
       MICS_CUDA(cudaEventDestroy(*e));
       MICS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
-    for (auto* v : {&st->ev_wg, &st->ev_rsd})
+    for (auto* v : {&st->ev_wg, &st->ev_rsd, &st->ev_copied})
       for (auto& e : *v) {
         MICS_CUDA(cudaEventDestroy(e));
         MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

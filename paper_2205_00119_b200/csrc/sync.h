@@ -128,6 +128,19 @@ struct mics_step {
     uint64_t bytes;
   };
   std::vector<std::vector<CeCopy>> ce;
+  // Copy-engine-staged reduce-scatter (step with compute, partition groups spanning
+  // GPUs; MICS_CE_RS): the reduce-scatter of micro-step t (t < s-1) is carried by the
+  // backward pass of t+1: on the gather stream, after each layer's gather, the copy
+  // engines pull that layer's chunks of the peers' micro-step-t gradients into local
+  // staging (between two barriers with the partition peers on channel 2), then
+  // rs_local folds local + staged sources (HBM only, same fold order).  The last
+  // micro-step, which overlaps nothing, keeps the SM pull reduce-scatter.
+  bool ce_rs = false;
+  mics_buf stage{};                              // per rank: [p][sum_l c_l] gradient dtype
+  std::vector<std::vector<std::vector<CeCopy>>> ce_rs_copies;  // [slot][layer]
+  std::vector<mics::Launch> rs_local;             // [micro-step]
+  mics::Launch rs_bar{};                          // full barrier with the partition peers, channel 2
+  std::vector<cudaEvent_t> ev_copied;             // [slot]
   std::vector<mics::GemmLaunch> gfwd, gdgrad, gwgrad;  // [(t * L + l) * per + local rank]
   cudaStream_t gs = nullptr, cs = nullptr;
   cudaEvent_t ev_g[2] = {}, ev_free[2] = {}, ev_fork = nullptr, ev_jg = nullptr, ev_jc = nullptr;
