@@ -44,17 +44,23 @@ namespace {
 // rows [128r, 128r+128) of A and columns [128r, 128r+128) of B in its shared memory,
 // the leader issues M=256 N=256 MMAs that read both halves, and each CTA's TMEM
 // receives its 128 rows x 256 columns.  Per SM and k-block: 16 KiB of A + 16 KiB of B.
-constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 6;
+constexpr int kBM = 128, kBK = 64;
 constexpr int kCluster = 2;
-constexpr uint32_t kABytes = kBM * kBK * 2;              // 16 KiB: this CTA's 128 rows of A
-constexpr uint32_t kBHalfBytes = kBN / kCluster * kBK * 2;  // 16 KiB: this CTA's 128 columns of B
-constexpr uint32_t kStageBytes = kABytes + kBHalfBytes;
+constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KiB: this CTA's 128 rows of A
 constexpr int kGemmThreads = 192;
-constexpr uint32_t kTmemCols = 2 * kBN;  // double-buffered accumulator
 // epilogue staging for TMA stores: per epilogue warp two 32 x 32 chunks (fp32 worst case)
 constexpr uint32_t kEpiChunkBytes = 32 * 32 * 4;
 constexpr uint32_t kEpiBytes = 4 * 2 * kEpiChunkBytes;  // 32 KiB
-constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /* align */ + 256 /* barriers */;
+// Tile width N of a CTA pair: 256 (default) or 128 (MICS_GEMM_BN=128; slower, see
+// plan_gemm); the ring keeps ~192 KiB of stages either way.
+template <int BN>
+struct Tile {
+  static constexpr uint32_t kBHalfBytes = BN / kCluster * kBK * 2;  // this CTA's BN/2 columns of B
+  static constexpr uint32_t kStageBytes = kABytes + kBHalfBytes;
+  static constexpr int kStages = int((192u << 10) / kStageBytes);
+  static constexpr uint32_t kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /* align */ + 256 /* barriers */;
+};
 
 struct GemmParams {
   void* c;
@@ -191,10 +197,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// instruction descriptor: fp32 accumulate, bf16 x bf16, M=256 (pair), N=256, majors
+// instruction descriptor: fp32 accumulate, bf16 x bf16, M=256 (pair), N=BN, majors
+template <int BN>
 __device__ __forceinline__ uint32_t idesc_bf16(int a_mn, int b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
-         (uint32_t(kBN >> 3) << 17) | (uint32_t((kCluster * kBM) >> 4) << 24);
+         (uint32_t(BN >> 3) << 17) | (uint32_t((kCluster * kBM) >> 4) << 24);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -229,9 +236,12 @@ __device__ __forceinline__ void mbar_wait_probe(uint32_t bar, uint32_t parity, u
   *acc += static_cast<unsigned long long>(clock64() - t0);
 }
 
+template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
            const __grid_constant__ CUtensorMap tma_c, GemmParams P) {
+  constexpr int kBN = BN, kStages = Tile<BN>::kStages;
+  constexpr uint32_t kStageBytes = Tile<BN>::kStageBytes, kTmemCols = Tile<BN>::kTmemCols;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_smem = smem + kStages * kStageBytes;  // [4 warps][2 buffers][32 x 32 chunk]
@@ -313,7 +323,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && crank == 0) {  // ---------------- MMA issuer (leader CTA only)
-      const uint32_t idesc = idesc_bf16(P.a_mn, P.b_mn);
+      const uint32_t idesc = idesc_bf16<BN>(P.a_mn, P.b_mn);
       // K-major: the 16-element K slice advances 32 B inside the 128 B swizzle row;
       // MN-major: it advances 16 rows of 128 B.  LBO = distance between 64-wide MN blocks.
       const uint32_t a_step = P.a_mn ? 2048u : 32u, b_step = P.b_mn ? 2048u : 32u;
@@ -529,7 +539,10 @@ int gemm_grid(int ntiles, int max_sms) {
     int dev = 0, n = 0;
     MICS_CUDA(cudaGetDevice(&dev));
     MICS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    MICS_CUDA(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
+    MICS_CUDA(cudaFuncSetAttribute(k_gemm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(Tile<256>::kSmemBytes)));
+    MICS_CUDA(cudaFuncSetAttribute(k_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(Tile<128>::kSmemBytes)));
     return n;
   }();
   const int sms = max_sms > 0 && max_sms < nsm ? max_sms : nsm;
@@ -549,15 +562,20 @@ GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint6
   GemmLaunch g;
   // A(m,k): K-major -> [M rows, K inner]; M-major -> [K rows, M inner]
   g.ma = a_mn ? make_map(a, uint64_t(M), uint64_t(K), lda, 64) : make_map(a, uint64_t(K), uint64_t(M), lda, kBM);
+  // tile width 256; MICS_GEMM_BN=128 selects the narrow tile.  Measured (tools/gemm_bench.py)
+  // the narrow tile loses even where it pads far less (N = 1600: 0.588 vs 0.439 ms for
+  // the GPT-2 dgrad): half the MMA work per staged A byte makes it operand-bound.
+  const char* be = std::getenv("MICS_GEMM_BN");
+  g.bn = be && std::atoi(be) == 128 ? 128 : 256;
   g.mb = b_mn ? make_map(b, uint64_t(N), uint64_t(K), ldb, 64)
-              : make_map(b, uint64_t(K), uint64_t(N), ldb, kBN / kCluster);  // each CTA loads its 128 B rows
+              : make_map(b, uint64_t(K), uint64_t(N), ldb, uint32_t(g.bn / kCluster));  // each CTA: BN/2 B rows
   const char* te = std::getenv("MICS_GEMM_TMA_STORE");  // 0: register stores (A/B runs)
   const bool tma_store = !(te && te[0] == '0') && make_c_map(&g.mc, c, ldc, M, N, c_t == MICS_BF16);
   if (!tma_store) g.mc = g.ma;  // unused placeholder
   GemmParams P{c, ldc, M, N, K, c_t == MICS_BF16, accumulate != 0, a_mn != 0, b_mn != 0, nullptr, tma_store};
   static_assert(sizeof(GemmParams) <= sizeof(g.params), "GemmParams fits");
   memcpy(g.params, &P, sizeof(P));
-  g.ntiles = ((M + kCluster * kBM - 1) / (kCluster * kBM)) * ((N + kBN - 1) / kBN);  // 256 x 256 pair tiles
+  g.ntiles = ((M + kCluster * kBM - 1) / (kCluster * kBM)) * ((N + g.bn - 1) / g.bn);  // 256 x BN pair tiles
   g.grid = gemm_grid(g.ntiles, max_sms);
   g.flops = 2.0 * double(M) * double(N) * double(K);
   return g;
@@ -580,7 +598,7 @@ void launch_gemm(cudaStream_t s, const GemmLaunch& g) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(g.grid));
   cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.dynamicSmemBytes = g.bn == 128 ? Tile<128>::kSmemBytes : Tile<256>::kSmemBytes;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -589,7 +607,10 @@ void launch_gemm(cudaStream_t s, const GemmLaunch& g) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm, g.ma, g.mb, g.mc, P));
+  if (g.bn == 128)
+    MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm<128>, g.ma, g.mb, g.mc, P));
+  else
+    MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm<256>, g.ma, g.mb, g.mc, P));
   if (probe) {
     std::vector<unsigned long long> h(size_t(g.grid) * 8);
     MICS_CUDA(cudaMemcpyAsync(h.data(), d_probe, h.size() * 8, cudaMemcpyDeviceToHost, s));

@@ -169,6 +169,7 @@ struct GemmLaunch {
   CUtensorMap ma, mb, mc;
   alignas(8) unsigned char params[64];
   int ntiles = 0, grid = 1;
+  int bn = 256;  // pair tile width (256 or 128)
   double flops = 0;
 };
 GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint64_t ldb, int b_mn, void* c,

@@ -26,6 +26,8 @@ def main():
         ("fwd Y=X.W^T (BERT block)", T, 12301, h, False, False),
         ("dgrad dX=dY.W", T, h, 12301, False, True),
         ("wgrad dW=dY^T.X", 12301, h, T, True, True),
+        ("GPT-2 1.5B dgrad (h=1600)", 8192, 1600, 19213, False, True),
+        ("GPT-2 1.5B wgrad (h=1600)", 19213, 1600, 8192, True, True),
     ]
     pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
@@ -35,7 +37,7 @@ def main():
         ldc = N + 7 & ~7
         a = torch.randn((K if a_mn else M), lda, device="cuda").to(torch.bfloat16)
         b = torch.randn((K if b_mn else N), ldb, device="cuda").to(torch.bfloat16)
-        c = torch.empty(M, ldc, device="cuda", dtype=torch.float32 if name.startswith("wgrad") else torch.bfloat16)
+        c = torch.empty(M, ldc, device="cuda", dtype=torch.float32 if "wgrad" in name else torch.bfloat16)
         out = "f32" if c.dtype == torch.float32 else "bf16"
         torch.cuda.synchronize()
 
