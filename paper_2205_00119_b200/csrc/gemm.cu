@@ -123,6 +123,14 @@ __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* map, uint32_t
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_2sm_mc(const CUtensorMap* map, uint32_t dst, uint32_t bar, int c0, int c1,
+                                                   uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
@@ -236,11 +244,15 @@ __device__ __forceinline__ void mbar_wait_probe(uint32_t bar, uint32_t parity, u
   *acc += static_cast<unsigned long long>(clock64() - t0);
 }
 
-template <int BN>
+// PAIRS = CTA pairs per cluster: 1, or 2 pairs computing vertically adjacent 256-row
+// tiles that share their B tile — each CTA then loads a quarter of its pair's B columns
+// and multicasts it into the CTA with the same pair rank in the other pair.
+template <int BN, int PAIRS>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
            const __grid_constant__ CUtensorMap tma_c, GemmParams P) {
   constexpr int kBN = BN, kStages = Tile<BN>::kStages;
+  constexpr int kCtas = kCluster * PAIRS;
   constexpr uint32_t kStageBytes = Tile<BN>::kStageBytes, kTmemCols = Tile<BN>::kTmemCols;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -251,14 +263,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
   const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int crank = int(cluster_rank());
-  constexpr uint16_t kMask = (1u << kCluster) - 1;
+  const int cl_rank = int(cluster_rank());
+  const int pair = cl_rank / kCluster, crank = cl_rank % kCluster;  // crank: rank inside the pair
+  const uint32_t leader = uint32_t(pair * kCluster);
+  constexpr uint16_t kAllMask = uint16_t((1u << kCtas) - 1);
+  const uint16_t kMask = uint16_t(((1u << kCluster) - 1) << (pair * kCluster));  // this pair
   const long long t_start = P.probe ? clock64() : 0;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full0 + 8 * s, 1);   // leader: its producer's expect_tx (both CTAs' bytes)
-      mbar_init(empty0 + 8 * s, 1);  // the leader's MMA commit, multicast to both CTAs
+      mbar_init(empty0 + 8 * s, PAIRS);  // every leader's MMA commit, multicast to all CTAs
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);                 // the leader's commit, multicast
@@ -282,18 +297,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // work unit = one 256 x 256 tile per pair; CTA `crank` owns rows m0 + 128*crank
   // (possibly past M: zero-filled loads, masked stores) and loads B columns
   // n0 + 128*crank (possibly past N: zero-filled)
-  const int tiles_m = (P.M + kCluster * kBM - 1) / (kCluster * kBM), tiles_n = (P.N + kBN - 1) / kBN;
+  // tile t of a cluster: n-block t / tiles_m, pair `pair` takes 256-row block
+  // (t % tiles_m) * PAIRS + pair
+  const int tiles_m = (P.M + kCluster * kBM * PAIRS - 1) / (kCluster * kBM * PAIRS), tiles_n = (P.N + kBN - 1) / kBN;
   const int ntiles = tiles_m * tiles_n, nk = (P.K + kBK - 1) / kBK;
-  const int cid = blockIdx.x / kCluster, ncl = gridDim.x / kCluster;
+  const int cid = blockIdx.x / kCtas, ncl = gridDim.x / kCtas;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
-      const uint32_t leader_full0 = mapa(full0, 0);
+      const uint32_t leader_full0 = mapa(full0, leader);
+      // multicast loads name the barrier with the pair bit cleared: each destination
+      // CTA's bytes are counted on its own pair leader's barrier (CUTLASS 2SM convention)
+      const uint32_t full_pair0 = full0 & 0xFEFFFFFFu;
+      const uint16_t bmask = uint16_t(((1u << kCtas) - 1) / ((1u << kCluster) - 1)) << crank;  // same crank
       unsigned long long w_empty = 0, *pw = P.probe ? &w_empty : nullptr;
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < ntiles; t += ncl) {
-        const int m0 = ((t % tiles_m) * kCluster + crank) * kBM;
+        const int m0 = (((t % tiles_m) * PAIRS + pair) * kCluster + crank) * kBM;
         const int nb = (t / tiles_m) * kBN + crank * (kBN / kCluster);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait_probe(empty0 + 8 * stage, phase ^ 1, pw);
@@ -307,11 +328,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           } else {
             tma_load_2d_2sm(&tma_a, sa, lfull, k0, m0);
           }
-          if (P.b_mn) {
+          if (PAIRS == 1) {
+            if (P.b_mn) {
 #pragma unroll
-            for (int j = 0; j < kBN / kCluster / 64; ++j) tma_load_2d_2sm(&tma_b, sb + j * 8192, lfull, nb + 64 * j, k0);
-          } else {
-            tma_load_2d_2sm(&tma_b, sb, lfull, k0, nb);
+              for (int j = 0; j < kBN / kCluster / 64; ++j)
+                tma_load_2d_2sm(&tma_b, sb + j * 8192, lfull, nb + 64 * j, k0);
+            } else {
+              tma_load_2d_2sm(&tma_b, sb, lfull, k0, nb);
+            }
+          } else {  // this CTA's share of the pair-half of B, multicast to the same crank of every pair
+            constexpr int kQ = kBN / kCluster / PAIRS;  // columns per share (64 for BN = 256)
+            const uint32_t fb = full_pair0 + 8 * stage;
+            if (P.b_mn) {
+#pragma unroll
+              for (int j = 0; j < kQ / 64; ++j) {
+                const int jj = pair * (kQ / 64) + j;
+                tma_load_2d_2sm_mc(&tma_b, sb + jj * 8192, fb, nb + 64 * jj, k0, bmask);
+              }
+            } else {
+              tma_load_2d_2sm_mc(&tma_b, sb + pair * kQ * 128, fb, k0, nb + pair * kQ, bmask);
+            }
           }
           if (++stage == kStages) {
             stage = 0;
@@ -346,7 +382,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint64_t bd = umma_desc(sb + k * b_step, b_lbo, 1024);
             umma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0);
           }
-          umma_commit_2sm_mc(empty0 + 8 * stage, kMask);  // frees this stage in both CTAs once read
+          umma_commit_2sm_mc(empty0 + 8 * stage, kAllMask);  // frees this stage in every CTA once read
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -366,12 +402,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else {  // ---------------- epilogue: warps 2..5 of both CTAs, TMEM lane quarter = warp % 4
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const uint32_t leader_tempty0 = mapa(tempty0, 0);
+    const uint32_t leader_tempty0 = mapa(tempty0, leader);
     int acc = 0;
     uint32_t acc_phase = 0;
     unsigned long long w_tf = 0, busy = 0, *ptf = (P.probe && warp == 2 && lane == 0) ? &w_tf : nullptr;
     for (int t = cid; t < ntiles; t += ncl) {
-      const int m0 = ((t % tiles_m) * kCluster + crank) * kBM, n0 = (t / tiles_m) * kBN;
+      const int m0 = (((t % tiles_m) * PAIRS + pair) * kCluster + crank) * kBM, n0 = (t / tiles_m) * kBN;
       mbar_wait_probe(tfull0 + 8 * acc, acc_phase, ptf);
       const long long tb0 = ptf ? clock64() : 0;
       fence_after();
@@ -534,20 +570,22 @@ bool make_c_map(CUtensorMap* m, void* c, uint64_t ldc, int M, int N, bool bf16) 
   return r == CUDA_SUCCESS;
 }
 
-int gemm_grid(int ntiles, int max_sms) {
+int gemm_grid(int ntiles, int max_sms, int ctas) {
   static int nsm = [] {
     int dev = 0, n = 0;
     MICS_CUDA(cudaGetDevice(&dev));
     MICS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    MICS_CUDA(cudaFuncSetAttribute(k_gemm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MICS_CUDA(cudaFuncSetAttribute(k_gemm<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(Tile<256>::kSmemBytes)));
-    MICS_CUDA(cudaFuncSetAttribute(k_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MICS_CUDA(cudaFuncSetAttribute(k_gemm<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(Tile<128>::kSmemBytes)));
+    MICS_CUDA(cudaFuncSetAttribute(k_gemm<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(Tile<256>::kSmemBytes)));
     return n;
   }();
   const int sms = max_sms > 0 && max_sms < nsm ? max_sms : nsm;
-  const int pairs = sms / kCluster > 0 ? sms / kCluster : 1;
-  return kCluster * (ntiles < pairs ? ntiles : pairs);
+  const int clusters = sms / ctas > 0 ? sms / ctas : 1;
+  return ctas * (ntiles < clusters ? ntiles : clusters);
 }
 
 }  // namespace
@@ -567,16 +605,23 @@ GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint6
   // the GPT-2 dgrad): half the MMA work per staged A byte makes it operand-bound.
   const char* be = std::getenv("MICS_GEMM_BN");
   g.bn = be && std::atoi(be) == 128 ? 128 : 256;
+  // MICS_GEMM_PAIRS=2: two pairs per cluster share B by multicast.  Correct (tested) but
+  // slower on every shape but one (8192^3: 958 vs 1393 TF/s): the pairs advance in
+  // lockstep on shared stages, and 4-CTA clusters place less evenly on the GPCs.
+  const char* pe0 = std::getenv("MICS_GEMM_PAIRS");
+  const int pairs = g.bn == 256 && pe0 && std::atoi(pe0) == 2 ? 2 : 1;
   g.mb = b_mn ? make_map(b, uint64_t(N), uint64_t(K), ldb, 64)
-              : make_map(b, uint64_t(K), uint64_t(N), ldb, uint32_t(g.bn / kCluster));  // each CTA: BN/2 B rows
+              : make_map(b, uint64_t(K), uint64_t(N), ldb, uint32_t(g.bn / kCluster / pairs));  // rows per load
   const char* te = std::getenv("MICS_GEMM_TMA_STORE");  // 0: register stores (A/B runs)
   const bool tma_store = !(te && te[0] == '0') && make_c_map(&g.mc, c, ldc, M, N, c_t == MICS_BF16);
   if (!tma_store) g.mc = g.ma;  // unused placeholder
   GemmParams P{c, ldc, M, N, K, c_t == MICS_BF16, accumulate != 0, a_mn != 0, b_mn != 0, nullptr, tma_store};
   static_assert(sizeof(GemmParams) <= sizeof(g.params), "GemmParams fits");
   memcpy(g.params, &P, sizeof(P));
-  g.ntiles = ((M + kCluster * kBM - 1) / (kCluster * kBM)) * ((N + g.bn - 1) / g.bn);  // 256 x BN pair tiles
-  g.grid = gemm_grid(g.ntiles, max_sms);
+  g.pairs = pairs;
+  const int rows = kCluster * kBM * g.pairs;
+  g.ntiles = ((M + rows - 1) / rows) * ((N + g.bn - 1) / g.bn);  // (256 * pairs) x BN cluster tiles
+  g.grid = gemm_grid(g.ntiles, max_sms, kCluster * g.pairs);
   g.flops = 2.0 * double(M) * double(N) * double(K);
   return g;
 }
@@ -602,15 +647,17 @@ void launch_gemm(cudaStream_t s, const GemmLaunch& g) {
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kCluster;
+  at[0].val.clusterDim.x = unsigned(kCluster * g.pairs);
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (g.bn == 128)
-    MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm<128>, g.ma, g.mb, g.mc, P));
+    MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm<128, 1>, g.ma, g.mb, g.mc, P));
+  else if (g.pairs == 2)
+    MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm<256, 2>, g.ma, g.mb, g.mc, P));
   else
-    MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm<256>, g.ma, g.mb, g.mc, P));
+    MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm<256, 1>, g.ma, g.mb, g.mc, P));
   if (probe) {
     std::vector<unsigned long long> h(size_t(g.grid) * 8);
     MICS_CUDA(cudaMemcpyAsync(h.data(), d_probe, h.size() * 8, cudaMemcpyDeviceToHost, s));

@@ -170,6 +170,7 @@ struct GemmLaunch {
   alignas(8) unsigned char params[64];
   int ntiles = 0, grid = 1;
   int bn = 256;  // pair tile width (256 or 128)
+  int pairs = 1;  // CTA pairs per cluster (2: B tile multicast across the pairs)
   double flops = 0;
 };
 GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint64_t ldb, int b_mn, void* c,

@@ -109,3 +109,12 @@ def test_gemm_bn128_tiles(eng, monkeypatch, a_mn, b_mn):
 def test_gemm_hidden_1600_accumulate(eng):
     """N = 1600 (GPT-2 1.5B hidden: 6.25 tiles of 256, a ragged last column of tiles); accumulate."""
     run(eng, 512, 1600, 320, False, True, "f32", accumulate=True, seed=6)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (True, True), (False, True)])
+def test_gemm_two_pairs_multicast(eng, monkeypatch, a_mn, b_mn):
+    """Opt-in 4-CTA clusters (MICS_GEMM_PAIRS=2): two CTA pairs share the B tile by TMA
+    multicast (odd number of 256-row blocks included)."""
+    monkeypatch.setenv("MICS_GEMM_PAIRS", "2")
+    run(eng, 700, 600, 200, a_mn, b_mn, "f32", seed=8)
+    run(eng, 1024, 1032, 136, a_mn, b_mn, "bf16", seed=9)
