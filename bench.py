@@ -54,6 +54,8 @@ def parse():
                     help="headline = the step with its layer GEMMs (tcgen05), gathers overlapped with compute")
     ap.add_argument("--no-compute", action="store_true", help="skip the step-with-compute sub-measurement")
     ap.add_argument("--compute-steps", type=int, default=3)
+    ap.add_argument("--no-collectives", action="store_true",
+                    help="skip the per-N partition-group collective GB/s points (N > 1)")
     return ap.parse_args()
 
 
@@ -692,6 +694,19 @@ def run_mics(args, wl, rank, world, local):
     }
     step.close()
     eng.close()
+    if world > 1 and not args.no_collectives:
+        # partition-group collectives vs NVLink at this GPU count (BASELINE.json metric, second
+        # half): one rank per GPU, p in {2, 4, 8} dividing N, 256 MiB and 1 GiB, libmics vs NCCL
+        try:
+            from tools.sweep import run_sweep
+            pts = run_sweep(args, rank, world, local, sizes=[256 << 20, 1 << 30], quiet=True)
+            line["collectives"] = [{"op": r["op"], "p": r["p"], "bytes": r["bytes"],
+                                    "busbw_GBps": round(r["mics_busbw_GBps"], 1),
+                                    "frac_of_770": round(r["frac_nvlink_770"], 3),
+                                    "nccl_busbw_GBps": round(r["nccl_busbw_GBps"], 1) if r["nccl_busbw_GBps"] else None}
+                                   for r in pts]
+        except Exception as e:  # noqa: BLE001
+            line["collectives"] = {"error": str(e)[:200]}
     if not args.no_compute and wl.hidden and args.schedule == "two_hop":
         try:
             line["compute_step"] = measure_compute(args, wl, rank, world, local)

@@ -40,7 +40,10 @@ def _time(fn, stream_ext, reps, world, gloo, trials=3):
     return t * 1e3  # us
 
 
-def run_sweep(args, rank, world, local):
+def run_sweep(args, rank, world, local, sizes=None, quiet=False):
+    """All-gather / reduce-scatter busBW (libmics plans and NCCL) for every p in {2,4,8}
+    dividing `world`, one rank per GPU; prints one JSON line per point unless `quiet`;
+    returns the points."""
     import torch
     import torch.distributed as dist
 
@@ -50,9 +53,10 @@ def run_sweep(args, rank, world, local):
     from paper_2205_00119_b200.engine import Engine
 
     gloo = bench.GLOO
-    maxlog = int(os.environ.get("MICS_SWEEP_MAXLOG", 30))
-    sizes = [1 << e for e in range(20, maxlog + 1)]
-    M = sizes[-1]
+    if sizes is None:
+        maxlog = int(os.environ.get("MICS_SWEEP_MAXLOG", 30))
+        sizes = [1 << e for e in range(20, maxlog + 1)]
+    M = max(sizes)
     eng = Engine(n_ranks=world, world=world, world_rank=rank, device=local, arena_bytes=3 * M + (64 << 20))
     mdist.connect(eng, gloo)
     src, dst = eng.alloc(M), eng.alloc(M)
@@ -98,14 +102,15 @@ def run_sweep(args, rank, world, local):
                         "mics_busbw_GBps": bus, "frac_nvlink_770": bus / NVLINK,
                         "nccl_us": nus, "nccl_busbw_GBps": (p - 1) * m / p / (nus * 1e-6) / 1e9 if nus else None}
                 results.append(line)
-                if rank == 0:
+                if rank == 0 and not quiet:
                     print(json.dumps(line), flush=True)
             ag.close()
             rs.close()
-    if rank == 0 and results:
+    if rank == 0 and results and not quiet:
         big = [r for r in results if r["bytes"] >= (256 << 20)]
         wins = sum(1 for r in results if r["nccl_us"] and r["mics_us"] < r["nccl_us"])
         print(json.dumps({"sweep_summary": "C2", "points": len(results), "beats_nccl": wins,
                           "min_frac_nvlink_>=256MiB": min(r["frac_nvlink_770"] for r in big) if big else None}),
               flush=True)
     eng.close()
+    return results
