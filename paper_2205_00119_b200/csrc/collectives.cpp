@@ -262,6 +262,10 @@ void enqueue(mics_ctx* ctx, const Launch& l, int dep_first, cudaStream_t stream)
     case Launch::BARRIER:
       launch_barrier(st, bar);
       break;
+    case Launch::TAIL:
+      launch_tail(st, l.in_t, l.tail_r, l.tail_p, static_cast<const TailJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid,
+                  l.adam, l.dyn, l.mode, bar);
+      break;
     case Launch::BOUNDARY:
       launch_boundary(st, static_cast<const BndJob*>(l.d_desc), l.ndesc, l.rs_tiles, l.ntiles, l.grid,
                       l.adam, l.epoch, l.dyn, bar);

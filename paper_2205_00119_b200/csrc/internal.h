@@ -117,6 +117,24 @@ struct BndJob {
   uint32_t rs_tile0, ad_tile0, pad_;
 };
 
+// Fused tail (K8, every rank on this GPU): the last micro-step's reduce-scatter, the
+// boundary all-reduce and Adam in one pass over (partition position j, layer): for
+// every replica q of position j, a_q = acc_q (+)= fold_i grads_{q,i}; red = fold_q a_q;
+// Adam on replica q's state with red.  Same operations in the same order as the
+// K2 + K2 + K5 sequence it replaces, without writing / re-reading a_q and red.
+constexpr int kTailMaxR = 8, kTailMaxP = 8;
+constexpr uint32_t kTailTile = kThreads * 4;  // fp32 elements per tile (one float4 per thread)
+struct TailJob {
+  const float* acc[kTailMaxR];                    // replica q's accumulator (shard, this layer)
+  const uint8_t* grads[kTailMaxR * kTailMaxP];   // [q][i]: member i of replica q's group, chunk j
+  float* prm[kTailMaxR];
+  float* m[kTailMaxR];
+  float* v[kTailMaxR];
+  uint16_t* bf[kTailMaxR];                        // nullable
+  uint64_t elems, valid;                          // chunk elements (multiple of 8); valid gradient prefix
+  uint32_t tile0, pad_;
+};
+
 // Flag barrier between processes: remote_flag[w] is the slot on process w's
 // arena reserved for this process; local_flag[w] is the slot process w writes
 // on ours.  Values are monotone barrier counts per process pair.
@@ -155,6 +173,10 @@ int resident_ctas(int kind /* 0 copy, 1 reduce, 2 adam */, mics_dtype in_t, int 
 void launch_adam(cudaStream_t s, const AdamJob* jobs, int njobs, uint32_t ntiles, int grid, const AdamScalars& sc,
                  const DevScalars* dyn, const BarrierArg& bar);
 void launch_set_scalars(cudaStream_t s, DevScalars* dst, const DevScalars& v);
+// false when (r, p) has no instantiation (the caller keeps the unfused tail)
+bool tail_supported(mics_dtype in_t, int r, int p);
+void launch_tail(cudaStream_t s, mics_dtype in_t, int r, int p, const TailJob* jobs, int njobs, uint32_t ntiles,
+                 int grid, const AdamScalars& sc, const DevScalars* dyn, int zero_accum, const BarrierArg& bar);
 constexpr uint32_t kAdamTile = kThreads * kAdamUnroll * 4;
 void launch_generate(cudaStream_t s, void* out, mics_dtype dtype, uint64_t seed, int rank, int step, int layer,
                      uint64_t start, uint64_t count, int grid);
@@ -285,7 +307,8 @@ struct AdamPlan {
 
 // A device-resident, replayable launch (built once, launched many times).
 struct Launch {
-  enum Kind { COPY, REDUCE, ADAM, BARRIER, BOUNDARY } kind = COPY;
+  enum Kind { COPY, REDUCE, ADAM, BARRIER, BOUNDARY, TAIL } kind = COPY;
+  int tail_r = 0, tail_p = 0;  // TAIL: replicas and group size (mode = 1 zero-accumulate)
   uint32_t rs_tiles = 0;   // BOUNDARY: tiles of the reduce-scatter phase
   uint64_t epoch = 0;      // BOUNDARY: flag value of this launch (monotone per sync state)
   void* d_desc = nullptr;  // owned device table (cudaMalloc)

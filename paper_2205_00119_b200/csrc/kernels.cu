@@ -549,6 +549,94 @@ __global__ void __launch_bounds__(kThreads) k_adam(const AdamJob* __restrict__ j
   pdl_end(bar);
 }
 
+// ---------------------------------------------------------------- K8: fused tail (all ranks local)
+template <typename In>
+__device__ __forceinline__ void load4(const uint8_t* base, uint64_t e, float (&x)[4]) {
+  if constexpr (sizeof(In) == 4) {
+    const uint4 r = ld_stream(reinterpret_cast<const float*>(base) + e);
+    x[0] = __uint_as_float(r.x);
+    x[1] = __uint_as_float(r.y);
+    x[2] = __uint_as_float(r.z);
+    x[3] = __uint_as_float(r.w);
+  } else {  // bf16 -> fp32 is exact
+    const uint2 r = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(base) + e);
+    x[0] = __uint_as_float(r.x << 16);
+    x[1] = __uint_as_float(r.x & 0xffff0000u);
+    x[2] = __uint_as_float(r.y << 16);
+    x[3] = __uint_as_float(r.y & 0xffff0000u);
+  }
+}
+
+template <typename In, int R, int P>
+__global__ void __launch_bounds__(kThreads, 2) k_tail(const TailJob* __restrict__ jobs, int njobs, uint32_t ntiles,
+                                                     AdamScalars sc, const DevScalars* __restrict__ dyn, int zero_accum,
+                                                     BarrierArg bar) {
+  if (dyn) sc = dyn->sc;
+  pdl_begin(bar);
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const TailJob& J = jobs[find_desc(jobs, njobs, tile)];
+    const uint64_t e = uint64_t(tile - J.tile0) * kTailTile + uint64_t(threadIdx.x) * 4;
+    if (e >= J.elems) continue;  // elems is a multiple of 8: every vector is whole
+    // phase 1: every replica's accumulator and gradient sources in flight, then the folds
+    float a[R][4], g[R][P][4];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      if (!zero_accum) {
+        const float4 t = *reinterpret_cast<const float4*>(J.acc[q] + e);
+        a[q][0] = t.x;
+        a[q][1] = t.y;
+        a[q][2] = t.z;
+        a[q][3] = t.w;
+      }
+#pragma unroll
+      for (int i = 0; i < P; ++i) load4<In>(J.grads[q * kTailMaxP + i], e, g[q][i]);
+    }
+    float red[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool valid = e + uint64_t(k) < J.valid;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        float f = 0.0f;  // padding: every position contributes zeros, the fold is +0
+        if (valid) {
+          f = g[q][0][k];
+#pragma unroll
+          for (int i = 1; i < P; ++i) f = __fadd_rn(f, g[q][i][k]);
+        }
+        a[q][k] = zero_accum ? __fadd_rn(0.0f, f) : __fadd_rn(a[q][k], f);  // micro-step accumulate
+      }
+      red[k] = a[0][k];
+#pragma unroll
+      for (int q = 1; q < R; ++q) red[k] = __fadd_rn(red[k], a[q][k]);  // boundary fold, ascending replica
+    }
+    // phase 2: Adam on every replica's state (all loads of the replica set in flight)
+    float4 pp[R], mm[R], vv[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      pp[q] = *reinterpret_cast<const float4*>(J.prm[q] + e);
+      mm[q] = *reinterpret_cast<const float4*>(J.m[q] + e);
+      vv[q] = *reinterpret_cast<const float4*>(J.v[q] + e);
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      adam_one(red[0], pp[q].x, mm[q].x, vv[q].x, sc);
+      adam_one(red[1], pp[q].y, mm[q].y, vv[q].y, sc);
+      adam_one(red[2], pp[q].z, mm[q].z, vv[q].z, sc);
+      adam_one(red[3], pp[q].w, mm[q].w, vv[q].w, sc);
+      *reinterpret_cast<float4*>(J.prm[q] + e) = pp[q];
+      *reinterpret_cast<float4*>(J.m[q] + e) = mm[q];
+      *reinterpret_cast<float4*>(J.v[q] + e) = vv[q];
+      if (J.bf[q]) {
+        uint2 pk;
+        pk.x = uint32_t(f32_to_bf16(pp[q].x)) | (uint32_t(f32_to_bf16(pp[q].y)) << 16);
+        pk.y = uint32_t(f32_to_bf16(pp[q].z)) | (uint32_t(f32_to_bf16(pp[q].w)) << 16);
+        *reinterpret_cast<uint2*>(J.bf[q] + e) = pk;
+      }
+    }
+  }
+  pdl_end(bar);
+}
+
 // ---------------------------------------------------------------- K6: counter-based gradients
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
@@ -842,6 +930,26 @@ void launch_reduce(cudaStream_t s, mics_dtype in_t, mics_dtype acc_t, const RedJ
 void launch_adam(cudaStream_t s, const AdamJob* jobs, int njobs, uint32_t ntiles, int grid, const AdamScalars& sc,
                  const DevScalars* dyn, const BarrierArg& bar) {
   launch_ex(k_adam, grid, kThreads, 0, s, jobs, njobs, ntiles, sc, dyn, bar);
+}
+
+bool tail_supported(mics_dtype in_t, int r, int p) {
+  return (in_t == MICS_F32 || in_t == MICS_BF16) && ((r == 4 && p == 2) || (r == 2 && p == 4) || (r == 1 && p == 8));
+}
+
+void launch_tail(cudaStream_t s, mics_dtype in_t, int r, int p, const TailJob* jobs, int njobs, uint32_t ntiles,
+                 int grid, const AdamScalars& sc, const DevScalars* dyn, int zero_accum, const BarrierArg& bar) {
+  const bool bf = in_t == MICS_BF16;
+  if (r == 4 && p == 2)
+    bf ? launch_ex(k_tail<uint16_t, 4, 2>, grid, kThreads, 0, s, jobs, njobs, ntiles, sc, dyn, zero_accum, bar)
+       : launch_ex(k_tail<float, 4, 2>, grid, kThreads, 0, s, jobs, njobs, ntiles, sc, dyn, zero_accum, bar);
+  else if (r == 2 && p == 4)
+    bf ? launch_ex(k_tail<uint16_t, 2, 4>, grid, kThreads, 0, s, jobs, njobs, ntiles, sc, dyn, zero_accum, bar)
+       : launch_ex(k_tail<float, 2, 4>, grid, kThreads, 0, s, jobs, njobs, ntiles, sc, dyn, zero_accum, bar);
+  else if (r == 1 && p == 8)
+    bf ? launch_ex(k_tail<uint16_t, 1, 8>, grid, kThreads, 0, s, jobs, njobs, ntiles, sc, dyn, zero_accum, bar)
+       : launch_ex(k_tail<float, 1, 8>, grid, kThreads, 0, s, jobs, njobs, ntiles, sc, dyn, zero_accum, bar);
+  else
+    raise(MICS_SHAPE_ERROR, "fused tail: unsupported (replicas, group size)");
 }
 
 void launch_set_scalars(cudaStream_t s, DevScalars* dst, const DevScalars& v) {

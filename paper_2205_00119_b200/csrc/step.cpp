@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "internal.h"
@@ -52,6 +53,7 @@ void release(mics_step* st) {
   for (auto e : st->ev_bnd) cudaEventDestroy(e);
   if (st->gexec) cudaGraphExecDestroy(st->gexec);
   for (auto& l : st->tail_rs) l.release();
+  st->ftail.release();
   for (auto& b : st->tail_bnd) {
     b.rs.release();
     b.ag.release();
@@ -257,6 +259,72 @@ void enqueue_tail(mics_step* st, std::vector<cudaEvent_t>* clk) {
     MICS_CUDA(cudaEventRecord(st->ev_tail_done, S));
     MICS_CUDA(cudaStreamWaitEvent(M, st->ev_tail_done, 0));
   }
+}
+
+// K8 plan: one job per (partition position j, layer) covering that layer's chunk of
+// every replica of position j (all ranks are local: world == 1).
+void build_fused_tail(mics_step* st) {
+  mics_ctx* ctx = st->ctx;
+  mics_sync* sy = st->sync;
+  const int n = sy->n, p = sy->p, r = n / p, L = st->cfg.nlayers, s = st->cfg.s;
+  const uint64_t szg = dtype_size(st->cfg.grad_t);
+  const uint64_t goff = uint64_t((s - 1) % st->gslots) * sy->grad_elems * szg;
+  std::vector<TailJob> jobs;
+  uint32_t tiles = 0;
+  uint64_t bytes = 0;
+  for (int j = 0; j < p; ++j)
+    for (int l = 0; l < L; ++l) {
+      TailJob J;
+      std::memset(&J, 0, sizeof(J));
+      const uint64_t c = sy->chunk[size_t(l)], so = sy->shard_off[size_t(l)], first = uint64_t(j) * c;
+      const uint64_t len = sy->len[size_t(l)];
+      for (int q = 0; q < r; ++q) {
+        const int rho = q * p + j;  // replica q of position j (partition group q)
+        J.acc[q] = reinterpret_cast<const float*>(ctx->rank_ptr(sy->shard, rho)) + so;
+        for (int i = 0; i < p; ++i)
+          J.grads[q * kTailMaxP + i] = reinterpret_cast<const uint8_t*>(
+              ctx->rank_ptr(st->grads, q * p + i) + goff + (sy->grad_off[size_t(l)] + first) * szg);
+        J.prm[q] = reinterpret_cast<float*>(ctx->rank_ptr(st->master, rho)) + so;
+        J.m[q] = reinterpret_cast<float*>(ctx->rank_ptr(st->m, rho)) + so;
+        J.v[q] = reinterpret_cast<float*>(ctx->rank_ptr(st->v, rho)) + so;
+        J.bf[q] = reinterpret_cast<uint16_t*>(ctx->rank_ptr(st->pbf16, rho)) + so;
+      }
+      J.elems = c;
+      J.valid = len > first ? len - first : 0;
+      J.tile0 = tiles;
+      tiles += uint32_t(ceil_div(c, kTailTile));
+      jobs.push_back(J);
+      // HBM per element: r x (acc + p gradients + p, m, v) read, r x (p, m, v, bf16) written
+      bytes += c * uint64_t(r) * ((s > 1 ? 4 : 0) + uint64_t(p) * szg + 12 + 14);
+    }
+  Launch& t = st->ftail;
+  t.kind = Launch::TAIL;
+  t.in_t = st->cfg.grad_t;
+  t.tail_r = r;
+  t.tail_p = p;
+  t.mode = s == 1 ? 1 : 0;  // zero-accumulate when the last micro-step is the first
+  t.ndesc = int(jobs.size());
+  t.ntiles = tiles;
+  t.grid = ctx->grid_for(tiles, 2);
+  t.bar = ctx->barrier(0, 0, 0);
+  t.hbm_bytes = bytes;
+  MICS_CUDA(cudaMalloc(&t.d_desc, jobs.size() * sizeof(TailJob)));
+  MICS_CUDA(cudaMemcpy(t.d_desc, jobs.data(), jobs.size() * sizeof(TailJob), cudaMemcpyHostToDevice));
+  st->fused_tail = true;
+}
+
+void enqueue_fused_tail(mics_step* st) {
+  mics_ctx* ctx = st->ctx;
+  st->adam_step++;
+  const AdamScalars sc = make_adam_scalars(st->cfg.lr, st->cfg.beta1, st->cfg.beta2, st->cfg.eps,
+                                           st->cfg.weight_decay, st->adam_step, st->adam.grad_scale);
+  if (st->d_scalars && !st->capturing) {
+    DevScalars v{};
+    v.sc = sc;
+    launch_set_scalars(ctx->stream, st->d_scalars, v);
+  }
+  st->ftail.adam = sc;
+  enqueue(ctx, st->ftail);
 }
 
 // forward then backward per-layer gathers.  The first gather of a window follows
@@ -817,6 +885,10 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
         for (auto& e : st->ev_tail) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         MICS_CUDA(cudaEventCreateWithFlags(&st->ev_tail_done, cudaEventDisableTiming));
       }
+      const char* fe = std::getenv("MICS_FUSED_TAIL");
+      if (!st->tail && !st->compute && ctx->world == 1 && !(fe && fe[0] == '0') &&
+          tail_supported(cfg->grad_t, sy->n / sy->p, sy->p))
+        build_fused_tail(st);
     } else {  // shards already hold the global sum: the boundary is Adam on the own shard
       AdamPlan ap;
       uint64_t pmask = 0;
@@ -863,7 +935,7 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
         S2.ag_hbm_bytes += 2 * uint64_t(cfg->s) * x.hbm_bytes;
       }
     for (size_t t = 0; t < st->micro.size(); ++t) {
-      if (st->tail && t + 1 == st->micro.size()) continue;  // replaced by the per-group tail launches
+      if ((st->tail || st->fused_tail) && t + 1 == st->micro.size()) continue;  // replaced by the tail launches
       for (auto& x : st->micro[t]) {
         S2.rs_launches += runs(x);
         S2.rs_remote_bytes += x.remote_bytes;
@@ -880,8 +952,12 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
       for (const auto& x : st->bndg[0]) bl.push_back(&x);
     else if (st->tail)
       for (const auto& x : st->tail_bnd) bl.push_back(&x);
-    else
+    else if (!st->fused_tail)
       bl.push_back(&st->bnd);
+    if (st->fused_tail) {
+      S2.bnd_launches += 1;
+      S2.bnd_hbm_bytes += st->ftail.hbm_bytes;
+    }
     for (const BoundaryLaunches* b : bl)
       for (const Launch* x : {&b->rs, &b->ag}) {
         if ((x == &b->rs && !b->has_rs) || (x == &b->ag && !b->has_ag)) continue;
@@ -938,6 +1014,7 @@ void build_graph(mics_step* st) {
   MICS_CUDA(cudaMalloc(&st->d_scalars, sizeof(DevScalars)));
   st->bnd.rs.dyn = st->bnd.ag.dyn = st->d_scalars;
   for (auto& b : st->tail_bnd) b.ag.dyn = st->d_scalars;
+  st->ftail.dyn = st->d_scalars;
   const int adam_step0 = st->adam_step;
   const uint64_t epoch0 = st->sync->epoch, launches0 = ctx->launches;
   cudaGraph_t g = nullptr;
@@ -949,14 +1026,17 @@ void build_graph(mics_step* st) {
     } else {
       for (int t = 0; t < st->cfg.s; ++t) {
         if (generated(st)) enqueue_generate(st, t);
-        if (st->tail && t == st->cfg.s - 1) {
+        if ((st->tail || st->fused_tail) && t == st->cfg.s - 1) {
           enqueue_gathers(st, t, false);
-          enqueue_tail(st, nullptr);
+          if (st->tail)
+            enqueue_tail(st, nullptr);
+          else
+            enqueue_fused_tail(st);
         } else {
           enqueue_micro(st, t, false);
         }
       }
-      if (!st->tail) enqueue_boundary(st, false);
+      if (!st->tail && !st->fused_tail) enqueue_boundary(st, false);
     }
   } catch (...) {
     st->capturing = false;
@@ -1018,14 +1098,17 @@ void step_run(mics_step* st, int iters) {
     }
     for (int t = 0; t < st->cfg.s; ++t) {
       if (generated(st)) enqueue_generate(st, t);
-      if (st->tail && t == st->cfg.s - 1) {
+      if ((st->tail || st->fused_tail) && t == st->cfg.s - 1) {
         enqueue_gathers(st, t, true);
-        enqueue_tail(st, nullptr);
+        if (st->tail)
+          enqueue_tail(st, nullptr);
+        else
+          enqueue_fused_tail(st);
       } else {
         enqueue_micro(st, t, true);
       }
     }
-    if (!st->tail) enqueue_boundary(st, true);
+    if (!st->tail && !st->fused_tail) enqueue_boundary(st, true);
     st->step_idx++;
   }
   join_side(st);
@@ -1062,13 +1145,15 @@ void step_profile(mics_step* st, double* ms) {
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
     enqueue_gathers(st, t, false);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
-    if (!(st->tail && t == s - 1)) enqueue_sync(st, t, false);
+    if (!((st->tail || st->fused_tail) && t == s - 1)) enqueue_sync(st, t, false);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
   }
   MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
   std::vector<cudaEvent_t> tclk;  // overlapped tail, serialised: RS / boundary per layer group
   if (st->tail)
     enqueue_tail(st, &tclk);
+  else if (st->fused_tail)
+    enqueue_fused_tail(st);  // timed as the boundary phase (it carries the last reduce-scatter)
   else
     enqueue_boundary(st, false);
   st->step_idx++;
@@ -1168,12 +1253,14 @@ void step_run_host(mics_step* st, const void* host_grads, int iters, void* host_
       MICS_CUDA(cudaStreamWaitEvent(ctx->stream, st->ev_h2d[size_t(k)], 0));
       if (st->tail && t == s - 1)
         enqueue_tail(st, nullptr);  // last reduce-scatter + boundary, overlapped per layer group
+      else if (st->fused_tail && t == s - 1)
+        enqueue_fused_tail(st);     // last reduce-scatter + boundary + Adam in one kernel
       else
         enqueue_sync(st, t, true);
       MICS_CUDA(cudaEventRecord(st->ev_rs_slot[size_t(k)], ctx->stream));
       if (nslot != s && t + 1 < s) copy_in(t + 1);
     }
-    if (!st->tail) enqueue_boundary(st, true);
+    if (!st->tail && !st->fused_tail) enqueue_boundary(st, true);
     st->step_idx++;
     if (host_result) {
       join_side(st);

@@ -90,6 +90,10 @@ struct mics_step {
   // per layer group on the main stream (channel 0) while each finished group's
   // boundary all-reduce + Adam (NVLink) runs on the side stream (channel 1).
   bool tail = false;
+  // Fused tail (every rank on this GPU, N=1; MICS_FUSED_TAIL=0 disables): the last
+  // micro-step's reduce-scatter + the boundary all-reduce + Adam as one K8 launch
+  bool fused_tail = false;
+  mics::Launch ftail{};
   std::vector<mics::Launch> tail_rs;
   std::vector<mics::BoundaryLaunches> tail_bnd;
   std::vector<cudaEvent_t> ev_tail;

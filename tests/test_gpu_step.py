@@ -220,6 +220,7 @@ def test_overlapped_tail_matches_in_order(monkeypatch, graph):
     from paper_2205_00119_b200.engine import Engine, host_alloc, host_free
     from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
     monkeypatch.setenv("MICS_GRAPH", graph)
+    monkeypatch.setenv("MICS_FUSED_TAIL", "0")  # the in-order reference path, not K8 (one GPU)
     wl = Workload("tail", [70_000, 12_345, 40_000, 9_999, 33_333, 4_096], p=2, s=3)
     res = {}
     for tail in ("0", "1"):
@@ -249,3 +250,36 @@ def test_overlapped_tail_matches_in_order(monkeypatch, graph):
     # same reduce-scatter bytes; the tail splits the last reduce-scatter and the boundary per layer group
     assert res["1launch"][2] == res["0launch"][2]
     assert res["1launch"][0] > res["0launch"][0] and res["1launch"][1] > res["0launch"][1]
+
+
+@pytest.mark.parametrize("p,s,grad_dtype", [(2, 3, "f32"), (4, 2, "bf16"), (8, 2, "f32"), (2, 1, "bf16")])
+def test_fused_tail_matches_unfused(monkeypatch, p, s, grad_dtype):
+    """K8 (last reduce-scatter + boundary all-reduce + Adam in one kernel, all ranks on one
+    GPU): same bits as the K2 + K2 + K5 sequence over several steps (graph, profiled and
+    host-input steps included), for every instantiated (replicas, group size)."""
+    from paper_2205_00119_b200.engine import Engine, host_alloc, host_free
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
+    wl = Workload("ft", [70_000, 12_345, 40_000, 9_999, 4_096], p=p, s=s, grad_dtype=grad_dtype)
+    res = {}
+    for fused in ("0", "1"):
+        monkeypatch.setenv("MICS_FUSED_TAIL", fused)
+        eng = Engine(n_ranks=8, device=0, arena_bytes=256 << 20)
+        step = MicsStep(eng, wl, StepOptions(seed=17, lr=1e-3, weight_decay=0.02))
+        G = step.stats().grad_elems
+        szg = 2 if grad_dtype == "bf16" else 4
+        host, hptr = host_alloc(G * szg)
+        host[:] = np.random.default_rng(2).integers(0, 255, G * szg, dtype=np.uint8) & 0x3f
+        step.run(2)
+        step.profile()
+        step.run_host(hptr, 1)
+        step.run(1)
+        eng.synchronize()
+        S = step.sync_info()[0].shard_elems
+        b = step.buffers()
+        res[fused] = [eng.d2h(b[k], r, S) for k in ("master", "exp_avg", "exp_avg_sq") for r in range(8)]
+        res[fused].append(eng.d2h(b["param_bf16"], 6, S, "bf16"))
+        step.close()
+        host_free(hptr)
+        eng.close()
+    for x, y in zip(res["0"], res["1"]):
+        assert np.array_equal(x.view(np.uint16), y.view(np.uint16))
