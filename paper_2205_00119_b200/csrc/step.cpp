@@ -59,6 +59,8 @@ void release(mics_step* st) {
     b.ag.release();
   }
   for (auto e : st->ev_tail) cudaEventDestroy(e);
+  for (auto e : st->ev_tail_rs) cudaEventDestroy(e);
+  if (st->tail_rs_stream) cudaStreamDestroy(st->tail_rs_stream);
   if (st->ev_tail_done) cudaEventDestroy(st->ev_tail_done);
   for (auto e : st->ev_h2d) cudaEventDestroy(e);
   for (auto e : st->ev_rs_slot) cudaEventDestroy(e);
@@ -241,16 +243,24 @@ void enqueue_tail(mics_step* st, std::vector<cudaEvent_t>* clk) {
     MICS_CUDA(cudaEventRecord(e, M));
     clk->push_back(e);
   };
+  // three streams: last RS per group (main, channel 0) -> boundary RS per group (its own
+  // stream, channel 2: NVLink-bound) -> Adam per group (side stream, channel 1: HBM-bound),
+  // so group g+1's boundary reduce-scatter runs under group g's Adam
+  cudaStream_t R2 = serial ? M : st->tail_rs_stream;
   mark();
   for (size_t g = 0; g < st->tail_rs.size(); ++g) {
     enqueue(ctx, st->tail_rs[g], -1, M);
     mark();
     if (!serial) {
       MICS_CUDA(cudaEventRecord(st->ev_tail[g], M));
-      MICS_CUDA(cudaStreamWaitEvent(S, st->ev_tail[g], 0));
+      MICS_CUDA(cudaStreamWaitEvent(R2, st->ev_tail[g], 0));
     }
     BoundaryLaunches& b = st->tail_bnd[g];
-    if (b.has_rs) enqueue(ctx, b.rs, -1, S);
+    if (b.has_rs) enqueue(ctx, b.rs, -1, R2);
+    if (!serial) {
+      MICS_CUDA(cudaEventRecord(st->ev_tail_rs[g], R2));
+      MICS_CUDA(cudaStreamWaitEvent(S, st->ev_tail_rs[g], 0));
+    }
     b.ag.adam = sc;
     enqueue(ctx, b.ag, -1, S);
     mark();
@@ -878,11 +888,15 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
           st->tail_rs.push_back(build_micro_launch(sy, st->grads, goff, cfg->grad_t, 1.0,
                                                    s_last == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE, true, false,
                                                    1, 1, nullptr, l0, l1));
-          st->tail_bnd.push_back(
-              build_boundary_range(sy, &st->adam, sy->shard, st->group_range[g].first, st->group_range[g].second, 1));
+          // boundary reduce-scatter on channel 2 (its own stream), Adam on channel 1 (side stream)
+          st->tail_bnd.push_back(build_boundary_range(sy, &st->adam, sy->shard, st->group_range[g].first,
+                                                      st->group_range[g].second, 1, 2));
         }
         st->ev_tail.resize(st->group_range.size());
         for (auto& e : st->ev_tail) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        st->ev_tail_rs.resize(st->group_range.size());
+        for (auto& e : st->ev_tail_rs) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        MICS_CUDA(cudaStreamCreateWithFlags(&st->tail_rs_stream, cudaStreamNonBlocking));
         MICS_CUDA(cudaEventCreateWithFlags(&st->ev_tail_done, cudaEventDisableTiming));
       }
       const char* fe = std::getenv("MICS_FUSED_TAIL");

@@ -263,7 +263,7 @@ BoundaryLaunches build_boundary(mics_sync* st, const mics_adam* adam, bool persi
 // `chan`.  Same fold order and Adam as build_boundary: the range is split into r
 // slices of ceil(len/r) (rounded to 4) and position i reduces slice i in place.
 BoundaryLaunches build_boundary_range(mics_sync* st, const mics_adam* adam, mics_buf shard, uint64_t lo, uint64_t hi,
-                                      int chan) {
+                                      int chan, int rs_chan) {
   mics_ctx* ctx = st->ctx;
   const int n = st->n, p = st->p, r = n / p;
   const uint64_t len = hi - lo;
@@ -289,7 +289,7 @@ BoundaryLaunches build_boundary_range(mics_sync* st, const mics_adam* adam, mics
       for (int q = 0; q < r; ++q) srcs[size_t(q)] = ctx->rank_ptr(shard, j + q * p) + start * 4;
       rs.add(srcs, ctx->rank_ptr(shard, rho) + start * 4, elems, elems);
     }
-    out.rs = make_reduce_launch(ctx, rs, MICS_F32, MICS_F32, 1.0, MICS_RS_STORE, ctx->barrier(rmask, 1, 1, chan), true);
+    out.rs = make_reduce_launch(ctx, rs, MICS_F32, MICS_F32, 1.0, MICS_RS_STORE, ctx->barrier(rmask, 1, 1, rs_chan < 0 ? chan : rs_chan), true);
     out.has_rs = true;
   }
   AdamPlan ap;

@@ -44,7 +44,7 @@ Launch build_micro_launch(mics_sync* st, mics_buf grads, uint64_t goff, mics_dty
                           const mics_buf* shard_override = nullptr, int seg_lo = 0, int seg_hi = -1);
 BoundaryLaunches build_boundary(mics_sync* st, const mics_adam* adam, bool persistent, bool record);
 BoundaryLaunches build_boundary_range(mics_sync* st, const mics_adam* adam, mics_buf shard, uint64_t lo, uint64_t hi,
-                                      int chan);
+                                      int chan, int rs_chan = -1);
 void micro_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode);
 void boundary(mics_sync* st, const mics_adam* adam);
 void alt_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale);
@@ -96,8 +96,9 @@ struct mics_step {
   mics::Launch ftail{};
   std::vector<mics::Launch> tail_rs;
   std::vector<mics::BoundaryLaunches> tail_bnd;
-  std::vector<cudaEvent_t> ev_tail;
+  std::vector<cudaEvent_t> ev_tail, ev_tail_rs;   // [group]: last RS done / boundary RS done
   cudaEvent_t ev_tail_done = nullptr;
+  cudaStream_t tail_rs_stream = nullptr;          // boundary reduce-scatters (channel 2), ahead of Adam
   // CUDA-graph replay (default; MICS_GRAPH=0 enqueues every kernel per step):
   // one captured step whose boundary kernels read the per-step Adam scalars and
   // flag epoch from d_scalars, set by one small kernel before each replay.
