@@ -184,24 +184,26 @@ def main():
     step.close()
     e6.close()
 
-    # ---- overlapped tail (auto-on when partition groups stay inside a GPU) vs in order
-    res = {}
-    for tail in ("0", "1"):
-        os.environ["MICS_TAIL_OVERLAP"] = tail
-        e5 = Engine(n_ranks=n, world=world, world_rank=rank, device=local, arena_bytes=256 << 20)
-        mdist.connect(e5)
-        step = MicsStep(e5, Workload("tail", [70_000, 12_345, 40_000, 9_999, 33_333], p=2, s=3), StepOptions(seed=5))
-        step.run(2)
-        step.profile()
-        step.run(1)
-        e5.synchronize()
-        S = step.sync_info()[0].shard_elems
-        res[tail] = [e5.d2h(step.buffers()["master"], r, S) for r in e5.local_ranks]
-        step.close()
-        e5.close()
-    os.environ.pop("MICS_TAIL_OVERLAP")
-    for x, y in zip(res["0"], res["1"]):
-        expect(np.array_equal(x.view(np.uint32), y.view(np.uint32)), "overlapped tail != in-order")
+    # ---- overlapped tail (auto-on for multi-process jobs) vs in order; p=4 spans GPUs at world 4
+    for pt in (2, 4):
+        res = {}
+        for tail in ("0", "1"):
+            os.environ["MICS_TAIL_OVERLAP"] = tail
+            e5 = Engine(n_ranks=n, world=world, world_rank=rank, device=local, arena_bytes=256 << 20)
+            mdist.connect(e5)
+            step = MicsStep(e5, Workload("tail", [70_000, 12_345, 40_000, 9_999, 33_333], p=pt, s=3),
+                            StepOptions(seed=5))
+            step.run(2)
+            step.profile()
+            step.run(1)
+            e5.synchronize()
+            S = step.sync_info()[0].shard_elems
+            res[tail] = [e5.d2h(step.buffers()["master"], r, S) for r in e5.local_ranks]
+            step.close()
+            e5.close()
+        os.environ.pop("MICS_TAIL_OVERLAP")
+        for x, y in zip(res["0"], res["1"]):
+            expect(np.array_equal(x.view(np.uint32), y.view(np.uint32)), f"overlapped tail != in-order (p={pt})")
 
     # ---- pipelined boundary (side stream + channel-1 barriers) vs in order, 3 steps
     res = {}
