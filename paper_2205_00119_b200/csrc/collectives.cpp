@@ -87,6 +87,14 @@ void AdamPlan::add(const std::vector<const void*>& src, float* param, float* m, 
   srcs.push_back(src);
 }
 
+void AdamPlan::add_replica(float* param2, float* m2, float* v2, uint16_t* pbf16_2) {
+  AdamJob& j = jobs.back();
+  j.param2 = param2;
+  j.m2 = m2;
+  j.v2 = v2;
+  j.pbf16_2 = pbf16_2;
+}
+
 void Launch::release() {
   if (d_desc) cudaFree(d_desc);
   d_desc = nullptr;
@@ -188,6 +196,7 @@ Launch make_adam_launch(mics_ctx* ctx, const AdamPlan& plan, const AdamScalars& 
       (ctx->is_local_ptr(plan.srcs[j][q]) ? l.hbm_bytes : l.remote_bytes) += (hi - lo) * 4;
     }
     l.hbm_bytes += J.elems * (24 + (J.pbf16 ? 2 : 0) + (J.gout ? 4 : 0));  // r/w p, m, v; w bf16; w grad
+    if (J.param2) l.hbm_bytes += J.elems * (24 + (J.pbf16_2 ? 2 : 0));      // the second replica's state
   }
   if (l.ndesc) l.d_desc = upload_jobs(ctx, plan.jobs, plan.srcs, persistent);
   return l;

@@ -80,6 +80,12 @@ struct AdamJob {              // boundary: all-gather phase fused with Adam, one
   uint64_t sub;               // slice owned by each replication position (multiple of 4)
   uint32_t rr;
   uint32_t tile0;
+  // optional second local replica of the same position (same reduced gradient, its own
+  // state): the gradient is pulled once and both replicas are updated (nullable)
+  float* param2;
+  float* m2;
+  float* v2;
+  uint16_t* pbf16_2;
 };
 
 struct AdamScalars {
@@ -303,6 +309,8 @@ struct AdamPlan {
   uint32_t tiles = 0;
   void add(const std::vector<const void*>& src, float* param, float* m, float* v, uint16_t* pbf16, float* gout,
            uint64_t elems, uint64_t sub);
+  // the job just added also updates a second replica (param2, m2, v2, pbf16_2)
+  void add_replica(float* param2, float* m2, float* v2, uint16_t* pbf16_2);
 };
 
 // A device-resident, replayable launch (built once, launched many times).

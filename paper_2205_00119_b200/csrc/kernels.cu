@@ -503,6 +503,32 @@ __global__ void __launch_bounds__(kThreads) k_adam(const AdamJob* __restrict__ j
         }
         if (J.gout) st_vec(J.gout + e, gr[u]);
       }
+      if (J.param2) {  // second replica of the position: same gradient (already in registers)
+#pragma unroll
+        for (int u = 0; u < kAdamUnroll; ++u) {
+          const uint64_t e = e0 + uint64_t(u * kThreads + threadIdx.x) * 4;
+          p[u] = *reinterpret_cast<const float4*>(J.param2 + e);
+          m[u] = *reinterpret_cast<const float4*>(J.m2 + e);
+          v[u] = *reinterpret_cast<const float4*>(J.v2 + e);
+        }
+#pragma unroll
+        for (int u = 0; u < kAdamUnroll; ++u) {
+          const uint64_t e = e0 + uint64_t(u * kThreads + threadIdx.x) * 4;
+          adam_one(__uint_as_float(gr[u].x), p[u].x, m[u].x, v[u].x, sc);
+          adam_one(__uint_as_float(gr[u].y), p[u].y, m[u].y, v[u].y, sc);
+          adam_one(__uint_as_float(gr[u].z), p[u].z, m[u].z, v[u].z, sc);
+          adam_one(__uint_as_float(gr[u].w), p[u].w, m[u].w, v[u].w, sc);
+          *reinterpret_cast<float4*>(J.param2 + e) = p[u];
+          *reinterpret_cast<float4*>(J.m2 + e) = m[u];
+          *reinterpret_cast<float4*>(J.v2 + e) = v[u];
+          if (J.pbf16_2) {
+            uint2 pk;
+            pk.x = uint32_t(f32_to_bf16(p[u].x)) | (uint32_t(f32_to_bf16(p[u].y)) << 16);
+            pk.y = uint32_t(f32_to_bf16(p[u].z)) | (uint32_t(f32_to_bf16(p[u].w)) << 16);
+            *reinterpret_cast<uint2*>(J.pbf16_2 + e) = pk;
+          }
+        }
+      }
       continue;
     }
 #pragma unroll 1
@@ -531,6 +557,24 @@ __global__ void __launch_bounds__(kThreads) k_adam(const AdamJob* __restrict__ j
           *reinterpret_cast<uint2*>(J.pbf16 + e) = pk;
         }
         if (J.gout) st_vec(J.gout + e, gr);
+        if (J.param2) {
+          float4 p2 = *reinterpret_cast<const float4*>(J.param2 + e);
+          float4 m2 = *reinterpret_cast<const float4*>(J.m2 + e);
+          float4 v2 = *reinterpret_cast<const float4*>(J.v2 + e);
+          adam_one(g[0], p2.x, m2.x, v2.x, sc);
+          adam_one(g[1], p2.y, m2.y, v2.y, sc);
+          adam_one(g[2], p2.z, m2.z, v2.z, sc);
+          adam_one(g[3], p2.w, m2.w, v2.w, sc);
+          *reinterpret_cast<float4*>(J.param2 + e) = p2;
+          *reinterpret_cast<float4*>(J.m2 + e) = m2;
+          *reinterpret_cast<float4*>(J.v2 + e) = v2;
+          if (J.pbf16_2) {
+            uint2 pk;
+            pk.x = uint32_t(f32_to_bf16(p2.x)) | (uint32_t(f32_to_bf16(p2.y)) << 16);
+            pk.y = uint32_t(f32_to_bf16(p2.z)) | (uint32_t(f32_to_bf16(p2.w)) << 16);
+            *reinterpret_cast<uint2*>(J.pbf16_2 + e) = pk;
+          }
+        }
       } else {
         for (uint64_t x = e; x < send; ++x) {
           const float g = J.srcs[x / J.sub][x];
@@ -541,6 +585,14 @@ __global__ void __launch_bounds__(kThreads) k_adam(const AdamJob* __restrict__ j
           J.v[x] = v;
           if (J.pbf16) J.pbf16[x] = f32_to_bf16(p);
           if (J.gout) J.gout[x] = g;
+          if (J.param2) {
+            float p2 = J.param2[x], m2 = J.m2[x], v2 = J.v2[x];
+            adam_one(g, p2, m2, v2, sc);
+            J.param2[x] = p2;
+            J.m2[x] = m2;
+            J.v2[x] = v2;
+            if (J.pbf16_2) J.pbf16_2[x] = f32_to_bf16(p2);
+          }
         }
       }
     }

@@ -293,17 +293,33 @@ BoundaryLaunches build_boundary_range(mics_sync* st, const mics_adam* adam, mics
     out.has_rs = true;
   }
   AdamPlan ap;
+  // Two local replicas of the same position need the same reduced gradient: one job
+  // pulls it once and updates both (each from its own state).  MICS_ADAM_DEDUP=0 keeps
+  // one job per rank.
+  const char* de = std::getenv("MICS_ADAM_DEDUP");
+  const bool dedup = !(de && de[0] == '0');
+  std::vector<char> merged(static_cast<size_t>(n), 0);
+  auto bf_of = [&](int rho) -> uint16_t* {
+    return adam->param_bf16.stride ? reinterpret_cast<uint16_t*>(ctx->rank_ptr(adam->param_bf16, rho)) + lo : nullptr;
+  };
   for (int rho = 0; rho < n; ++rho) {
-    if (!ctx->local(rho)) continue;
+    if (!ctx->local(rho) || merged[size_t(rho)]) continue;
     const int j = rho % p;
     std::vector<const void*> srcs(static_cast<size_t>(r));
     for (int q = 0; q < r; ++q) srcs[size_t(q)] = ctx->rank_ptr(shard, j + q * p) + lo * 4;
-    uint16_t* pb = adam->param_bf16.stride ? reinterpret_cast<uint16_t*>(ctx->rank_ptr(adam->param_bf16, rho)) + lo
-                                           : nullptr;
     ap.add(srcs, reinterpret_cast<float*>(ctx->rank_ptr(adam->param, rho)) + lo,
            reinterpret_cast<float*>(ctx->rank_ptr(adam->exp_avg, rho)) + lo,
-           reinterpret_cast<float*>(ctx->rank_ptr(adam->exp_avg_sq, rho)) + lo, pb, nullptr, len,
+           reinterpret_cast<float*>(ctx->rank_ptr(adam->exp_avg_sq, rho)) + lo, bf_of(rho), nullptr, len,
            r > 1 ? subg : round_up(std::max<uint64_t>(len, 1), 4));
+    if (!dedup || len == 0) continue;
+    for (int rho2 = rho + p; rho2 < n; rho2 += p)
+      if (ctx->local(rho2) && !merged[size_t(rho2)]) {
+        ap.add_replica(reinterpret_cast<float*>(ctx->rank_ptr(adam->param, rho2)) + lo,
+                       reinterpret_cast<float*>(ctx->rank_ptr(adam->exp_avg, rho2)) + lo,
+                       reinterpret_cast<float*>(ctx->rank_ptr(adam->exp_avg_sq, rho2)) + lo, bf_of(rho2));
+        merged[size_t(rho2)] = 1;
+        break;
+      }
   }
   out.ag = make_adam_launch(ctx, ap,
                             make_adam_scalars(adam->lr, adam->beta1, adam->beta2, adam->eps, adam->weight_decay,
