@@ -227,7 +227,10 @@ struct mics_ctx {
   // Barrier channels: each has its own flag slots, pairwise counters and CTA
   // tickets, so two streams can run barrier kernels concurrently (channel c is
   // only ever used from one stream, in the same order on every process).
-  static constexpr int kChannels = 3;  // 0 main stream, 1 side / gather stream, 2 copy-engine stream
+  // 0: main stream; 1: side stream (pipelined boundary, tail Adam) or the compute step's
+  // gather stream; 2: the tail's boundary reduce-scatter stream or the compute step's
+  // copy-engine reduce-scatter barriers.  Each channel is driven by one stream per step.
+  static constexpr int kChannels = 3;
   cudaStream_t side_stream = nullptr;  // channel 1: the step's pipelined boundary
   char* base = nullptr;           // local arena (IPC-exportable)
   uint64_t cap = 0, used = 0;
