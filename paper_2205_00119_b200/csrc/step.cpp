@@ -200,11 +200,13 @@ void enqueue_boundary(mics_step* st, bool side) {
 
 // Up to 4 layer groups of about equal shard size, in forward order: layer l joins
 // the group its shard midpoint falls in (empty groups vanish).
-void plan_layer_groups(mics_step* st) {
+void plan_layer_groups(mics_step* st, int groups = 4) {
   if (!st->group_range.empty()) return;
   mics_sync* sy = st->sync;
   const int L = st->cfg.nlayers;
-  const uint64_t G = uint64_t(std::min(4, L)), S = sy->shard_elems;
+  // MICS_TAIL_GROUPS overrides the pipeline depth of the overlapped tail / pipelined boundary
+  if (const char* e = std::getenv("MICS_TAIL_GROUPS")) groups = std::max(1, std::min(16, std::atoi(e)));
+  const uint64_t G = uint64_t(std::min(groups, L)), S = sy->shard_elems;
   int prev = -1;
   for (int l = 0; l < L; ++l) {
     const uint64_t mid = sy->shard_off[size_t(l)] + sy->chunk[size_t(l)] / 2;
@@ -880,7 +882,9 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
       const bool auto_on = ctx->world > 1 && sy->n / sy->p > 1;
       st->tail = !st->compute && sy->n / sy->p > 1 && (te ? te[0] == '1' : auto_on);
       if (st->tail) {
-        plan_layer_groups(st);
+        // 8 groups when the last reduce-scatter stays inside a GPU (HBM): N=2 16.36 -> 16.00 ms,
+        // N=4 8.68 -> 8.50; 4 when it crosses GPUs too (one rank per GPU: 9.85 vs 10.39 ms at 8)
+        plan_layer_groups(st, ctx->per >= cfg->p ? 8 : 4);
         const int s_last = cfg->s - 1;
         const uint64_t goff = uint64_t(s_last % st->gslots) * sy->grad_elems * szg;
         for (size_t g = 0; g < st->group_range.size(); ++g) {
