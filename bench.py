@@ -661,6 +661,10 @@ def run_mics(args, wl, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(wl, os.cpu_count() or 1)
+        if cpu and cpu["kind"] == "reference" and (os.cpu_count() or 1) > 1:
+            one = cpu_baseline(wl, 1)  # the reference's engine at 1 thread and at nproc
+            if one:
+                cpu["single_thread"] = {"value": one["value"], "cores": 1, "step_seconds": one["step_seconds"]}
 
     nccl = None
     if world > 1 and per == 1:
