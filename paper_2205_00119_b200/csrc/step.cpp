@@ -36,6 +36,7 @@ constexpr uint32_t kAlignElems = 8;
 void release(mics_step* st) {
   for (auto& v : st->ag)
     for (auto& l : v) l.release();
+  for (auto& l : st->agm) l.release();
   for (auto& v : st->micro)
     for (auto& l : v) l.release();
   for (auto& v : st->micro1)
@@ -78,7 +79,8 @@ void release(mics_step* st) {
 }
 
 // flat all-gather of layer l into gathered buffer (l % 2) of every local rank
-std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan) {
+std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan, CopyPlan* ph1_out = nullptr,
+                                   CopyPlan* ph2_out = nullptr, uint64_t* mask_out = nullptr) {
   mics_ctx* ctx = st->ctx;
   mics_sync* sy = st->sync;
   const int p = sy->p, n = sy->n;
@@ -134,6 +136,11 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan) {
         ph2.add_group(g2, cb);
       }
   }
+  if (ph1_out) {
+    *ph1_out = ph1;
+    *ph2_out = ph2;
+    *mask_out = mask;
+  }
   // phase 1's exit barrier publishes every rank's stage-1 chunks before phase 2
   // reads them.  Phase 2 needs no barrier of its own: the next overwrite of a
   // gathered buffer (phase 1 of layer l+2) sits behind layer l+1's phase-1
@@ -141,6 +148,43 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan) {
   out.push_back(make_copy_launch(ctx, ph1, ctx->barrier(mask, 0, 1, chan), true));
   out.push_back(make_copy_launch(ctx, ph2, ctx->barrier(0, 0, 0), true));
   return out;
+}
+
+// tiles of `b` follow those of `a` in one launch
+CopyPlan concat_plans(const CopyPlan& a, const CopyPlan& b) {
+  CopyPlan c = a;
+  for (CopySeg sg : b.segs) {
+    sg.tile0 += a.tiles;
+    c.segs.push_back(sg);
+  }
+  c.tiles = a.tiles + b.tiles;
+  return c;
+}
+
+// Hierarchical gathers of one micro-step as 2L+1 launches: phase 1 of visit 0; then
+// phase 2 of visit i-1 together with phase 1 of visit i (one launch, phase 1's exit
+// barrier); then phase 2 of the last visit.  Safe: phase 2 of visit i-1 reads the node
+// peers' stage-1 chunks published by the previous launch's exit barrier; phase 1 of
+// visit i writes buffer (layer % 2), whose last readers (the peers' phase 2 two visits
+// back) finished before they reached that same barrier; when consecutive visits are
+// the same layer (the forward/backward turn) phase 1 rewrites identical bytes.
+void build_hier_merged(mics_step* st) {
+  mics_ctx* ctx = st->ctx;
+  const int L = st->cfg.nlayers;
+  std::vector<CopyPlan> p1(static_cast<size_t>(L)), p2(static_cast<size_t>(L));
+  uint64_t mask = 0;
+  for (int l = 0; l < L; ++l) {
+    std::vector<Launch> tmp = build_layer_ag(st, l, 0, &p1[size_t(l)], &p2[size_t(l)], &mask);
+    for (auto& x : tmp) x.release();
+  }
+  std::vector<int> visits;
+  for (int l = 0; l < L; ++l) visits.push_back(l);
+  for (int l = L; l-- > 0;) visits.push_back(l);
+  st->agm.push_back(make_copy_launch(ctx, p1[size_t(visits[0])], ctx->barrier(mask, 0, 1), true));
+  for (size_t i = 1; i < visits.size(); ++i)
+    st->agm.push_back(make_copy_launch(ctx, concat_plans(p2[size_t(visits[i - 1])], p1[size_t(visits[i])]),
+                                       ctx->barrier(mask, 0, 1), true));
+  st->agm.push_back(make_copy_launch(ctx, p2[size_t(visits.back())], ctx->barrier(0, 0, 0), true));
 }
 
 void enqueue_generate(mics_step* st, int t) {
@@ -345,6 +389,10 @@ void enqueue_fused_tail(mics_step* st) {
 // boundary, layer group g's first gather of the window waits for group g's Adam.
 void enqueue_gathers(mics_step* st, int t, bool side) {
   mics_ctx* ctx = st->ctx;
+  if (!st->agm.empty()) {  // merged hierarchical sequence (not with the pipelined boundary)
+    for (size_t i = 0; i < st->agm.size(); ++i) enqueue(ctx, st->agm[i], i == 0 && t == 0 ? 1 : -1);
+    return;
+  }
   bool first = true;
   size_t g = 0;
   for (size_t l = 0; l < st->layers.size(); ++l) {
@@ -855,6 +903,11 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     // the hook for overlapping the optimizer with a real forward pass.
     const char* penv = std::getenv("MICS_PIPELINE");
     st->pipelined = !cfg->alternative && !st->compute && penv && penv[0] == '1';
+    {
+      const char* me = std::getenv("MICS_HIER_MERGE");
+      if (cfg->hier_k > 0 && cfg->p > cfg->hier_k && !st->compute && !st->pipelined && !(me && me[0] == '0'))
+        build_hier_merged(st);
+    }
     if (st->pipelined) {
       st->gacc1 = alloc_sym(ctx, sy->shard.stride);
       MICS_CUDA(cudaMemsetAsync(ctx->base + st->gacc1.offset, 0, st->gacc1.stride * uint64_t(ctx->per), ctx->stream));
@@ -947,12 +1000,20 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     // kernels and algorithmic bytes of one step on this process (enqueue() skips empty launches)
     auto runs = [](const Launch& x) -> uint64_t { return (x.ndesc || x.bar.mask) ? 1 : 0; };
     mics_step_stats& S2 = st->stats;
-    for (auto& v : st->ag)
-      for (auto& x : v) {  // forward + backward pass, every micro-step
-        S2.ag_launches += 2 * uint64_t(cfg->s) * runs(x);
-        S2.ag_remote_bytes += 2 * uint64_t(cfg->s) * x.remote_bytes;
-        S2.ag_hbm_bytes += 2 * uint64_t(cfg->s) * x.hbm_bytes;
+    if (!st->agm.empty()) {
+      for (auto& x : st->agm) {  // one micro-step's merged forward + backward sequence
+        S2.ag_launches += uint64_t(cfg->s) * runs(x);
+        S2.ag_remote_bytes += uint64_t(cfg->s) * x.remote_bytes;
+        S2.ag_hbm_bytes += uint64_t(cfg->s) * x.hbm_bytes;
       }
+    } else {
+      for (auto& v : st->ag)
+        for (auto& x : v) {  // forward + backward pass, every micro-step
+          S2.ag_launches += 2 * uint64_t(cfg->s) * runs(x);
+          S2.ag_remote_bytes += 2 * uint64_t(cfg->s) * x.remote_bytes;
+          S2.ag_hbm_bytes += 2 * uint64_t(cfg->s) * x.hbm_bytes;
+        }
+    }
     for (size_t t = 0; t < st->micro.size(); ++t) {
       if ((st->tail || st->fused_tail) && t + 1 == st->micro.size()) continue;  // replaced by the tail launches
       for (auto& x : st->micro[t]) {

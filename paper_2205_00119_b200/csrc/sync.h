@@ -63,6 +63,10 @@ struct mics_step {
   mics_buf pbf16{}, master{}, m{}, v{}, gathered{}, grads{};
   uint64_t gathered_half = 0;                 // bytes of one gathered buffer
   std::vector<std::vector<mics::Launch>> ag;  // per layer: 1 launch (flat) or 2 (hierarchical)
+  // hierarchical gathers of one micro-step (forward 0..L-1, backward L-1..0) with phase 2
+  // of each visit merged into the launch of the next visit's phase 1: 2L+1 launches
+  // instead of 4L (MICS_HIER_MERGE=0 keeps the per-layer pairs)
+  std::vector<mics::Launch> agm;
   // per micro-step: the 2-hop reduce-scatter, or the alternative schedule's
   // all-n reduce-scatter + all-gather + owned-chunk accumulate
   std::vector<std::vector<mics::Launch>> micro;
