@@ -710,6 +710,12 @@ def run_mics(args, wl, rank, world, local):
                                     "frac_of_770": round(r["frac_nvlink_770"], 3),
                                     "nccl_busbw_GBps": round(r["nccl_busbw_GBps"], 1) if r["nccl_busbw_GBps"] else None}
                                    for r in pts]
+            big = [r for r in pts if r["bytes"] >= (1 << 30)]
+            line["collectives_summary"] = {
+                "points": len(pts),
+                "beats_nccl": sum(1 for r in pts if r["nccl_us"] and r["mics_us"] < r["nccl_us"]),
+                "min_frac_of_770_at_1GiB": round(min(r["frac_nvlink_770"] for r in big), 3) if big else None,
+                "p": sorted({r["p"] for r in pts})}
         except Exception as e:  # noqa: BLE001
             line["collectives"] = {"error": str(e)[:200]}
     if not args.no_compute and wl.hidden and args.schedule == "two_hop":
