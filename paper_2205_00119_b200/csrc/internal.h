@@ -157,9 +157,12 @@ struct BarrierArg {
   int entry;                  // signal + wait before any data access
   int exit;                   // last CTA signals + waits after all data access
   // Programmatic dependent launch: 1 = griddepcontrol.wait before touching memory
-  // (the kernel consumes its predecessor's results); 0 = independent of the
+  // (the kernel consumes its predecessor's results); 0 and 2 = independent of the
   // predecessor (barrier-free all-gathers of static shards): it waits only at its
   // end, so completion order — and every transitive dependency — is preserved.
+  // 0 ("fence") lets its successor start only once its own predecessor completed;
+  // 2 lets it start at once.  A chain with a fence every m gathers therefore has at
+  // most m+1 consecutive gathers in flight (step.cpp enqueue_gathers).
   int dep_first;
   // 1 = full system fences around every signal (the conservative protocol, kept
   // for A/B runs: MICS_BAR_STRICT=1); 0 = relaxed signals, see bar_entry/bar_exit
@@ -347,7 +350,7 @@ Launch make_adam_launch(mics_ctx* ctx, const AdamPlan& plan, const AdamScalars& 
 // jobs[i].ptrs is patched to point at ptrs[i] (2r entries) in the uploaded table
 Launch make_boundary_launch(mics_ctx* ctx, std::vector<BndJob> jobs, const std::vector<std::vector<const void*>>& ptrs,
                             const AdamScalars& sc, const BarrierArg& bar, bool persistent);
-// dep_first: -1 = as planned, 0/1 = override BarrierArg::dep_first for this launch
+// dep_first: -1 = as planned, 0/1/2 = override BarrierArg::dep_first for this launch
 void enqueue(mics_ctx* ctx, const Launch& l, int dep_first = -1, cudaStream_t stream = nullptr);
 
 void check_group(const mics_ctx* ctx, const int* ranks, int p);

@@ -54,14 +54,16 @@ __device__ __forceinline__ void st_vec(void* p, const uint4& v) { *reinterpret_c
 // A dependent kernel triggers its successor only once its own wait returned, so at
 // most one grid sits waiting behind a running one (triggering first let a whole
 // queue of replays become resident and cost 0.6 us per 1 MiB all-gather on 2 GPUs).
-// An independent kernel (the step's per-layer gathers) starts copying at once, but
-// one thread per CTA first waits for the predecessor and only then triggers: the
-// successor can therefore not start before this kernel's predecessor completed, so
-// at most two gathers are in flight and the two that share a double-buffered
-// destination (layers l and l+2) never write it concurrently.
+// An independent kernel (the step's per-layer gathers) starts copying at once.  A
+// fencing one (dep_first 0) has one thread per CTA wait for the predecessor before
+// triggering, so its successor cannot start before its predecessor completed: this
+// bounds how many gathers are in flight, and so which ones may share a destination
+// slot (step.cpp enqueue_gathers).
 __device__ __forceinline__ void pdl_begin(const BarrierArg& b) {
-  if (b.dep_first) {
+  if (b.dep_first == 1) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  } else if (b.dep_first == 2) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   } else if (threadIdx.x == 0) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -69,7 +71,7 @@ __device__ __forceinline__ void pdl_begin(const BarrierArg& b) {
   }
 }
 __device__ __forceinline__ void pdl_end(const BarrierArg& b) {
-  if (!b.dep_first) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (b.dep_first != 1) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- barrier

@@ -132,10 +132,10 @@ mics_ctx* create_ctx(const mics_init_args* a) {
       raise(MICS_CONFIG_ERROR, std::string("libmics is built for sm_100a (B200); device is ") + prop.name);
     c->nsm = prop.multiProcessorCount;
     c->occ_copy = resident_ctas(0, MICS_F32);
-    // Independent back-to-back gathers (the step's per-layer all-gathers): at most two
-    // are in flight (kernels.cu pdl_begin), so each needs enough CTAs to stream on its
-    // own.  C3 step AG phase, 1/2/3/4 CTAs per SM: N=1 12.09/11.26/10.31/10.32 ms,
-    // N=2 6.31/5.69/5.18/5.16 ms (profiles/r1/pdl_bound).
+    // Independent back-to-back gathers (the step's per-layer all-gathers): at most
+    // three are in flight (step.cpp enqueue_gathers), so each needs several CTAs per
+    // SM to stream.  C3 step AG phase at N=4, 1/2/3 CTAs per SM: 2.95/2.64/2.55 ms
+    // (profiles/r1/pdl_bound).
     c->occ_copy_indep = std::min(c->occ_copy, 3);
     if (const char* e = std::getenv("MICS_COPY_CTAS_PER_SM"))  // tuning knob
       c->occ_copy_indep = std::max(1, std::min(c->occ_copy, std::atoi(e)));

@@ -11,7 +11,7 @@
 //
 // Everything is planned once into device-resident descriptor tables (persistent
 // Launches) and replayed every step.  Layout per rank (symmetric arena):
-//   param_bf16 [shard]  master/m/v fp32 [shard]  gathered bf16 [2 x max layer]
+//   param_bf16 [shard]  master/m/v fp32 [shard]  gathered bf16 [2 or 3 x max layer]
 //   grads [s x grad_elems] (resident) or [grad_elems] (generated each micro-step)
 //   gradient accumulator = the mics_sync shard (fp32, padded to r*sub)
 // Layer l's chunk is ceil(E_l/p) rounded up to 8 elements, so every all-gather
@@ -78,14 +78,14 @@ void release(mics_step* st) {
   if (st->d_scalars) cudaFree(st->d_scalars);
 }
 
-// flat all-gather of layer l into gathered buffer (l % 2) of every local rank
+// flat all-gather of layer l into gathered slot (l % gather_slots) of every local rank
 std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan, CopyPlan* ph1_out = nullptr,
                                    CopyPlan* ph2_out = nullptr, uint64_t* mask_out = nullptr) {
   mics_ctx* ctx = st->ctx;
   mics_sync* sy = st->sync;
   const int p = sy->p, n = sy->n;
   const uint64_t c = sy->chunk[size_t(l)], cb = c * 2, soff = sy->shard_off[size_t(l)] * 2;
-  const uint64_t goff = uint64_t(l % 2) * st->gathered_half;
+  const uint64_t goff = uint64_t(l % st->gather_slots) * st->gathered_half;
   auto G = [&](int r, uint64_t pos) { return ctx->rank_ptr(st->gathered, r) + goff + pos * cb; };
   std::vector<Launch> out;
   const int k = st->cfg.hier_k;
@@ -104,7 +104,7 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan, CopyPlan* ph1
     // no barrier: shards are static between boundaries; the micro-step
     // reduce-scatter and Adam barriers order every write against these reads
     Launch l = make_copy_launch(ctx, plan, ctx->barrier(0, 0, 0), true);
-    l.bar.dep_first = 0;  // independent of the previous layer's gather: overlaps its tail (PDL)
+    l.bar.dep_first = 0;  // independent of the previous layer's gather (PDL); see enqueue_gathers
     l.grid = ctx->grid_for(plan.tiles, ctx->occ_copy_indep);
     out.push_back(l);
     return out;
@@ -387,6 +387,11 @@ void enqueue_fused_tail(mics_step* st) {
 // the boundary's Adam (which rewrote the shards it reads), so it waits for its
 // predecessor; the others only depend on static shards.  With the pipelined
 // boundary, layer group g's first gather of the window waits for group g's Adam.
+// In-flight bound: every (slots-1)-th gather is a fence (dep_first 0), so at most
+// `slots` consecutive gathers run at once.  Two gathers within `slots` positions
+// of each other either hit different slots (layers a != b mod slots) or carry the
+// same bytes (the same layer at the forward/backward turn): no write-after-write
+// race on a slot.
 void enqueue_gathers(mics_step* st, int t, bool side) {
   mics_ctx* ctx = st->ctx;
   if (!st->agm.empty()) {  // merged hierarchical sequence (not with the pipelined boundary)
@@ -395,6 +400,13 @@ void enqueue_gathers(mics_step* st, int t, bool side) {
   }
   bool first = true;
   size_t g = 0;
+  const int m = st->gather_slots - 1;
+  int pos = 0;
+  // only the flat gathers are independent; hierarchical launches keep their plan
+  auto dep = [&](const Launch& x) {
+    if (x.bar.dep_first != 0 || x.bar.mask) return -1;
+    return pos++ % m == m - 1 ? 0 : 2;
+  };
   for (size_t l = 0; l < st->layers.size(); ++l) {
     if (st->pipelined && side && t == 0 && g < st->group_first_layer.size() &&
         int(l) == st->group_first_layer[g]) {
@@ -402,12 +414,13 @@ void enqueue_gathers(mics_step* st, int t, bool side) {
       ++g;
     }
     for (auto& x : st->ag[l]) {
-      enqueue(ctx, x, first && t == 0 ? 1 : -1);
+      const int d = dep(x);
+      enqueue(ctx, x, first && t == 0 ? 1 : d);
       first = false;
     }
   }
   for (size_t l = st->layers.size(); l-- > 0;)
-    for (auto& x : st->ag[l]) enqueue(ctx, x);
+    for (auto& x : st->ag[l]) enqueue(ctx, x, dep(x));
 }
 
 void enqueue_sync(mics_step* st, int t, bool side) {
@@ -494,7 +507,7 @@ void setup_compute(mics_step* st) {
         if (!ctx->local(r)) continue;
         const int rows = int(st->rows[size_t(l)]);
         const uint64_t ldy = st->ldy[size_t(l)];
-        char* W = ctx->rank_ptr(st->gathered, r) + uint64_t(l % 2) * st->gathered_half;
+        char* W = ctx->rank_ptr(st->gathered, r) + uint64_t(l % st->gather_slots) * st->gathered_half;
         char* X = ctx->rank_ptr(st->x, r) + uint64_t(t) * xe * 2;
         char* Y = ctx->rank_ptr(st->y, r) + st->yoff[size_t(l)] * 2;
         char* dX = ctx->rank_ptr(st->dx, r);
@@ -524,7 +537,7 @@ void setup_compute(mics_step* st) {
       for (int r = 0; r < ctx->n; ++r) {
         if (!ctx->local(r)) continue;
         const int g = r / cfg.p;
-        char* G = ctx->rank_ptr(st->gathered, r) + uint64_t(l % 2) * st->gathered_half;
+        char* G = ctx->rank_ptr(st->gathered, r) + uint64_t(l % st->gather_slots) * st->gathered_half;
         for (int i = 0; i < cfg.p; ++i) v.push_back({G + uint64_t(i) * cb, ctx->rank_ptr(st->pbf16, g * cfg.p + i) + soff, cb});
       }
       st->ce.push_back(std::move(v));
@@ -849,7 +862,12 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     st->master = alloc_sym(ctx, S * 4);
     st->m = alloc_sym(ctx, S * 4);
     st->v = alloc_sym(ctx, S * 4);
-    st->gathered = alloc_sym(ctx, 2 * st->gathered_half);
+    // Without compute nothing consumes a gather, so up to three run concurrently
+    // (enqueue_gathers): three slots.  With compute a layer's GEMMs release its slot.
+    st->gather_slots = cfg->compute ? 2 : 3;
+    if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)
+      st->gather_slots = std::max(2, std::min(4, std::atoi(e)));
+    st->gathered = alloc_sym(ctx, uint64_t(st->gather_slots) * st->gathered_half);
     // gradient slots: s resident sets, 1 regenerated per micro-step, or with compute 2
     // (the GEMMs of micro-step t+1 write one while the reduce-scatter of t reads the other)
     st->compute = cfg->compute != 0;

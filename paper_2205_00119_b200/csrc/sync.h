@@ -61,7 +61,8 @@ struct mics_step {
   std::vector<uint64_t> layers;
   mics_sync* sync = nullptr;
   mics_buf pbf16{}, master{}, m{}, v{}, gathered{}, grads{};
-  uint64_t gathered_half = 0;                 // bytes of one gathered buffer
+  uint64_t gathered_half = 0;                 // bytes of one gathered buffer (slot)
+  int gather_slots = 2;                       // layer l gathers into slot l % gather_slots
   std::vector<std::vector<mics::Launch>> ag;  // per layer: 1 launch (flat) or 2 (hierarchical)
   // hierarchical gathers of one micro-step (forward 0..L-1, backward L-1..0) with phase 2
   // of each visit merged into the launch of the next visit's phase 1: 2L+1 launches
