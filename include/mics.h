@@ -295,8 +295,8 @@ mics_status mics_generate(mics_ctx* ctx, mics_buf buf, int rank, uint64_t off, m
  *              per-layer parameter all-gather (bwd, L-1..0),
  *              coalesced gradient reduce-scatter of all layers (2-hop hop 1);
  *   boundary:  replication-group all-reduce fused with sharded fp32 Adam (hop 2).
- * Parameters are bf16 shards (+ fp32 master, m, v), gathered into a double
- * buffer; gradients are pre-generated (resident) or produced per micro-step by
+ * Parameters are bf16 shards (+ fp32 master, m, v), gathered into rotating
+ * per-layer slots (3, or 2 with compute); gradients are pre-generated (resident) or produced per micro-step by
  * the K6 generator (models backward's gradient write). */
 typedef struct {
   int p, s, nlayers;
