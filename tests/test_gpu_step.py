@@ -89,16 +89,18 @@ def test_step_matches_cpu_restatement(oracle, alternative, grad_dtype, hier_k, p
         assert np.array_equal(u32(eng.d2h(bufs["exp_avg"], r, S)), u32(wm)), r
         assert np.array_equal(u32(eng.d2h(bufs["exp_avg_sq"], r, S)), u32(wv)), r
         assert np.array_equal(eng.d2h(bufs["param_bf16"], r, S, "bf16"), wb), r
-    # the last gathered layer (layer 0, backward pass) holds the pre-update bf16 params of the group
-    ln0, c0, so0, _ = segs[0]
-    for r in range(n):
-        g = r // p
-        got = eng.d2h(bufs["gathered"], r, p * c0, "bf16")
-        for i in range(p):
-            src = init[g * p + i][so0:so0 + c0]
-            want_bf = oracle.f32_to_bf16(src)
-            assert np.array_equal(got[i * c0:(i + 1) * c0], want_bf), (r, i)
+    # the last gathers (backward pass, layers 2, 1, 0) left layer l in slot l mod 3
+    # (csrc/step.cpp gather_slots): the pre-update bf16 params of the group
     stats = step.stats()
+    half = (stats.gathered_max_bytes + 255) // 256 * 256
+    for l in range(min(3, len(segs))):
+        _, cl, sol, _ = segs[l]
+        for r in range(n):
+            g = r // p
+            got = eng.d2h(bufs["gathered"], r, p * cl, "bf16", off=(l % 3) * half)
+            for i in range(p):
+                want_bf = oracle.f32_to_bf16(init[g * p + i][sol:sol + cl])
+                assert np.array_equal(got[i * cl:(i + 1) * cl], want_bf), (l, r, i)
     # flat: one launch per layer visit; hierarchical: 2L+1 merged launches per micro-step
     want_ag = s * (2 * len(layers) + 1) if hier_k and p > hier_k else 2 * s * len(layers)
     assert stats.launches > 0 and stats.ag_launches == want_ag
