@@ -866,7 +866,7 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     // (enqueue_gathers): three slots.  With compute a layer's GEMMs release its slot.
     st->gather_slots = cfg->compute ? 2 : 3;
     if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)
-      st->gather_slots = std::max(2, std::min(4, std::atoi(e)));
+      st->gather_slots = std::max(2, std::min(8, std::atoi(e)));
     st->gathered = alloc_sym(ctx, uint64_t(st->gather_slots) * st->gathered_half);
     // gradient slots: s resident sets, 1 regenerated per micro-step, or with compute 2
     // (the GEMMs of micro-step t+1 write one while the reduce-scatter of t reads the other)
