@@ -167,6 +167,12 @@ struct BarrierArg {
   // 1 = full system fences around every signal (the conservative protocol, kept
   // for A/B runs: MICS_BAR_STRICT=1); 0 = relaxed signals, see bar_entry/bar_exit
   int strict;
+  // Gather-slot ordering instead of fences (step.cpp enqueue_gathers, MICS_GATHER_CTR):
+  // before writing, wait until *slot_ctr >= slot_target (every earlier gather into
+  // this destination slot completed); the last CTA (slot_ticket) then bumps *slot_ctr.
+  uint64_t* slot_ctr = nullptr;
+  uint64_t slot_target = 0;
+  unsigned* slot_ticket = nullptr;
 };
 
 // --------------------------------------------------------------------------

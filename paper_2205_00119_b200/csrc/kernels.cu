@@ -146,6 +146,36 @@ __device__ void bar_exit(const BarrierArg& b) {
   }
 }
 
+// Gather-slot ordering (see BarrierArg::slot_ctr).  Every earlier gather into the slot
+// is already resident or finished (each triggers its successor at entry), so the
+// wait cannot block one of them; the counter is bumped after this gather's last
+// store, before its end-of-kernel wait for its predecessor.
+__device__ __forceinline__ void slot_wait(const BarrierArg& b) {
+  if (!b.slot_ctr) return;
+  if (threadIdx.x == 0) {
+    uint64_t v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(b.slot_ctr) : "memory");
+      if (v >= b.slot_target) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void slot_done(const BarrierArg& b) {
+  if (!b.slot_ctr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(b.slot_ticket, 1u) == gridDim.x - 1) {  // last CTA: every store of the grid is done
+      *b.slot_ticket = 0;
+      __threadfence();
+      atomicAdd(reinterpret_cast<unsigned long long*>(b.slot_ctr), 1ull);
+    }
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ int find_desc(const T* __restrict__ d, int n, uint32_t tile) {
   int lo = 0, hi = n - 1;
@@ -170,6 +200,7 @@ __global__ void __launch_bounds__(kThreads) k_copy(const CopySeg* __restrict__ g
   const CopySeg* segs = staged ? reinterpret_cast<const CopySeg*>(smem) : gsegs;
   pdl_begin(bar);
   bar_entry(bar);
+  slot_wait(bar);
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     // last segment whose group starts at or before `tile`; stripe groups interleave their tiles
     int idx = find_desc(segs, nseg, tile);
@@ -218,6 +249,7 @@ __global__ void __launch_bounds__(kThreads) k_copy(const CopySeg* __restrict__ g
       }
     }
   }
+  slot_done(bar);
   bar_exit(bar);
   pdl_end(bar);
 }

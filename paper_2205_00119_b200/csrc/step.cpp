@@ -76,6 +76,8 @@ void release(mics_step* st) {
   if (st->cs) cudaStreamDestroy(st->cs);
   if (st->copy_stream) cudaStreamDestroy(st->copy_stream);
   if (st->d_scalars) cudaFree(st->d_scalars);
+  if (st->d_slot_ctr) cudaFree(st->d_slot_ctr);
+  if (st->d_slot_tickets) cudaFree(st->d_slot_tickets);
 }
 
 // flat all-gather of layer l into gathered slot (l % gather_slots) of every local rank
@@ -407,6 +409,27 @@ void enqueue_gathers(mics_step* st, int t, bool side) {
     if (x.bar.dep_first != 0 || x.bar.mask) return -1;
     return pos++ % m == m - 1 ? 0 : 2;
   };
+  // MICS_GATHER_CTR: no fences; a gather waits on the device for every earlier
+  // gather into its slot (counters zeroed at the start of each step, in stream order,
+  // so host targets and device counts always agree)
+  if (st->gather_ctr && t == 0) {
+    MICS_CUDA(cudaMemsetAsync(st->d_slot_ctr, 0, 8 * sizeof(uint64_t), ctx->stream));
+    std::fill(st->slot_host.begin(), st->slot_host.end(), 0);
+  }
+  const int L = int(st->layers.size());
+  auto go = [&](const Launch& x, int l, int dir, int forced) {
+    if (!st->gather_ctr || x.bar.dep_first != 0 || x.bar.mask || x.ndesc == 0) {
+      const int d = dep(x);
+      enqueue(ctx, x, forced >= 0 ? forced : d);
+      return;
+    }
+    const int s = l % st->gather_slots;
+    Launch y = x;
+    y.bar.slot_ctr = st->d_slot_ctr + s;
+    y.bar.slot_target = st->slot_host[size_t(s)]++;
+    y.bar.slot_ticket = st->d_slot_tickets + dir * L + l;
+    enqueue(ctx, y, forced >= 0 ? forced : 2);
+  };
   for (size_t l = 0; l < st->layers.size(); ++l) {
     if (st->pipelined && side && t == 0 && g < st->group_first_layer.size() &&
         int(l) == st->group_first_layer[g]) {
@@ -414,13 +437,12 @@ void enqueue_gathers(mics_step* st, int t, bool side) {
       ++g;
     }
     for (auto& x : st->ag[l]) {
-      const int d = dep(x);
-      enqueue(ctx, x, first && t == 0 ? 1 : d);
+      go(x, int(l), 0, first && t == 0 ? 1 : -1);
       first = false;
     }
   }
   for (size_t l = st->layers.size(); l-- > 0;)
-    for (auto& x : st->ag[l]) enqueue(ctx, x, dep(x));
+    for (auto& x : st->ag[l]) go(x, int(l), 1, -1);
 }
 
 void enqueue_sync(mics_step* st, int t, bool side) {
@@ -868,6 +890,14 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)
       st->gather_slots = std::max(2, std::min(8, std::atoi(e)));
     st->gathered = alloc_sym(ctx, uint64_t(st->gather_slots) * st->gathered_half);
+    if (const char* e = std::getenv("MICS_GATHER_CTR"); e && !cfg->compute) st->gather_ctr = std::atoi(e) != 0;
+    if (st->gather_ctr) {
+      MICS_CUDA(cudaMalloc(&st->d_slot_ctr, 8 * sizeof(uint64_t)));
+      MICS_CUDA(cudaMemset(st->d_slot_ctr, 0, 8 * sizeof(uint64_t)));
+      MICS_CUDA(cudaMalloc(&st->d_slot_tickets, 2 * size_t(cfg->nlayers) * sizeof(unsigned)));
+      MICS_CUDA(cudaMemset(st->d_slot_tickets, 0, 2 * size_t(cfg->nlayers) * sizeof(unsigned)));
+      st->slot_host.assign(size_t(st->gather_slots), 0);
+    }
     // gradient slots: s resident sets, 1 regenerated per micro-step, or with compute 2
     // (the GEMMs of micro-step t+1 write one while the reduce-scatter of t reads the other)
     st->compute = cfg->compute != 0;

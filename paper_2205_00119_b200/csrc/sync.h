@@ -63,6 +63,11 @@ struct mics_step {
   mics_buf pbf16{}, master{}, m{}, v{}, gathered{}, grads{};
   uint64_t gathered_half = 0;                 // bytes of one gathered buffer (slot)
   int gather_slots = 2;                       // layer l gathers into slot l % gather_slots
+  // slot ordering by device counters instead of fences (MICS_GATHER_CTR; comm-only step)
+  bool gather_ctr = false;
+  uint64_t* d_slot_ctr = nullptr;             // [gather_slots] completed gathers per slot this step
+  unsigned* d_slot_tickets = nullptr;         // [2 L] CTA tickets per (direction, layer) gather
+  std::vector<uint64_t> slot_host;            // gathers enqueued per slot this step
   std::vector<std::vector<mics::Launch>> ag;  // per layer: 1 launch (flat) or 2 (hierarchical)
   // hierarchical gathers of one micro-step (forward 0..L-1, backward L-1..0) with phase 2
   // of each visit merged into the launch of the next visit's phase 1: 2L+1 launches
