@@ -413,7 +413,7 @@ void enqueue_gathers(mics_step* st, int t, bool side) {
   // gather into its slot (counters zeroed at the start of each step, in stream order,
   // so host targets and device counts always agree)
   if (st->gather_ctr && t == 0) {
-    MICS_CUDA(cudaMemsetAsync(st->d_slot_ctr, 0, 8 * sizeof(uint64_t), ctx->stream));
+    MICS_CUDA(cudaMemsetAsync(st->d_slot_ctr, 0, kMaxGatherSlots * sizeof(uint64_t), ctx->stream));
     std::fill(st->slot_host.begin(), st->slot_host.end(), 0);
   }
   const int L = int(st->layers.size());
@@ -888,12 +888,12 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     // (enqueue_gathers): three slots.  With compute a layer's GEMMs release its slot.
     st->gather_slots = cfg->compute ? 2 : 3;
     if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)
-      st->gather_slots = std::max(2, std::min(8, std::atoi(e)));
+      st->gather_slots = std::max(2, std::min(kMaxGatherSlots, std::atoi(e)));
     st->gathered = alloc_sym(ctx, uint64_t(st->gather_slots) * st->gathered_half);
     if (const char* e = std::getenv("MICS_GATHER_CTR"); e && !cfg->compute) st->gather_ctr = std::atoi(e) != 0;
     if (st->gather_ctr) {
-      MICS_CUDA(cudaMalloc(&st->d_slot_ctr, 8 * sizeof(uint64_t)));
-      MICS_CUDA(cudaMemset(st->d_slot_ctr, 0, 8 * sizeof(uint64_t)));
+      MICS_CUDA(cudaMalloc(&st->d_slot_ctr, kMaxGatherSlots * sizeof(uint64_t)));
+      MICS_CUDA(cudaMemset(st->d_slot_ctr, 0, kMaxGatherSlots * sizeof(uint64_t)));
       MICS_CUDA(cudaMalloc(&st->d_slot_tickets, 2 * size_t(cfg->nlayers) * sizeof(unsigned)));
       MICS_CUDA(cudaMemset(st->d_slot_tickets, 0, 2 * size_t(cfg->nlayers) * sizeof(unsigned)));
       st->slot_host.assign(size_t(st->gather_slots), 0);

@@ -55,6 +55,8 @@ void alt_boundary(mics_sync* st);
 }  // namespace mics
 
 // MiCS step driver state (step.cpp)
+constexpr int kMaxGatherSlots = 8;  // mics_step::gather_slots upper bound (MICS_GATHER_SLOTS)
+
 struct mics_step {
   mics_ctx* ctx = nullptr;
   mics_step_cfg cfg{};
