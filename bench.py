@@ -162,8 +162,6 @@ def arena_bytes(wl, per, resident, n=N_RANKS, alternative=False, compute=None):
             per_rank += p * S * szg
     if alternative:  # all-n reduce-scatter scratch: n slices of ceil(p*chunk/n) per layer
         per_rank += sum(-(-p * c // n) * n for c in chunks) * 4
-    elif os.environ.get("MICS_PIPELINE") == "1":  # pipelined boundary: second gradient accumulator
-        per_rank += r * (sub + 131072) * 4
     return per * (per_rank + 8 * 4096) + (256 << 20)
 
 
@@ -209,68 +207,127 @@ def ncu_traffic(workload, n_gpus, phase):
     return ent["dram_bytes_per_launch"] if ent else None
 
 
+# ----------------------------------------------------------------------------- config (both arms)
+def grad_elems(wl):
+    """Padded gradient elements per rank (csrc/step.cpp: chunk = ceil(E/p) rounded to 8)."""
+    return sum(((e + wl.p - 1) // wl.p + 7) // 8 * 8 * wl.p for e in wl.layer_params)
+
+
+def config_for(wl, args, world):
+    """The workload description both arms print (the driver compares them key by key):
+    pure function of the workload and the command line."""
+    szg = 2 if wl.grad_dtype == "bf16" else 4
+    n = args.ranks
+    return {"workload": wl.name, "n_ranks": n, "ranks_per_gpu": n // world, "p": wl.p, "s": wl.s,
+            "micro_batch": MICRO_BATCH, "params": wl.params, "grad_dtype": wl.grad_dtype,
+            "param_dtype": "bf16 (fp32 master, m, v)", "hierarchical_k": wl.hier_k,
+            "l2": "inputs larger than L2 (gradient sets of %.2f GB/rank)" % (wl.s * grad_elems(wl) * szg / 1e9),
+            "parallelism": f"MiCS p={wl.p} x {n // wl.p} replicas", "schedule": args.schedule}
+
+
 # ----------------------------------------------------------------------------- CPU baseline (reference)
-def cpu_baseline(wl, threads):
-    """The reference's own step functions (oracle/_ref) on a bounded sample: ONE
-    full-size transformer block (or layer) of the workload, extrapolated to the
-    whole model by parameter count."""
+def ref_layer_seconds(wl, threads, size, port=None):
+    """Wall seconds of the reference's own step functions (oracle/_ref, compiled from
+    the unmodified sources) over ONE layer of `size` parameters for all n ranks:
+    per-layer all_gather fwd + bwd in every partition group, two_hop_micro_step x s,
+    two_hop_boundary, plus the Adam loop the reference lacks (oracle/ref_shim.cpp
+    ref_step_sample).  Falls back to the plain-C restatement (`port`) when the
+    reference was not built.  Returns (seconds, kind, threads used)."""
     import ctypes as C
     from oracle.oracle import REF_SO, RefLib
-    sample = [max(wl.layer_params[1:] or wl.layer_params)]
     if RefLib.available():
         lib = C.CDLL(REF_SO)
         lib.ref_step_sample.restype = C.c_double
-        arr = (C.c_uint64 * 1)(*sample)
-        sec = lib.ref_step_sample(threads, wl.n, wl.p, wl.s, 1, arr, 1)
-        kind = "reference"
-    else:  # the plain-C restatement, timed the same way (AG + 2-hop + Adam)
-        import numpy as np
-        from oracle.oracle import Oracle
-        ora = Oracle()
-        n, p, s, ln = wl.n, wl.p, wl.s, sample[0]
-        g = np.random.default_rng(0).standard_normal((s, n, ln)).astype(np.float32)
-        sh = np.zeros((p, (ln + p - 1) // p * 2), np.uint8)
-        t0 = time.perf_counter()
-        for _ in range(s):
-            for _ in range(2 * n // p):
-                ora.all_gather(sh)
-        out, _, _ = ora.two_hop(g, n, p, "f32")
-        for r in range(n):
-            ora.adam(np.zeros(out.shape[1]), np.zeros(out.shape[1]), np.zeros(out.shape[1]), out[r], 1e-4, 0.9,
-                     0.999, 1e-8, 0.0, 1, 1.0 / (n * s))
-        sec = time.perf_counter() - t0
-        kind, threads = "port", 1
-    if sec <= 0:
+        arr = (C.c_uint64 * 1)(size)
+        return lib.ref_step_sample(threads, wl.n, wl.p, wl.s, 1, arr, 1), "reference", threads
+    import numpy as np
+    from oracle.oracle import Oracle
+    ora = port or Oracle()
+    n, p, s, ln = wl.n, wl.p, wl.s, size
+    g = np.random.default_rng(0).standard_normal((s, n, ln)).astype(np.float32)
+    sh = np.zeros((p, (ln + p - 1) // p * 2), np.uint8)
+    t0 = time.perf_counter()
+    for _ in range(s):
+        for _ in range(2 * n // p):
+            ora.all_gather(sh)
+    out, _, _ = ora.two_hop(g, n, p, "f32")
+    for r in range(n):
+        ora.adam(np.zeros(out.shape[1]), np.zeros(out.shape[1]), np.zeros(out.shape[1]), out[r], 1e-4, 0.9,
+                 0.999, 1e-8, 0.0, 1, 1.0 / (n * s))
+    return time.perf_counter() - t0, "port", 1
+
+
+def layer_sizes(wl):
+    """{size: count} over the workload's layers; the most frequent size is the per-step sample."""
+    sizes = {}
+    for e in wl.layer_params:
+        sizes[e] = sizes.get(e, 0) + 1
+    block = max(sizes, key=lambda e: (sizes[e], e))
+    return sizes, block
+
+
+def cpu_baseline(wl, threads, calib=None):
+    """The reference's CPU step for the whole model, assembled from per-layer timings:
+    every distinct layer size is timed once at full size (C3: the 31.8M-parameter
+    embedding and one 12.6M-parameter block, all 8 ranks), and the step time is the
+    sum over the model's layers — the reference's step cost is a sum of independent
+    per-layer collectives plus element-wise 2-hop / Adam work."""
+    sizes, block = layer_sizes(wl)
+    t = dict(calib or {})
+    kind = "reference"
+    for e in sizes:
+        if e not in t:
+            t[e], kind, threads = ref_layer_seconds(wl, threads, e)
+    if any(v <= 0 for v in t.values()):
         return None
-    scale = wl.params / sample[0]
-    step_s = sec * scale
+    step_s = sum(t[e] * c for e, c in sizes.items())
+    timed = ", ".join(f"{c} x {e:,}-param layer at {t[e]:.2f} s" for e, c in sizes.items())
     return {"value": N_RANKS * MICRO_BATCH * wl.s / step_s, "unit": "samples/s", "cores": threads, "kind": kind,
-            "sample": f"1 of {len(wl.layer_params)} layers at full size ({sample[0]:,} params, all {wl.n} ranks, "
-                      f"p={wl.p}, s={wl.s}: per-layer all_gather fwd+bwd, two_hop_micro_step x s, "
-                      f"two_hop_boundary, Adam loop) = {sec:.2f} s, extrapolated x{scale:.1f} by parameter count",
-            "step_seconds": step_s}
+            "sample": f"each distinct layer size timed once at full size (all {wl.n} ranks, p={wl.p}, s={wl.s}: "
+                      f"per-layer all_gather fwd+bwd, two_hop_micro_step x s, two_hop_boundary, Adam loop); "
+                      f"step = {timed} = {step_s:.1f} s (sum over layers)",
+            "step_seconds": step_s, "extrapolated": len(wl.layer_params) > len(sizes), "layer_seconds": t}
 
 
-def run_reference(args, wl, rank):
+def run_reference(args, wl, rank, world):
+    """`--impl reference`: the reference's own CPU implementation (oracle/_ref: the
+    unmodified sdpsim sources) on the box's host cores, same workload and config.
+    The full C3 step takes ~70 s on 16 cores, so each timed step is a bounded sample:
+    one full-size transformer block for all 8 ranks (the other layer sizes are
+    timed once up front); `value` is the whole-model step assembled from them
+    (`extrapolated`), `ms_per_step` the sample actually timed per step."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    vals = []
+    sizes, block = layer_sizes(wl)
+    calib = {}
+    for e in sizes:
+        if e != block:
+            calib[e], kind, threads = ref_layer_seconds(wl, threads, e)
+    samples = []
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(wl, threads)
-        if cb is None:
+        sec, kind, threads = ref_layer_seconds(wl, threads, block)
+        if sec <= 0:
             print(json.dumps({"impl": "reference", "unavailable": "reference step sample failed"}))
             return
         if i >= args.warmup:
-            vals.append(cb)
-    v = statistics.median([c["value"] for c in vals])
+            samples.append(sec)
+    t_block = statistics.median(samples)
+    cb = cpu_baseline(wl, threads, calib | {block: t_block})
+    v = cb["value"]
     line = {"impl": "reference", "metric": "MiCS step samples/s", "value": v, "unit": "samples/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000 * statistics.median([c["step_seconds"] for c in vals]),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": wl.name, "n_ranks": wl.n, "p": wl.p, "s": wl.s,
-                                            "micro_batch": MICRO_BATCH},
-            "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "samples/s"},
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * t_block, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic", "config": config_for(wl, args, world),
+            "extrapolated": True,
+            "extrapolation": {"timed_per_step": f"one {block:,}-parameter layer, all {wl.n} ranks",
+                              "sample_ms_per_step": 1000 * t_block,
+                              "full_step_ms": 1000 * cb["step_seconds"],
+                              "other_layers_timed_once_s": calib,
+                              "formula": "step = sum over layers of the timed per-layer seconds; "
+                                         "value = n * micro_batch * s / step"},
+            "cpu_baseline": {"kind": cb["kind"], "cores": cb["cores"], "sample": cb["sample"], "value": v,
+                             "unit": "samples/s"},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -663,9 +720,14 @@ def run_mics(args, wl, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(wl, os.cpu_count() or 1)
         if cpu and cpu["kind"] == "reference" and (os.cpu_count() or 1) > 1:
-            one = cpu_baseline(wl, 1)  # the reference's engine at 1 thread and at nproc
-            if one:
-                cpu["single_thread"] = {"value": one["value"], "cores": 1, "step_seconds": one["step_seconds"]}
+            # the reference's engine at 1 thread too (the block only, scaled by
+            # the nproc run's per-layer ratio to keep the bench within minutes)
+            sizes, block = layer_sizes(wl)
+            t1, _, _ = ref_layer_seconds(wl, 1, block)
+            if t1 > 0:
+                step1 = cpu["step_seconds"] * t1 / cpu["layer_seconds"][block]
+                cpu["single_thread"] = {"value": N_RANKS * MICRO_BATCH * wl.s / step1, "cores": 1,
+                                        "step_seconds": step1, "block_seconds": t1}
 
     nccl = None
     if world > 1 and per == 1:
@@ -678,14 +740,10 @@ def run_mics(args, wl, rank, world, local):
         "metric": "MiCS step samples/s", "value": value, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": wl.name, "n_ranks": n, "ranks_per_gpu": per, "p": wl.p, "s": wl.s,
-                   "micro_batch": MICRO_BATCH, "params": wl.params, "grad_dtype": wl.grad_dtype,
-                   "param_dtype": "bf16 (fp32 master, m, v)", "hierarchical_k": wl.hier_k,
-                   "grads": "resident in HBM (generated before timing)" if resident else "generated in-step (K6)",
-                   "l2": "inputs larger than L2 (gradient sets of %.2f GB/rank)" % (s * stats.grad_elems * szg / 1e9),
-                   "parallelism": f"MiCS p={wl.p} x {n // wl.p} replicas", "schedule": args.schedule,
-                   "launch": "stream" if os.environ.get("MICS_GRAPH") == "0" or os.environ.get("MICS_PIPELINE") == "1"
-                             else "CUDA graph replay (one graph per step)"},
+        "config": config_for(wl, args, world),
+        "run": {"grads": "resident in HBM (generated before timing)" if resident else "generated in-step (K6)",
+                "launch": "stream" if os.environ.get("MICS_GRAPH") == "0"
+                          else "CUDA graph replay (one graph per step)"},
         "roofline": roof,
         "phases_ms": {k: v[0] for k, v in phases.items()},
         "per_rank_bytes": {"allgather_in": stats.ag_bytes_in, "reducescatter_in": stats.rs_bytes_in,
@@ -758,13 +816,8 @@ def main():
     global GLOO
     args = parse()
     rank, world, local = env()
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group(backend="cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
-        GLOO = dist.new_group(backend="gloo")
-    from paper_2205_00119_b200.step import workloads
+    # pure Python: the reference arm never loads libmics (the package __init__ is lazy)
+    from paper_2205_00119_b200.workloads import workloads
     wl = workloads()[args.workload]
     if args.p or args.micro_steps:
         import dataclasses
@@ -776,11 +829,18 @@ def main():
             wl.name += f", p={wl.p}"
         if f"s={wl.s}" not in wl.name:
             wl.name += f", s={wl.s}"
+    if args.impl == "reference":  # CPU only: no process group, ranks > 0 exit without work
+        run_reference(args, wl, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group(backend="cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
+        GLOO = dist.new_group(backend="gloo")
     if args.sweep:
         from tools.sweep import run_sweep
         run_sweep(args, rank, world, local)
-    elif args.impl == "reference":
-        run_reference(args, wl, rank)
     elif args.compute:
         run_compute_headline(args, wl, rank, world, local)
     else:

@@ -202,53 +202,6 @@ Launch make_adam_launch(mics_ctx* ctx, const AdamPlan& plan, const AdamScalars& 
   return l;
 }
 
-Launch make_boundary_launch(mics_ctx* ctx, std::vector<BndJob> jobs, const std::vector<std::vector<const void*>>& ptrs,
-                            const AdamScalars& sc, const BarrierArg& bar, bool persistent) {
-  Launch l;
-  l.kind = Launch::BOUNDARY;
-  l.ndesc = int(jobs.size());
-  uint32_t rs = 0, ad = 0;
-  for (auto& J : jobs) {
-    J.rs_tile0 = rs;
-    rs += J.nblk;
-    const uint32_t n_ad = uint32_t(ceil_div(J.elems, kBndBlock));
-    J.ad_tile0 = ad;
-    ad += n_ad;
-    for (uint32_t q = 0; q < J.r; ++q) {  // reduce-scatter: r sources for the own slice; Adam: one owner per slice
-      const bool local = ctx->is_local_ptr(ptrs[&J - jobs.data()][q]);
-      (local ? l.hbm_bytes : l.remote_bytes) += J.sub * 4;
-      const uint64_t lo = std::min<uint64_t>(q * J.sub, J.elems), hi = std::min<uint64_t>((q + 1) * J.sub, J.elems);
-      (local ? l.hbm_bytes : l.remote_bytes) += (hi - lo) * 4;
-    }
-    l.hbm_bytes += J.sub * 4 + J.elems * (24 + (J.pbf16 ? 2 : 0) + (J.gout ? 4 : 0));
-  }
-  l.rs_tiles = rs;
-  l.ntiles = rs + ad;
-  // every CTA must be resident: Adam tiles wait for flags that other CTAs' reduce tiles publish
-  l.grid = int(std::min<uint64_t>(l.ntiles ? l.ntiles : 1, uint64_t(ctx->nsm) * uint64_t(ctx->occ_bnd)));
-  l.adam = sc;
-  l.bar = bar;
-  if (l.ndesc) {
-    // same blob layout as upload_jobs: jobs, then each job's pointer array
-    uint64_t nptr = 0;
-    for (const auto& v : ptrs) nptr += v.size();
-    const uint64_t jbytes = round_up(sizeof(BndJob) * jobs.size(), 16);
-    const uint64_t bytes = round_up(jbytes + nptr * sizeof(void*), 16);
-    char* d = static_cast<char*>(table_memory(ctx, bytes, persistent));
-    std::vector<char> blob(bytes);
-    const void** pp = reinterpret_cast<const void**>(blob.data() + jbytes);
-    uint64_t k = 0;
-    for (size_t i = 0; i < jobs.size(); ++i) {
-      jobs[i].ptrs = reinterpret_cast<const void* const*>(d + jbytes + k * sizeof(void*));
-      for (const void* s : ptrs[i]) pp[k++] = s;
-    }
-    std::memcpy(blob.data(), jobs.data(), sizeof(BndJob) * jobs.size());
-    table_upload(ctx, d, blob.data(), bytes, persistent);
-    l.d_desc = d;
-  }
-  return l;
-}
-
 void enqueue(mics_ctx* ctx, const Launch& l, int dep_first, cudaStream_t stream) {
   cudaStream_t st = stream ? stream : ctx->stream;
   // A launch without local work still runs (one CTA) when it carries a barrier:
@@ -274,10 +227,6 @@ void enqueue(mics_ctx* ctx, const Launch& l, int dep_first, cudaStream_t stream)
     case Launch::TAIL:
       launch_tail(st, l.in_t, l.tail_r, l.tail_p, static_cast<const TailJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid,
                   l.adam, l.dyn, l.mode, bar);
-      break;
-    case Launch::BOUNDARY:
-      launch_boundary(st, static_cast<const BndJob*>(l.d_desc), l.ndesc, l.rs_tiles, l.ntiles, l.grid,
-                      l.adam, l.epoch, l.dyn, bar);
       break;
   }
   ctx->launches++;

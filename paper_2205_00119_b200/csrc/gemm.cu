@@ -11,19 +11,24 @@
 //   dgrad    dX = dY · W   A = dY (K-major), B = W  (N-major)
 //   wgrad    dW = dYᵀ · X  A = dY (M-major), B = X  (N-major)
 //
-// Structure (one CTA per SM, CTA pairs as thread-block clusters, persistent over
-// pairs of 128x256 output tiles that share their B tile):
-//   warp 0      TMA producer: 128B-swizzled boxes of A and B into a 4-stage ring;
-//               each CTA loads its own A tile and HALF of the shared B tile,
-//               multicast into both CTAs of the pair (L2->SM traffic 48 -> 32 KiB
-//               per k-block and CTA)
-//   warp 1      MMA issuer: one thread issues tcgen05.mma (M=128, N=256, K=16)
-//               into one of two TMEM accumulators (2 x 256 columns)
-//   warps 2..5  epilogue: tcgen05.ld accumulator rows -> registers -> fp32/bf16
-//               stores (optionally C += acc), overlapping the next tile's MMAs
-// Stage ring: full[s] (TMA bytes landed: own A + both B halves) / empty[s] (the
-// tcgen05.commit of BOTH CTAs' MMAs, multicast, since the peer's producer writes
-// into this CTA's stage); accumulators: tmem_full[a] (commit) / tmem_empty[a].
+// Structure: one CTA per SM; CTA pairs are thread-block clusters of 2 running
+// tcgen05 with cta_group::2, persistent over 256 x 256 output tiles:
+//   warp 0      TMA producer (both CTAs): CTA r loads rows [128r, 128r+128) of A and
+//               columns [128r, 128r+128) of B (128B-swizzled boxes) into its own
+//               stage of a 6-stage ring (32 KiB per stage: 16 KiB A + 16 KiB B), the
+//               bytes counted on the leader's full[s] barrier
+//   warp 1      MMA issuer (leader CTA only): one thread issues
+//               tcgen05.mma.cta_group::2 M=256 N=256 K=16, reading both CTAs' shared
+//               memory; each CTA's TMEM receives its 128 rows x 256 fp32 columns, in one
+//               of two accumulators (2 x 256 columns)
+//   warps 2..5  epilogue (both CTAs): tcgen05.ld accumulator rows -> registers ->
+//               bf16/fp32 -> swizzled shared memory -> TMA store (cp.reduce.async.bulk
+//               .add for C +=), overlapping the next tile's MMAs; register stores when
+//               C is not TMA-aligned
+// Barriers: full[s] (leader: both CTAs' TMA bytes landed), empty[s] (the leader's
+// tcgen05.commit multicast to both CTAs, since the peer's producer writes into its
+// own stage that the leader's MMAs read), tmem_full[a] (commit, multicast) and
+// tmem_empty[a] (leader: one remote arrival per epilogue warp of both CTAs).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -51,16 +56,14 @@ constexpr int kGemmThreads = 192;
 // epilogue staging for TMA stores: per epilogue warp two 32 x 32 chunks (fp32 worst case)
 constexpr uint32_t kEpiChunkBytes = 32 * 32 * 4;
 constexpr uint32_t kEpiBytes = 4 * 2 * kEpiChunkBytes;  // 32 KiB
-// Tile width N of a CTA pair: 256 (default) or 128 (MICS_GEMM_BN=128; slower, see
-// plan_gemm); the ring keeps ~192 KiB of stages either way.
-template <int BN>
-struct Tile {
-  static constexpr uint32_t kBHalfBytes = BN / kCluster * kBK * 2;  // this CTA's BN/2 columns of B
-  static constexpr uint32_t kStageBytes = kABytes + kBHalfBytes;
-  static constexpr int kStages = int((192u << 10) / kStageBytes);
-  static constexpr uint32_t kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /* align */ + 256 /* barriers */;
-};
+// Tile width N of a CTA pair: 256 (a 256 x 128 pair tile halves the MMA work per
+// staged A byte and measured slower on every shape); ~192 KiB of stages.
+constexpr int kBN = 256;
+constexpr uint32_t kBHalfBytes = kBN / kCluster * kBK * 2;  // this CTA's 128 columns of B
+constexpr uint32_t kStageBytes = kABytes + kBHalfBytes;
+constexpr int kStages = int((192u << 10) / kStageBytes);
+constexpr uint32_t kTmemCols = 2 * kBN;  // double-buffered accumulator
+constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /* align */ + 256 /* barriers */;
 
 struct GemmParams {
   void* c;
@@ -99,21 +102,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint32_t dst, uint32_t bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint32_t dst, uint32_t bar, int c0, int c1,
-                                               uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
 // both CTAs load into their own shared memory; the bytes are counted on the LEADER's barrier
 __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* map, uint32_t dst, uint32_t leader_bar, int c0,
                                                 int c1) {
@@ -121,14 +109,6 @@ __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* map, uint32_t
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
       "[%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d_2sm_mc(const CUtensorMap* map, uint32_t dst, uint32_t bar, int c0, int c1,
-                                                   uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
 }
 __device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
@@ -172,27 +152,6 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint3
   return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
          (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-// arrive on the barrier at the same offset in every CTA of `mask`
-__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-      "h"(mask)
-      : "memory");
-}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
@@ -205,11 +164,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// instruction descriptor: fp32 accumulate, bf16 x bf16, M=256 (pair), N=BN, majors
-template <int BN>
+// instruction descriptor: fp32 accumulate, bf16 x bf16, M=256 (pair), N=kBN, majors
 __device__ __forceinline__ uint32_t idesc_bf16(int a_mn, int b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
-         (uint32_t(BN >> 3) << 17) | (uint32_t((kCluster * kBM) >> 4) << 24);
+         (uint32_t(kBN >> 3) << 17) | (uint32_t((kCluster * kBM) >> 4) << 24);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -244,16 +202,9 @@ __device__ __forceinline__ void mbar_wait_probe(uint32_t bar, uint32_t parity, u
   *acc += static_cast<unsigned long long>(clock64() - t0);
 }
 
-// PAIRS = CTA pairs per cluster: 1, or 2 pairs computing vertically adjacent 256-row
-// tiles that share their B tile — each CTA then loads a quarter of its pair's B columns
-// and multicasts it into the CTA with the same pair rank in the other pair.
-template <int BN, int PAIRS>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
            const __grid_constant__ CUtensorMap tma_c, GemmParams P) {
-  constexpr int kBN = BN, kStages = Tile<BN>::kStages;
-  constexpr int kCtas = kCluster * PAIRS;
-  constexpr uint32_t kStageBytes = Tile<BN>::kStageBytes, kTmemCols = Tile<BN>::kTmemCols;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_smem = smem + kStages * kStageBytes;  // [4 warps][2 buffers][32 x 32 chunk]
@@ -263,17 +214,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
   const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int cl_rank = int(cluster_rank());
-  const int pair = cl_rank / kCluster, crank = cl_rank % kCluster;  // crank: rank inside the pair
-  const uint32_t leader = uint32_t(pair * kCluster);
-  constexpr uint16_t kAllMask = uint16_t((1u << kCtas) - 1);
-  const uint16_t kMask = uint16_t(((1u << kCluster) - 1) << (pair * kCluster));  // this pair
+  const int crank = int(cluster_rank());  // rank inside the pair; CTA 0 leads
+  const uint32_t leader = 0;
+  constexpr uint16_t kMask = uint16_t((1u << kCluster) - 1);  // both CTAs of the pair
   const long long t_start = P.probe ? clock64() : 0;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full0 + 8 * s, 1);   // leader: its producer's expect_tx (both CTAs' bytes)
-      mbar_init(empty0 + 8 * s, PAIRS);  // every leader's MMA commit, multicast to all CTAs
+      mbar_init(empty0 + 8 * s, 1);  // the leader's MMA commit, multicast to both CTAs
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);                 // the leader's commit, multicast
@@ -296,25 +245,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   // work unit = one 256 x 256 tile per pair; CTA `crank` owns rows m0 + 128*crank
   // (possibly past M: zero-filled loads, masked stores) and loads B columns
-  // n0 + 128*crank (possibly past N: zero-filled)
-  // tile t of a cluster: n-block t / tiles_m, pair `pair` takes 256-row block
-  // (t % tiles_m) * PAIRS + pair
-  const int tiles_m = (P.M + kCluster * kBM * PAIRS - 1) / (kCluster * kBM * PAIRS), tiles_n = (P.N + kBN - 1) / kBN;
+  // n0 + 128*crank (possibly past N: zero-filled); tile t = (n-block t / tiles_m,
+  // 256-row block t % tiles_m)
+  const int tiles_m = (P.M + kCluster * kBM - 1) / (kCluster * kBM), tiles_n = (P.N + kBN - 1) / kBN;
   const int ntiles = tiles_m * tiles_n, nk = (P.K + kBK - 1) / kBK;
-  const int cid = blockIdx.x / kCtas, ncl = gridDim.x / kCtas;
+  const int cid = blockIdx.x / kCluster, ncl = gridDim.x / kCluster;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       const uint32_t leader_full0 = mapa(full0, leader);
-      // multicast loads name the barrier with the pair bit cleared: each destination
-      // CTA's bytes are counted on its own pair leader's barrier (CUTLASS 2SM convention)
-      const uint32_t full_pair0 = full0 & 0xFEFFFFFFu;
-      const uint16_t bmask = uint16_t(((1u << kCtas) - 1) / ((1u << kCluster) - 1)) << crank;  // same crank
       unsigned long long w_empty = 0, *pw = P.probe ? &w_empty : nullptr;
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < ntiles; t += ncl) {
-        const int m0 = (((t % tiles_m) * PAIRS + pair) * kCluster + crank) * kBM;
+        const int m0 = ((t % tiles_m) * kCluster + crank) * kBM;
         const int nb = (t / tiles_m) * kBN + crank * (kBN / kCluster);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait_probe(empty0 + 8 * stage, phase ^ 1, pw);
@@ -328,26 +272,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           } else {
             tma_load_2d_2sm(&tma_a, sa, lfull, k0, m0);
           }
-          if (PAIRS == 1) {
-            if (P.b_mn) {
+          if (P.b_mn) {
 #pragma unroll
-              for (int j = 0; j < kBN / kCluster / 64; ++j)
-                tma_load_2d_2sm(&tma_b, sb + j * 8192, lfull, nb + 64 * j, k0);
-            } else {
-              tma_load_2d_2sm(&tma_b, sb, lfull, k0, nb);
-            }
-          } else {  // this CTA's share of the pair-half of B, multicast to the same crank of every pair
-            constexpr int kQ = kBN / kCluster / PAIRS;  // columns per share (64 for BN = 256)
-            const uint32_t fb = full_pair0 + 8 * stage;
-            if (P.b_mn) {
-#pragma unroll
-              for (int j = 0; j < kQ / 64; ++j) {
-                const int jj = pair * (kQ / 64) + j;
-                tma_load_2d_2sm_mc(&tma_b, sb + jj * 8192, fb, nb + 64 * jj, k0, bmask);
-              }
-            } else {
-              tma_load_2d_2sm_mc(&tma_b, sb + pair * kQ * 128, fb, k0, nb + pair * kQ, bmask);
-            }
+            for (int j = 0; j < kBN / kCluster / 64; ++j)
+              tma_load_2d_2sm(&tma_b, sb + j * 8192, lfull, nb + 64 * j, k0);
+          } else {
+            tma_load_2d_2sm(&tma_b, sb, lfull, k0, nb);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -359,7 +289,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && crank == 0) {  // ---------------- MMA issuer (leader CTA only)
-      const uint32_t idesc = idesc_bf16<BN>(P.a_mn, P.b_mn);
+      const uint32_t idesc = idesc_bf16(P.a_mn, P.b_mn);
       // K-major: the 16-element K slice advances 32 B inside the 128 B swizzle row;
       // MN-major: it advances 16 rows of 128 B.  LBO = distance between 64-wide MN blocks.
       const uint32_t a_step = P.a_mn ? 2048u : 32u, b_step = P.b_mn ? 2048u : 32u;
@@ -382,7 +312,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint64_t bd = umma_desc(sb + k * b_step, b_lbo, 1024);
             umma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0);
           }
-          umma_commit_2sm_mc(empty0 + 8 * stage, kAllMask);  // frees this stage in every CTA once read
+          umma_commit_2sm_mc(empty0 + 8 * stage, kMask);  // frees this stage in both CTAs once read
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -407,7 +337,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t acc_phase = 0;
     unsigned long long w_tf = 0, busy = 0, *ptf = (P.probe && warp == 2 && lane == 0) ? &w_tf : nullptr;
     for (int t = cid; t < ntiles; t += ncl) {
-      const int m0 = (((t % tiles_m) * PAIRS + pair) * kCluster + crank) * kBM, n0 = (t / tiles_m) * kBN;
+      const int m0 = ((t % tiles_m) * kCluster + crank) * kBM, n0 = (t / tiles_m) * kBN;
       mbar_wait_probe(tfull0 + 8 * acc, acc_phase, ptf);
       const long long tb0 = ptf ? clock64() : 0;
       fence_after();
@@ -575,12 +505,7 @@ int gemm_grid(int ntiles, int max_sms, int ctas) {
     int dev = 0, n = 0;
     MICS_CUDA(cudaGetDevice(&dev));
     MICS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    MICS_CUDA(cudaFuncSetAttribute(k_gemm<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(Tile<256>::kSmemBytes)));
-    MICS_CUDA(cudaFuncSetAttribute(k_gemm<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(Tile<128>::kSmemBytes)));
-    MICS_CUDA(cudaFuncSetAttribute(k_gemm<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(Tile<256>::kSmemBytes)));
+    MICS_CUDA(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
     return n;
   }();
   const int sms = max_sms > 0 && max_sms < nsm ? max_sms : nsm;
@@ -600,28 +525,17 @@ GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint6
   GemmLaunch g;
   // A(m,k): K-major -> [M rows, K inner]; M-major -> [K rows, M inner]
   g.ma = a_mn ? make_map(a, uint64_t(M), uint64_t(K), lda, 64) : make_map(a, uint64_t(K), uint64_t(M), lda, kBM);
-  // tile width 256; MICS_GEMM_BN=128 selects the narrow tile.  Measured (tools/gemm_bench.py)
-  // the narrow tile loses even where it pads far less (N = 1600: 0.588 vs 0.439 ms for
-  // the GPT-2 dgrad): half the MMA work per staged A byte makes it operand-bound.
-  const char* be = std::getenv("MICS_GEMM_BN");
-  g.bn = be && std::atoi(be) == 128 ? 128 : 256;
-  // MICS_GEMM_PAIRS=2: two pairs per cluster share B by multicast.  Correct (tested) but
-  // slower on every shape but one (8192^3: 958 vs 1393 TF/s): the pairs advance in
-  // lockstep on shared stages, and 4-CTA clusters place less evenly on the GPCs.
-  const char* pe0 = std::getenv("MICS_GEMM_PAIRS");
-  const int pairs = g.bn == 256 && pe0 && std::atoi(pe0) == 2 ? 2 : 1;
   g.mb = b_mn ? make_map(b, uint64_t(N), uint64_t(K), ldb, 64)
-              : make_map(b, uint64_t(K), uint64_t(N), ldb, uint32_t(g.bn / kCluster / pairs));  // rows per load
+              : make_map(b, uint64_t(K), uint64_t(N), ldb, uint32_t(kBN / kCluster));  // rows per load
   const char* te = std::getenv("MICS_GEMM_TMA_STORE");  // 0: register stores (A/B runs)
   const bool tma_store = !(te && te[0] == '0') && make_c_map(&g.mc, c, ldc, M, N, c_t == MICS_BF16);
   if (!tma_store) g.mc = g.ma;  // unused placeholder
   GemmParams P{c, ldc, M, N, K, c_t == MICS_BF16, accumulate != 0, a_mn != 0, b_mn != 0, nullptr, tma_store};
   static_assert(sizeof(GemmParams) <= sizeof(g.params), "GemmParams fits");
   memcpy(g.params, &P, sizeof(P));
-  g.pairs = pairs;
-  const int rows = kCluster * kBM * g.pairs;
-  g.ntiles = ((M + rows - 1) / rows) * ((N + g.bn - 1) / g.bn);  // (256 * pairs) x BN cluster tiles
-  g.grid = gemm_grid(g.ntiles, max_sms, kCluster * g.pairs);
+  const int rows = kCluster * kBM;
+  g.ntiles = ((M + rows - 1) / rows) * ((N + kBN - 1) / kBN);  // 256 x 256 pair tiles
+  g.grid = gemm_grid(g.ntiles, max_sms, kCluster);
   g.flops = 2.0 * double(M) * double(N) * double(K);
   return g;
 }
@@ -643,21 +557,16 @@ void launch_gemm(cudaStream_t s, const GemmLaunch& g) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(g.grid));
   cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = g.bn == 128 ? Tile<128>::kSmemBytes : Tile<256>::kSmemBytes;
+  cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = unsigned(kCluster * g.pairs);
+  at[0].val.clusterDim.x = unsigned(kCluster);
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (g.bn == 128)
-    MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm<128, 1>, g.ma, g.mb, g.mc, P));
-  else if (g.pairs == 2)
-    MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm<256, 2>, g.ma, g.mb, g.mc, P));
-  else
-    MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm<256, 1>, g.ma, g.mb, g.mc, P));
+  MICS_CUDA(cudaLaunchKernelEx(&cfg, k_gemm, g.ma, g.mb, g.mc, P));
   if (probe) {
     std::vector<unsigned long long> h(size_t(g.grid) * 8);
     MICS_CUDA(cudaMemcpyAsync(h.data(), d_probe, h.size() * 8, cudaMemcpyDeviceToHost, s));

@@ -94,33 +94,9 @@ struct AdamScalars {
 
 // Per-step values of a replayed (CUDA-graph) step, read by the boundary kernels
 // from device memory instead of their by-value parameters: the Adam scalars
-// (bias correction changes every step) and the fused boundary's flag epoch.
+// (bias correction changes every step).
 struct DevScalars {
   AdamScalars sc;
-  uint32_t pad_;
-  uint64_t epoch;
-};
-
-// Fused boundary (K5): one local rank's replication-group reduce-scatter of its
-// slice, then Adam over its whole shard, pulling each slice as soon as its owner
-// has published that tile (per-tile flags), so NVLink pulls, the folds and Adam's
-// HBM traffic overlap inside one kernel.
-constexpr uint32_t kBndTile = kThreads * 4 * 4;  // 4096 fp32 elements
-constexpr uint32_t kBndBlockTiles = 32;            // tiles per published block (512 KiB): one flag per block
-constexpr uint64_t kBndBlock = uint64_t(kBndTile) * kBndBlockTiles;
-struct BndJob {
-  const void* const* ptrs;    // [0, r): member shard bases; [r, 2r): member flag arrays
-  float* own;                 // this rank's shard (its slice is reduced in place)
-  float* param;
-  float* m;
-  float* v;
-  uint16_t* pbf16;            // nullable
-  float* gout;                // nullable: also leave the reduced gradient in the shard
-  uint64_t* my_flags;         // [r][nblk], written by the slice owners
-  uint64_t elems;             // shard elements (Adam range)
-  uint64_t sub;               // slice length, a multiple of kBndTile
-  uint32_t r, pos, nblk;
-  uint32_t rs_tile0, ad_tile0, pad_;
 };
 
 // Fused tail (K8, every rank on this GPU): the last micro-step's reduce-scatter, the
@@ -167,12 +143,6 @@ struct BarrierArg {
   // 1 = full system fences around every signal (the conservative protocol, kept
   // for A/B runs: MICS_BAR_STRICT=1); 0 = relaxed signals, see bar_entry/bar_exit
   int strict;
-  // Gather-slot ordering instead of fences (step.cpp enqueue_gathers, MICS_GATHER_CTR):
-  // before writing, wait until *slot_ctr >= slot_target (every earlier gather into
-  // this destination slot completed); the last CTA (slot_ticket) then bumps *slot_ctr.
-  uint64_t* slot_ctr = nullptr;
-  uint64_t slot_target = 0;
-  unsigned* slot_ticket = nullptr;
 };
 
 // --------------------------------------------------------------------------
@@ -197,8 +167,6 @@ void launch_generate(cudaStream_t s, void* out, mics_dtype dtype, uint64_t seed,
                      uint64_t start, uint64_t count, int grid);
 void launch_cast_bf16(cudaStream_t s, const float* in, uint16_t* out, uint64_t count, int grid);
 void launch_barrier(cudaStream_t s, const BarrierArg& bar);
-void launch_boundary(cudaStream_t s, const BndJob* jobs, int njobs, uint32_t rs_tiles, uint32_t ntiles, int grid,
-                     const AdamScalars& sc, uint64_t epoch, const DevScalars* dyn, const BarrierArg& bar);
 
 // K7 tcgen05 GEMM (gemm.cu): C[M,N] (+)= A[M,K]·B[K,N], bf16 operands K- or MN-major,
 // fp32 accumulation; planned once (TMA descriptors encoded), launched many times.
@@ -206,8 +174,6 @@ struct GemmLaunch {
   CUtensorMap ma, mb, mc;
   alignas(8) unsigned char params[64];
   int ntiles = 0, grid = 1;
-  int bn = 256;  // pair tile width (256 or 128)
-  int pairs = 1;  // CTA pairs per cluster (2: B tile multicast across the pairs)
   double flops = 0;
 };
 GemmLaunch plan_gemm(const void* a, uint64_t lda, int a_mn, const void* b, uint64_t ldb, int b_mn, void* c,
@@ -227,7 +193,6 @@ struct mics_ctx {
   int occ_copy = 2, occ_adam = 4, occ_reduce[4][4] = {};
   int occ_copy_indep = 1;  // CTAs/SM of barrier-free gathers chained with PDL
   int bar_strict = 0;      // BarrierArg::strict (MICS_BAR_STRICT)
-  int occ_bnd = 1;         // CTAs/SM of the fused boundary (all CTAs must be co-resident)
   int reduce_occ(mics_dtype t, uint32_t max_p) const {
     const int pc = mics::reduce_class(max_p);
     return occ_reduce[t][pc == 2 ? 0 : pc == 4 ? 1 : pc == 8 ? 2 : 3];
@@ -236,11 +201,11 @@ struct mics_ctx {
   // Barrier channels: each has its own flag slots, pairwise counters and CTA
   // tickets, so two streams can run barrier kernels concurrently (channel c is
   // only ever used from one stream, in the same order on every process).
-  // 0: main stream; 1: side stream (pipelined boundary, tail Adam) or the compute step's
+  // 0: main stream; 1: side stream (the overlapped tail's Adam) or the compute step's
   // gather stream; 2: the tail's boundary reduce-scatter stream or the compute step's
   // copy-engine reduce-scatter barriers.  Each channel is driven by one stream per step.
   static constexpr int kChannels = 3;
-  cudaStream_t side_stream = nullptr;  // channel 1: the step's pipelined boundary
+  cudaStream_t side_stream = nullptr;  // channel 1: the overlapped tail's Adam
   char* base = nullptr;           // local arena (IPC-exportable)
   uint64_t cap = 0, used = 0;
   char* peer_base[MICS_MAX_WORLD] = {};
@@ -327,10 +292,8 @@ struct AdamPlan {
 
 // A device-resident, replayable launch (built once, launched many times).
 struct Launch {
-  enum Kind { COPY, REDUCE, ADAM, BARRIER, BOUNDARY, TAIL } kind = COPY;
+  enum Kind { COPY, REDUCE, ADAM, BARRIER, TAIL } kind = COPY;
   int tail_r = 0, tail_p = 0;  // TAIL: replicas and group size (mode = 1 zero-accumulate)
-  uint32_t rs_tiles = 0;   // BOUNDARY: tiles of the reduce-scatter phase
-  uint64_t epoch = 0;      // BOUNDARY: flag value of this launch (monotone per sync state)
   void* d_desc = nullptr;  // owned device table (cudaMalloc)
   uint64_t table_bytes = 0;
   uint32_t max_p = 1;
@@ -341,7 +304,7 @@ struct Launch {
   double scale = 1.0;
   int mode = 0;
   AdamScalars adam{};
-  const DevScalars* dyn = nullptr;  // ADAM/BOUNDARY: per-step scalars in device memory (graph replay)
+  const DevScalars* dyn = nullptr;  // ADAM/TAIL: per-step scalars in device memory (graph replay)
   BarrierArg bar{};
   // algorithmic bytes one launch moves on this GPU: pulled from peers over NVLink,
   // and local HBM reads + writes (the roofline numerators of bench.py)
@@ -353,9 +316,6 @@ Launch make_reduce_launch(mics_ctx* ctx, const RedPlan& plan, mics_dtype in_t, m
                           const BarrierArg& bar, bool persistent);
 Launch make_adam_launch(mics_ctx* ctx, const AdamPlan& plan, const AdamScalars& sc, const BarrierArg& bar,
                         bool persistent);
-// jobs[i].ptrs is patched to point at ptrs[i] (2r entries) in the uploaded table
-Launch make_boundary_launch(mics_ctx* ctx, std::vector<BndJob> jobs, const std::vector<std::vector<const void*>>& ptrs,
-                            const AdamScalars& sc, const BarrierArg& bar, bool persistent);
 // dep_first: -1 = as planned, 0/1/2 = override BarrierArg::dep_first for this launch
 void enqueue(mics_ctx* ctx, const Launch& l, int dep_first = -1, cudaStream_t stream = nullptr);
 

@@ -76,15 +76,22 @@ __device__ __forceinline__ void pdl_end(const BarrierArg& b) {
 
 // ---------------------------------------------------------------- barrier
 // Pairwise monotone flags: process w's slot on each peer counts the barriers w has
-// reached with that peer.  Why relaxed signals are enough (strict = 0):
+// reached with that peer.  Memory ordering (strict = 0, the default):
 //  - entry announces "my inputs are ready"; they were written by kernels that
 //    completed before this one started (stream order, or griddepcontrol.wait),
 //    so they already sit in this GPU's L2, which is where peer loads are served.
-//  - exit announces "I finished reading your buffers": a CTA counts itself only
-//    after __syncthreads, when every load it issued has returned its value, and
-//    the last CTA's signal is issued after its ticket returns.
-//  - every data write of the collectives goes to this process's own memory.
+//    The entry signal is a relaxed store.
+//  - exit announces "I finished reading your buffers" AND publishes what this
+//    launch wrote (peers read it after the barrier without another one: the
+//    boundary Adam's bf16 parameters feed the next step's barrier-free gathers,
+//    hierarchical phase 1's stage-1 chunks feed the node peers' phase 2).  So every
+//    CTA fences its own stores (fence.acq_rel.gpu after __syncthreads, before its
+//    ticket), and the last CTA — which has observed every ticket — issues one
+//    system-scope fence before its relaxed signals: fence-to-fence synchronisation
+//    through the ticket chain, then a release pattern (fence.sys; st.relaxed.sys)
+//    towards the peers.  One MEMBAR.GPU per CTA and one MEMBAR.SYS per launch.
 // The waiter polls relaxed and acquires once, so its L1 holds nothing stale.
+// strict = 1 (MICS_BAR_STRICT) adds system fences around every signal (A/B runs).
 __device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -127,11 +134,13 @@ __device__ void bar_exit(const BarrierArg& b) {
   if (b.mask == 0) return;
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (b.exit) __threadfence();  // this CTA's stores before its ticket (publication, see above)
     if (b.strict) __threadfence_system();
     const unsigned t = atomicAdd(&b.tickets[1], 1u);
     if (t == gridDim.x - 1) {  // last CTA: every CTA of this GPU finished its accesses
       const uint64_t k = uint64_t(b.entry ? 1 : 0) + uint64_t(b.exit ? 1 : 0);
       if (b.exit) {
+        __threadfence_system();  // every CTA's fenced stores, observed through the tickets, before the signal
         bar_signal(b, k);
         bar_wait(b, k);
       }
@@ -142,36 +151,6 @@ __device__ void bar_exit(const BarrierArg& b) {
       b.tickets[0] = 0;
       b.tickets[1] = 0;
       __threadfence();
-    }
-  }
-}
-
-// Gather-slot ordering (see BarrierArg::slot_ctr).  Every earlier gather into the slot
-// is already resident or finished (each triggers its successor at entry), so the
-// wait cannot block one of them; the counter is bumped after this gather's last
-// store, before its end-of-kernel wait for its predecessor.
-__device__ __forceinline__ void slot_wait(const BarrierArg& b) {
-  if (!b.slot_ctr) return;
-  if (threadIdx.x == 0) {
-    uint64_t v;
-    for (;;) {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(b.slot_ctr) : "memory");
-      if (v >= b.slot_target) break;
-      __nanosleep(64);
-    }
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void slot_done(const BarrierArg& b) {
-  if (!b.slot_ctr) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(b.slot_ticket, 1u) == gridDim.x - 1) {  // last CTA: every store of the grid is done
-      *b.slot_ticket = 0;
-      __threadfence();
-      atomicAdd(reinterpret_cast<unsigned long long*>(b.slot_ctr), 1ull);
     }
   }
 }
@@ -200,7 +179,6 @@ __global__ void __launch_bounds__(kThreads) k_copy(const CopySeg* __restrict__ g
   const CopySeg* segs = staged ? reinterpret_cast<const CopySeg*>(smem) : gsegs;
   pdl_begin(bar);
   bar_entry(bar);
-  slot_wait(bar);
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     // last segment whose group starts at or before `tile`; stripe groups interleave their tiles
     int idx = find_desc(segs, nseg, tile);
@@ -249,7 +227,6 @@ __global__ void __launch_bounds__(kThreads) k_copy(const CopySeg* __restrict__ g
       }
     }
   }
-  slot_done(bar);
   bar_exit(bar);
   pdl_end(bar);
 }
@@ -504,8 +481,10 @@ __device__ __forceinline__ void adam_one(float g, float& p, float& m, float& v, 
 __global__ void __launch_bounds__(kThreads) k_adam(const AdamJob* __restrict__ jobs, int njobs, uint32_t ntiles,
                                                    AdamScalars sc, const DevScalars* __restrict__ dyn,
                                                    BarrierArg bar) {
-  if (dyn) sc = dyn->sc;  // written before the replayed step was launched (stream order)
   pdl_begin(bar);
+  // per-step scalars written by the preceding launch: read only after griddepcontrol.wait
+  // (pdl_begin with dep_first 1), never while the setter may still be running
+  if (dyn) sc = dyn->sc;
   bar_entry(bar);
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const AdamJob& J = jobs[find_desc(jobs, njobs, tile)];
@@ -667,8 +646,8 @@ template <typename In, int R, int P>
 __global__ void __launch_bounds__(kThreads, 2) k_tail(const TailJob* __restrict__ jobs, int njobs, uint32_t ntiles,
                                                      AdamScalars sc, const DevScalars* __restrict__ dyn, int zero_accum,
                                                      BarrierArg bar) {
-  if (dyn) sc = dyn->sc;
   pdl_begin(bar);
+  if (dyn) sc = dyn->sc;  // after griddepcontrol.wait (dep_first 1), as in k_adam
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const TailJob& J = jobs[find_desc(jobs, njobs, tile)];
     const uint64_t e = uint64_t(tile - J.tile0) * kTailTile + uint64_t(threadIdx.x) * 4;
@@ -761,152 +740,6 @@ __global__ void __launch_bounds__(kThreads) k_cast_bf16(const float* in, uint16_
     out[i] = f32_to_bf16(in[i]);
 }
 
-// ---------------------------------------------------------------- K5': fused boundary
-// Data another GPU writes during this kernel (published by a flag) is read with a
-// coherent load, never through the non-coherent path.
-__device__ __forceinline__ uint4 ld_coherent(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p)
-               : "memory");
-  return r;
-}
-
-// Work items are blocks of kBndBlockTiles tiles.  Items [0, rs_items): the
-// reduce-scatter of each local rank's slice (fold over the r replication positions
-// in ascending order, stored in place), then one release flag per block into every
-// replica's flag array.  Items [rs_items, nitems): Adam over every local rank's
-// shard, each block waiting for its slice owner's flag.  All reduce-scatter items
-// precede all Adam items in every CTA's grid-stride order and the grid is one
-// resident wave, so every awaited flag is produced by a running CTA.
-__device__ __forceinline__ void bnd_reduce_tile(const BndJob& J, uint64_t e0) {
-  const uint32_t r = J.r;
-#pragma unroll 1
-  for (int h = 0; h < 4; h += 2) {  // 2 x (2 float4 per thread)
-    uint4 raw[8][2];
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (q < int(r)) {
-        const float* s = static_cast<const float*>(J.ptrs[q]);
-#pragma unroll
-        for (int u = 0; u < 2; ++u) raw[q][u] = ld_stream(s + e0 + (uint64_t(h + u) * kThreads + threadIdx.x) * 4);
-      }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      float a[4];
-      Codec<float, float>::unpack(raw[0][u], a);
-#pragma unroll
-      for (int q = 1; q < 8; ++q)
-        if (q < int(r)) {
-          float x[4];
-          Codec<float, float>::unpack(raw[q][u], x);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) a[k] = __fadd_rn(a[k], x[k]);
-        }
-      *reinterpret_cast<float4*>(J.own + e0 + (uint64_t(h + u) * kThreads + threadIdx.x) * 4) =
-          make_float4(a[0], a[1], a[2], a[3]);
-    }
-  }
-}
-
-__device__ __forceinline__ void bnd_adam_tile(const BndJob& J, const float* g, uint64_t e0, const AdamScalars& sc) {
-  if (e0 + kBndTile <= J.elems) {
-#pragma unroll 1
-    for (int h = 0; h < 4; h += 2) {
-      uint4 gr[2];
-      float4 p[2], m[2], v[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const uint64_t e = e0 + (uint64_t(h + u) * kThreads + threadIdx.x) * 4;
-        gr[u] = ld_coherent(g + e);
-        p[u] = *reinterpret_cast<const float4*>(J.param + e);
-        m[u] = *reinterpret_cast<const float4*>(J.m + e);
-        v[u] = *reinterpret_cast<const float4*>(J.v + e);
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const uint64_t e = e0 + (uint64_t(h + u) * kThreads + threadIdx.x) * 4;
-        adam_one(__uint_as_float(gr[u].x), p[u].x, m[u].x, v[u].x, sc);
-        adam_one(__uint_as_float(gr[u].y), p[u].y, m[u].y, v[u].y, sc);
-        adam_one(__uint_as_float(gr[u].z), p[u].z, m[u].z, v[u].z, sc);
-        adam_one(__uint_as_float(gr[u].w), p[u].w, m[u].w, v[u].w, sc);
-        *reinterpret_cast<float4*>(J.param + e) = p[u];
-        *reinterpret_cast<float4*>(J.m + e) = m[u];
-        *reinterpret_cast<float4*>(J.v + e) = v[u];
-        if (J.pbf16) {
-          uint2 pk;
-          pk.x = uint32_t(f32_to_bf16(p[u].x)) | (uint32_t(f32_to_bf16(p[u].y)) << 16);
-          pk.y = uint32_t(f32_to_bf16(p[u].z)) | (uint32_t(f32_to_bf16(p[u].w)) << 16);
-          *reinterpret_cast<uint2*>(J.pbf16 + e) = pk;
-        }
-        if (J.gout) st_vec(J.gout + e, gr[u]);
-      }
-    }
-  } else {
-    for (uint64_t x = e0 + threadIdx.x; x < J.elems && x < e0 + kBndTile; x += kThreads) {
-      const float gx = *reinterpret_cast<const volatile float*>(g + x);
-      float p = J.param[x], m = J.m[x], v = J.v[x];
-      adam_one(gx, p, m, v, sc);
-      J.param[x] = p;
-      J.m[x] = m;
-      J.v[x] = v;
-      if (J.pbf16) J.pbf16[x] = f32_to_bf16(p);
-      if (J.gout) J.gout[x] = gx;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kThreads, 2) k_boundary(const BndJob* __restrict__ jobs, int njobs,
-                                                          uint32_t rs_items, uint32_t nitems, AdamScalars sc,
-                                                          uint64_t epoch, const DevScalars* __restrict__ dyn,
-                                                          BarrierArg bar) {
-  constexpr uint64_t kBlock = uint64_t(kBndTile) * kBndBlockTiles;
-  if (dyn) {
-    sc = dyn->sc;
-    epoch = dyn->epoch;
-  }
-  pdl_begin(bar);
-  bar_entry(bar);
-  for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-    if (item < rs_items) {
-      int j = 0;
-      while (j + 1 < njobs && jobs[j + 1].rs_tile0 <= item) ++j;
-      const BndJob& J = jobs[j];
-      const uint32_t b = item - J.rs_tile0;
-      const uint64_t e0 = uint64_t(J.pos) * J.sub + uint64_t(b) * kBlock;
-#pragma unroll 1
-      for (uint32_t t = 0; t < kBndBlockTiles; ++t) bnd_reduce_tile(J, e0 + uint64_t(t) * kBndTile);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence_system();
-        for (uint32_t q = 0; q < J.r; ++q)
-          st_release_sys(static_cast<uint64_t*>(const_cast<void*>(J.ptrs[J.r + q])) + uint64_t(J.pos) * J.nblk + b,
-                         epoch);
-      }
-    } else {
-      const uint32_t a = item - rs_items;
-      int j = 0;
-      while (j + 1 < njobs && jobs[j + 1].ad_tile0 <= a) ++j;
-      const BndJob& J = jobs[j];
-      const uint32_t t = a - J.ad_tile0, q = t / J.nblk;
-      const uint64_t e0 = uint64_t(t) * kBlock;  // slices are whole blocks: block t of the shard
-      if (threadIdx.x == 0)
-        while (ld_acquire_sys(J.my_flags + t) < epoch) __nanosleep(256);
-      __syncthreads();
-      const float* g = static_cast<const float*>(J.ptrs[q]);
-#pragma unroll 1
-      for (uint32_t k = 0; k < kBndBlockTiles; ++k) {
-        const uint64_t e = e0 + uint64_t(k) * kBndTile;
-        if (e >= J.elems) break;
-        bnd_adam_tile(J, g, e, sc);
-      }
-    }
-  }
-  bar_exit(bar);
-  pdl_end(bar);
-}
-
 __global__ void k_set_scalars(DevScalars* dst, DevScalars v) { *dst = v; }
 
 __global__ void k_barrier(BarrierArg bar) {
@@ -981,9 +814,6 @@ int resident_ctas(int kind, mics_dtype in_t, int pc) {
       else if (in_t == MICS_F64) n = reduce_occupancy<double, double>(pc);
       else if (in_t == MICS_I64) n = reduce_occupancy<long long, long long>(pc);
       else n = reduce_occupancy<float, float>(pc);
-      break;
-    case 3:
-      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_boundary, kThreads, 0));
       break;
     default:
       MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_adam, kThreads, 0));
@@ -1069,11 +899,6 @@ void launch_cast_bf16(cudaStream_t s, const float* in, uint16_t* out, uint64_t c
 
 void launch_barrier(cudaStream_t s, const BarrierArg& bar) {
   launch_ex(k_barrier, 1, 32, 0, s, bar);
-}
-
-void launch_boundary(cudaStream_t s, const BndJob* jobs, int njobs, uint32_t rs_tiles, uint32_t ntiles, int grid,
-                     const AdamScalars& sc, uint64_t epoch, const DevScalars* dyn, const BarrierArg& bar) {
-  launch_ex(k_boundary, grid, kThreads, 0, s, jobs, njobs, rs_tiles, ntiles, sc, epoch, dyn, bar);  // items, not tiles
 }
 
 }  // namespace mics

@@ -141,7 +141,6 @@ mics_ctx* create_ctx(const mics_init_args* a) {
       c->occ_copy_indep = std::max(1, std::min(c->occ_copy, std::atoi(e)));
     if (const char* e = std::getenv("MICS_BAR_STRICT")) c->bar_strict = std::atoi(e) != 0;
     c->occ_adam = resident_ctas(2, MICS_F32);
-    c->occ_bnd = resident_ctas(3, MICS_F32);
     const int classes[4] = {2, 4, 8, 9};
     for (int t = 0; t < 4; ++t)
       for (int k = 0; k < 4; ++k) c->occ_reduce[t][k] = resident_ctas(1, mics_dtype(t), classes[k]);

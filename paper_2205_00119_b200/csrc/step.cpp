@@ -39,19 +39,8 @@ void release(mics_step* st) {
   for (auto& l : st->agm) l.release();
   for (auto& v : st->micro)
     for (auto& l : v) l.release();
-  for (auto& v : st->micro1)
-    for (auto& l : v) l.release();
   st->bnd.rs.release();
   st->bnd.ag.release();
-  for (auto& b : st->bndg)
-    for (auto& x : b) {
-      x.rs.release();
-      x.ag.release();
-    }
-  if (st->ev_rs) cudaEventDestroy(st->ev_rs);
-  for (auto e : st->ev_done)
-    if (e) cudaEventDestroy(e);
-  for (auto e : st->ev_bnd) cudaEventDestroy(e);
   if (st->gexec) cudaGraphExecDestroy(st->gexec);
   for (auto& l : st->tail_rs) l.release();
   st->ftail.release();
@@ -76,8 +65,6 @@ void release(mics_step* st) {
   if (st->cs) cudaStreamDestroy(st->cs);
   if (st->copy_stream) cudaStreamDestroy(st->copy_stream);
   if (st->d_scalars) cudaFree(st->d_scalars);
-  if (st->d_slot_ctr) cudaFree(st->d_slot_ctr);
-  if (st->d_slot_tickets) cudaFree(st->d_slot_tickets);
 }
 
 // flat all-gather of layer l into gathered slot (l % gather_slots) of every local rank
@@ -167,9 +154,10 @@ CopyPlan concat_plans(const CopyPlan& a, const CopyPlan& b) {
 // phase 2 of visit i-1 together with phase 1 of visit i (one launch, phase 1's exit
 // barrier); then phase 2 of the last visit.  Safe: phase 2 of visit i-1 reads the node
 // peers' stage-1 chunks published by the previous launch's exit barrier; phase 1 of
-// visit i writes buffer (layer % 2), whose last readers (the peers' phase 2 two visits
-// back) finished before they reached that same barrier; when consecutive visits are
-// the same layer (the forward/backward turn) phase 1 rewrites identical bytes.
+// visit i writes slot (layer % gather_slots), whose last readers (the peers' phase 2
+// of an earlier visit to a layer of that slot, at least two visits back for any slot
+// count >= 2) finished before they reached that same barrier; when consecutive visits
+// are the same layer (the forward/backward turn) phase 1 rewrites identical bytes.
 void build_hier_merged(mics_step* st) {
   mics_ctx* ctx = st->ctx;
   const int L = st->cfg.nlayers;
@@ -203,54 +191,32 @@ void enqueue_generate(mics_step* st, int t) {
 
 bool generated(const mics_step* st) { return !st->cfg.resident_grads && !st->compute; }
 
-int cur_buf(const mics_step* st) { return st->pipelined ? int(st->step_idx & 1) : 0; }
-
-// side = the pipelined boundary goes to the side stream (channel 1) and overlaps the
-// next step; otherwise (profiling) everything runs in order on the main stream.
-void enqueue_boundary(mics_step* st, bool side) {
+// The boundary in order on the main stream: the replication-group reduce-scatter,
+// then Adam fused with the all-reduce's all-gather phase.
+void enqueue_boundary(mics_step* st) {
   mics_ctx* ctx = st->ctx;
   st->adam_step++;
   const AdamScalars sc = make_adam_scalars(st->cfg.lr, st->cfg.beta1, st->cfg.beta2, st->cfg.eps,
                                            st->cfg.weight_decay, st->adam_step, st->adam.grad_scale);
-  if (!st->pipelined) {
-    const uint64_t epoch = st->bnd.has_ag ? ++st->sync->epoch : 0;
-    if (st->d_scalars && !st->capturing) {  // boundary kernels read the device copy once a graph exists
-      DevScalars v{};
-      v.sc = sc;
-      v.epoch = epoch;
-      launch_set_scalars(ctx->stream, st->d_scalars, v);
-    }
-    if (st->bnd.has_rs) enqueue(ctx, st->bnd.rs);
-    if (st->bnd.has_ag) {
-      st->bnd.ag.adam = sc;
-      st->bnd.ag.epoch = epoch;
-      enqueue(ctx, st->bnd.ag);
-    }
-    return;
+  if (st->d_scalars && !st->capturing) {  // boundary kernels read the device copy once a graph exists
+    DevScalars v{};
+    v.sc = sc;
+    launch_set_scalars(ctx->stream, st->d_scalars, v);
   }
-  const int b = cur_buf(st);
-  cudaStream_t s = side ? ctx->side_stream : ctx->stream;
-  if (side) {  // the boundary reads the accumulator the main stream's last reduce-scatter wrote
-    MICS_CUDA(cudaEventRecord(st->ev_rs, ctx->stream));
-    MICS_CUDA(cudaStreamWaitEvent(s, st->ev_rs, 0));
+  if (st->bnd.has_rs) enqueue(ctx, st->bnd.rs);
+  if (st->bnd.has_ag) {
+    st->bnd.ag.adam = sc;
+    enqueue(ctx, st->bnd.ag);
   }
-  for (size_t g = 0; g < st->bndg[b].size(); ++g) {
-    BoundaryLaunches& x = st->bndg[b][g];
-    if (x.has_rs) enqueue(ctx, x.rs, -1, s);
-    x.ag.adam = sc;
-    enqueue(ctx, x.ag, -1, s);
-    if (side) MICS_CUDA(cudaEventRecord(st->ev_bnd[g], s));
-  }
-  if (side) MICS_CUDA(cudaEventRecord(st->ev_done[b], s));
 }
 
-// Up to 4 layer groups of about equal shard size, in forward order: layer l joins
-// the group its shard midpoint falls in (empty groups vanish).
+// Up to `groups` layer groups of about equal shard size, in forward order: layer l
+// joins the group its shard midpoint falls in (empty groups vanish).
 void plan_layer_groups(mics_step* st, int groups = 4) {
   if (!st->group_range.empty()) return;
   mics_sync* sy = st->sync;
   const int L = st->cfg.nlayers;
-  // MICS_TAIL_GROUPS overrides the pipeline depth of the overlapped tail / pipelined boundary
+  // MICS_TAIL_GROUPS overrides the pipeline depth of the overlapped tail
   if (const char* e = std::getenv("MICS_TAIL_GROUPS")) groups = std::max(1, std::min(16, std::atoi(e)));
   const uint64_t G = uint64_t(std::min(groups, L)), S = sy->shard_elems;
   int prev = -1;
@@ -385,77 +351,45 @@ void enqueue_fused_tail(mics_step* st) {
   enqueue(ctx, st->ftail);
 }
 
-// forward then backward per-layer gathers.  The first gather of a window follows
-// the boundary's Adam (which rewrote the shards it reads), so it waits for its
-// predecessor; the others only depend on static shards.  With the pipelined
-// boundary, layer group g's first gather of the window waits for group g's Adam.
+// forward then backward per-layer gathers.  The first gather of a step follows the
+// boundary's Adam (which rewrote the shards it reads), so it waits for its
+// predecessor; the others only depend on static shards.
 // In-flight bound: every (slots-1)-th gather is a fence (dep_first 0), so at most
 // `slots` consecutive gathers run at once.  Two gathers within `slots` positions
 // of each other either hit different slots (layers a != b mod slots) or carry the
 // same bytes (the same layer at the forward/backward turn): no write-after-write
-// race on a slot.
-void enqueue_gathers(mics_step* st, int t, bool side) {
+// race on a slot.  step_create rejects empty layers, so every gather launches and
+// the fence positions are the ones counted here.
+void enqueue_gathers(mics_step* st, int t) {
   mics_ctx* ctx = st->ctx;
-  if (!st->agm.empty()) {  // merged hierarchical sequence (not with the pipelined boundary)
+  if (!st->agm.empty()) {  // merged hierarchical sequence
     for (size_t i = 0; i < st->agm.size(); ++i) enqueue(ctx, st->agm[i], i == 0 && t == 0 ? 1 : -1);
     return;
   }
   bool first = true;
-  size_t g = 0;
   const int m = st->gather_slots - 1;
   int pos = 0;
   // only the flat gathers are independent; hierarchical launches keep their plan
-  auto dep = [&](const Launch& x) {
-    if (x.bar.dep_first != 0 || x.bar.mask) return -1;
-    return pos++ % m == m - 1 ? 0 : 2;
+  auto go = [&](const Launch& x) {
+    int d = -1;
+    if (x.bar.dep_first == 0 && !x.bar.mask) d = pos++ % m == m - 1 ? 0 : 2;
+    if (first && t == 0) d = 1;
+    first = false;
+    enqueue(ctx, x, d);
   };
-  // MICS_GATHER_CTR: no fences; a gather waits on the device for every earlier
-  // gather into its slot (counters zeroed at the start of each step, in stream order,
-  // so host targets and device counts always agree)
-  if (st->gather_ctr && t == 0) {
-    MICS_CUDA(cudaMemsetAsync(st->d_slot_ctr, 0, kMaxGatherSlots * sizeof(uint64_t), ctx->stream));
-    std::fill(st->slot_host.begin(), st->slot_host.end(), 0);
-  }
-  const int L = int(st->layers.size());
-  auto go = [&](const Launch& x, int l, int dir, int forced) {
-    if (!st->gather_ctr || x.bar.dep_first != 0 || x.bar.mask || x.ndesc == 0) {
-      const int d = dep(x);
-      enqueue(ctx, x, forced >= 0 ? forced : d);
-      return;
-    }
-    const int s = l % st->gather_slots;
-    Launch y = x;
-    y.bar.slot_ctr = st->d_slot_ctr + s;
-    y.bar.slot_target = st->slot_host[size_t(s)]++;
-    y.bar.slot_ticket = st->d_slot_tickets + dir * L + l;
-    enqueue(ctx, y, forced >= 0 ? forced : 2);
-  };
-  for (size_t l = 0; l < st->layers.size(); ++l) {
-    if (st->pipelined && side && t == 0 && g < st->group_first_layer.size() &&
-        int(l) == st->group_first_layer[g]) {
-      MICS_CUDA(cudaStreamWaitEvent(ctx->stream, st->ev_bnd[g], 0));
-      ++g;
-    }
-    for (auto& x : st->ag[l]) {
-      go(x, int(l), 0, first && t == 0 ? 1 : -1);
-      first = false;
-    }
-  }
+  for (size_t l = 0; l < st->layers.size(); ++l)
+    for (auto& x : st->ag[l]) go(x);
   for (size_t l = st->layers.size(); l-- > 0;)
-    for (auto& x : st->ag[l]) go(x, int(l), 1, -1);
+    for (auto& x : st->ag[l]) go(x);
 }
 
-void enqueue_sync(mics_step* st, int t, bool side) {
-  mics_ctx* ctx = st->ctx;
-  const int b = cur_buf(st);
-  if (st->pipelined && side && t == 0)  // the boundary two steps back has finished reading this buffer
-    MICS_CUDA(cudaStreamWaitEvent(ctx->stream, st->ev_done[b], 0));
-  for (auto& x : (b ? st->micro1 : st->micro)[size_t(t)]) enqueue(ctx, x);
+void enqueue_sync(mics_step* st, int t) {
+  for (auto& x : st->micro[size_t(t)]) enqueue(st->ctx, x);
 }
 
-void enqueue_micro(mics_step* st, int t, bool side) {
-  enqueue_gathers(st, t, side);
-  enqueue_sync(st, t, side);
+void enqueue_micro(mics_step* st, int t) {
+  enqueue_gathers(st, t);
+  enqueue_sync(st, t);
 }
 
 // ---------------------------------------------------------------- step with compute
@@ -843,7 +777,7 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
     if (!st->rs_overlap) wait(C, st->ev_rsd[size_t(slot)]);  // next micro-step's GEMMs after the RS
   }
   if (tr) tr->begin(M, "boundary", s, -1);
-  enqueue_boundary(st, false);
+  enqueue_boundary(st);
   if (tr) tr->end(M);
   if (clk) clk->mark(PH_BND);
   rec(st->ev_jg, G);
@@ -853,15 +787,14 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
   trace_flush(tr, ctx);
 }
 
-// the main stream waits for the side stream, so a main-stream sync covers the step
-void join_side(mics_step* st) {
-  if (st->pipelined && st->step_idx > 0)
-    MICS_CUDA(cudaStreamWaitEvent(st->ctx->stream, st->ev_done[(st->step_idx - 1) & 1], 0));
-}
 }  // namespace
 
 mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
   if (!cfg || cfg->nlayers < 1 || !cfg->layer_params) raise(MICS_OUT_OF_RANGE, "step config needs >= 1 layer");
+  // every layer gathers something: the fence positions of the gather chain
+  // (enqueue_gathers) and the first gather's wait for the boundary count on it
+  for (int l = 0; l < cfg->nlayers; ++l)
+    if (cfg->layer_params[l] == 0) raise(MICS_OUT_OF_RANGE, "layer " + std::to_string(l) + " has no parameters");
   if (cfg->grad_t != MICS_F32 && cfg->grad_t != MICS_BF16) raise(MICS_TYPE_MISMATCH, "gradients must be f32 or bf16");
   if (cfg->hier_k > 0) {
     if (!mics_partition_shape_ok(cfg->p, cfg->hier_k) || ctx->n % cfg->hier_k)
@@ -890,14 +823,6 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)
       st->gather_slots = std::max(2, std::min(kMaxGatherSlots, std::atoi(e)));
     st->gathered = alloc_sym(ctx, uint64_t(st->gather_slots) * st->gathered_half);
-    if (const char* e = std::getenv("MICS_GATHER_CTR"); e && !cfg->compute) st->gather_ctr = std::atoi(e) != 0;
-    if (st->gather_ctr) {
-      MICS_CUDA(cudaMalloc(&st->d_slot_ctr, kMaxGatherSlots * sizeof(uint64_t)));
-      MICS_CUDA(cudaMemset(st->d_slot_ctr, 0, kMaxGatherSlots * sizeof(uint64_t)));
-      MICS_CUDA(cudaMalloc(&st->d_slot_tickets, 2 * size_t(cfg->nlayers) * sizeof(unsigned)));
-      MICS_CUDA(cudaMemset(st->d_slot_tickets, 0, 2 * size_t(cfg->nlayers) * sizeof(unsigned)));
-      st->slot_host.assign(size_t(st->gather_slots), 0);
-    }
     // gradient slots: s resident sets, 1 regenerated per micro-step, or with compute 2
     // (the GEMMs of micro-step t+1 write one while the reduce-scatter of t reads the other)
     st->compute = cfg->compute != 0;
@@ -945,36 +870,12 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     st->adam.exp_avg_sq = st->v;
     st->adam.param_bf16 = st->pbf16;
     st->adam.write_grad = 0;
-    // Pipelined boundary, opt-in (MICS_PIPELINE=1).  Without compute in the step the
-    // only work independent of the updated parameters is the first micro-step's
-    // forward gathers, so it measured no gain (10.24 vs 10.16 ms on 4 GPUs); it is
-    // the hook for overlapping the optimizer with a real forward pass.
-    const char* penv = std::getenv("MICS_PIPELINE");
-    st->pipelined = !cfg->alternative && !st->compute && penv && penv[0] == '1';
     {
       const char* me = std::getenv("MICS_HIER_MERGE");
-      if (cfg->hier_k > 0 && cfg->p > cfg->hier_k && !st->compute && !st->pipelined && !(me && me[0] == '0'))
+      if (cfg->hier_k > 0 && cfg->p > cfg->hier_k && !st->compute && !(me && me[0] == '0'))
         build_hier_merged(st);
     }
-    if (st->pipelined) {
-      st->gacc1 = alloc_sym(ctx, sy->shard.stride);
-      MICS_CUDA(cudaMemsetAsync(ctx->base + st->gacc1.offset, 0, st->gacc1.stride * uint64_t(ctx->per), ctx->stream));
-      for (int t = 0; t < cfg->s; ++t) {
-        const uint64_t goff = uint64_t(t % st->gslots) * sy->grad_elems * szg;
-        st->micro1.push_back({build_micro_launch(sy, st->grads, goff, cfg->grad_t, 1.0,
-                                                 t == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE, true, false, 1, 1,
-                                                 &st->gacc1)});
-      }
-      plan_layer_groups(st);
-      for (const auto& [lo, hi] : st->group_range) {
-        st->bndg[0].push_back(build_boundary_range(sy, &st->adam, sy->shard, lo, hi, 1));
-        st->bndg[1].push_back(build_boundary_range(sy, &st->adam, st->gacc1, lo, hi, 1));
-      }
-      MICS_CUDA(cudaEventCreateWithFlags(&st->ev_rs, cudaEventDisableTiming));
-      for (auto& e : st->ev_done) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      st->ev_bnd.resize(st->group_range.size());
-      for (auto& e : st->ev_bnd) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    } else if (!cfg->alternative) {
+    if (!cfg->alternative) {
       st->bnd = build_boundary(sy, &st->adam, true, false);
       // overlapped tail (MICS_TAIL_OVERLAP=0/1 forces it)
       const char* te = std::getenv("MICS_TAIL_OVERLAP");
@@ -1076,9 +977,7 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
       S2.rs_hbm_bytes += x.hbm_bytes;
     }
     std::vector<const BoundaryLaunches*> bl;
-    if (st->pipelined)
-      for (const auto& x : st->bndg[0]) bl.push_back(&x);
-    else if (st->tail)
+    if (st->tail)
       for (const auto& x : st->tail_bnd) bl.push_back(&x);
     else if (!st->fused_tail)
       bl.push_back(&st->bnd);
@@ -1126,7 +1025,6 @@ void step_destroy(mics_step* st) {
 
 namespace {
 bool graph_enabled(const mics_step* st) {
-  if (st->pipelined) return false;  // the pipelined boundary overlaps the next step: not one closed graph
   const char* e = std::getenv("MICS_GRAPH");
   return !(e && e[0] == '0');
 }
@@ -1135,7 +1033,7 @@ bool graph_enabled(const mics_step* st) {
 // boundary kernels read their per-step scalars from st->d_scalars, so the same
 // graph replays every step; programmatic-dependent-launch edges are kept by the
 // capture.  The capture itself launches nothing: the state it advanced (Adam
-// step, flag epoch) is rolled back and re-advanced per replay.
+// step) is rolled back and re-advanced per replay.
 void build_graph(mics_step* st) {
   mics_ctx* ctx = st->ctx;
   st->graph_tried = true;
@@ -1144,7 +1042,7 @@ void build_graph(mics_step* st) {
   for (auto& b : st->tail_bnd) b.ag.dyn = st->d_scalars;
   st->ftail.dyn = st->d_scalars;
   const int adam_step0 = st->adam_step;
-  const uint64_t epoch0 = st->sync->epoch, launches0 = ctx->launches;
+  const uint64_t launches0 = ctx->launches;
   cudaGraph_t g = nullptr;
   MICS_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   st->capturing = true;
@@ -1155,16 +1053,16 @@ void build_graph(mics_step* st) {
       for (int t = 0; t < st->cfg.s; ++t) {
         if (generated(st)) enqueue_generate(st, t);
         if ((st->tail || st->fused_tail) && t == st->cfg.s - 1) {
-          enqueue_gathers(st, t, false);
+          enqueue_gathers(st, t);
           if (st->tail)
             enqueue_tail(st, nullptr);
           else
             enqueue_fused_tail(st);
         } else {
-          enqueue_micro(st, t, false);
+          enqueue_micro(st, t);
         }
       }
-      if (!st->tail && !st->fused_tail) enqueue_boundary(st, false);
+      if (!st->tail && !st->fused_tail) enqueue_boundary(st);
     }
   } catch (...) {
     st->capturing = false;
@@ -1191,7 +1089,6 @@ void build_graph(mics_step* st) {
   st->graph_launches = ctx->launches - launches0;
   ctx->launches = launches0;
   st->adam_step = adam_step0;
-  st->sync->epoch = epoch0;
   const cudaError_t e = cudaGraphInstantiate(&st->gexec, g, 0);
   cudaGraphDestroy(g);
   MICS_CUDA(e);
@@ -1203,7 +1100,6 @@ void replay(mics_step* st) {
   DevScalars v{};
   v.sc = make_adam_scalars(st->cfg.lr, st->cfg.beta1, st->cfg.beta2, st->cfg.eps, st->cfg.weight_decay,
                            st->adam_step, st->adam.grad_scale);
-  if (st->bnd.has_ag) v.epoch = ++st->sync->epoch;
   launch_set_scalars(ctx->stream, st->d_scalars, v);
   MICS_CUDA(cudaGraphLaunch(st->gexec, ctx->stream));
   ctx->launches += st->graph_launches + 1;
@@ -1227,19 +1123,18 @@ void step_run(mics_step* st, int iters) {
     for (int t = 0; t < st->cfg.s; ++t) {
       if (generated(st)) enqueue_generate(st, t);
       if ((st->tail || st->fused_tail) && t == st->cfg.s - 1) {
-        enqueue_gathers(st, t, true);
+        enqueue_gathers(st, t);
         if (st->tail)
           enqueue_tail(st, nullptr);
         else
           enqueue_fused_tail(st);
       } else {
-        enqueue_micro(st, t, true);
+        enqueue_micro(st, t);
       }
     }
-    if (!st->tail && !st->fused_tail) enqueue_boundary(st, true);
+    if (!st->tail && !st->fused_tail) enqueue_boundary(st);
     st->step_idx++;
   }
-  join_side(st);
   st->stats.adam_step = st->adam_step;
 }
 
@@ -1271,9 +1166,9 @@ void step_profile(mics_step* st, double* ms) {
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
     if (generated(st)) enqueue_generate(st, t);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
-    enqueue_gathers(st, t, false);
+    enqueue_gathers(st, t);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
-    if (!((st->tail || st->fused_tail) && t == s - 1)) enqueue_sync(st, t, false);
+    if (!((st->tail || st->fused_tail) && t == s - 1)) enqueue_sync(st, t);
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
   }
   MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
@@ -1283,7 +1178,7 @@ void step_profile(mics_step* st, double* ms) {
   else if (st->fused_tail)
     enqueue_fused_tail(st);  // timed as the boundary phase (it carries the last reduce-scatter)
   else
-    enqueue_boundary(st, false);
+    enqueue_boundary(st);
   st->step_idx++;
   MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
   MICS_CUDA(cudaEventSynchronize(ev[size_t(k - 1)]));
@@ -1377,21 +1272,20 @@ void step_run_host(mics_step* st, const void* host_grads, int iters, void* host_
       copy_in(0);
     for (int t = 0; t < s; ++t) {
       const int k = t % nslot;
-      enqueue_gathers(st, t, true);  // parameters only: overlaps the copies
+      enqueue_gathers(st, t);  // parameters only: overlaps the copies
       MICS_CUDA(cudaStreamWaitEvent(ctx->stream, st->ev_h2d[size_t(k)], 0));
       if (st->tail && t == s - 1)
         enqueue_tail(st, nullptr);  // last reduce-scatter + boundary, overlapped per layer group
       else if (st->fused_tail && t == s - 1)
         enqueue_fused_tail(st);     // last reduce-scatter + boundary + Adam in one kernel
       else
-        enqueue_sync(st, t, true);
+        enqueue_sync(st, t);
       MICS_CUDA(cudaEventRecord(st->ev_rs_slot[size_t(k)], ctx->stream));
       if (nslot != s && t + 1 < s) copy_in(t + 1);
     }
-    if (!st->tail && !st->fused_tail) enqueue_boundary(st, true);
+    if (!st->tail && !st->fused_tail) enqueue_boundary(st);
     st->step_idx++;
     if (host_result) {
-      join_side(st);
       int li = 0;
       for (int r = 0; r < ctx->n; ++r) {
         if (!ctx->local(r)) continue;

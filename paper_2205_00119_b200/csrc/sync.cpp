@@ -71,10 +71,8 @@ mics_sync* sync_create(mics_ctx* ctx, int p, int s, int nseg, const uint64_t* se
   st->shard_elems = so;
   st->grad_elems = go;
   const int r = n / p;
-  // boundary slices: whole fused-boundary tiles when the replication group is real
-  // the fused boundary publishes whole blocks: only for shards of at least one block per slice
-  st->fusable = r > 1 && acc_t == MICS_F32 && so >= uint64_t(r) * kBndBlock;
-  st->sub = round_up(ceil_div(so, uint64_t(r)), st->fusable ? kBndBlock : 4);
+  // boundary slices: position i of a replication group reduces slice i (16-byte aligned)
+  st->sub = round_up(ceil_div(so, uint64_t(r)), 4);
   const uint64_t sz = dtype_size(acc_t);
   st->shard = alloc_sym(ctx, std::max<uint64_t>(uint64_t(r) * st->sub, 1) * sz);
   // SyncState shards start at T{} (make_sync_states :65)
@@ -157,51 +155,6 @@ BoundaryLaunches build_boundary(mics_sync* st, const mics_adam* adam, bool persi
             ctx->record(j + a * p, j + b * p, padded / uint64_t(r) * sza);
             ctx->record(j + a * p, j + b * p, padded / uint64_t(r) * sza);
           }
-  }
-  const char* fenv = std::getenv("MICS_FUSED_BOUNDARY");
-  // opt-in (MICS_FUSED_BOUNDARY=1): measured 8.5 vs 7.7 ms (1 GPU) and 4.7 vs 4.9 ms
-  // (4 GPUs) per C3 boundary against the two-kernel path, so the latter is the default
-  const bool fused = adam && st->fusable && fenv && fenv[0] == '1';
-  if (fused) {  // one kernel: slice reduce-scatter + per-tile flags + Adam (K5')
-    const uint32_t nblk = uint32_t(sub / kBndBlock);
-    if (!st->bflags_ready) {  // SPMD: every process allocates at the same point
-      st->bflags = alloc_sym(ctx, uint64_t(r) * nblk * 8);
-      MICS_CUDA(cudaMemsetAsync(ctx->base + st->bflags.offset, 0, st->bflags.stride * uint64_t(ctx->per), ctx->stream));
-      st->bflags_ready = true;
-    }
-    std::vector<BndJob> jobs;
-    std::vector<std::vector<const void*>> ptrs;
-    for (int rho = 0; rho < n; ++rho) {
-      if (!ctx->local(rho)) continue;
-      const int j = rho % p;
-      std::vector<const void*> pp(2 * static_cast<size_t>(r));
-      for (int q = 0; q < r; ++q) {
-        pp[size_t(q)] = ctx->rank_ptr(st->shard, j + q * p);
-        pp[size_t(r + q)] = ctx->rank_ptr(st->bflags, j + q * p);
-      }
-      BndJob J;
-      std::memset(&J, 0, sizeof(J));
-      J.own = reinterpret_cast<float*>(ctx->rank_ptr(st->shard, rho));
-      J.param = reinterpret_cast<float*>(ctx->rank_ptr(adam->param, rho));
-      J.m = reinterpret_cast<float*>(ctx->rank_ptr(adam->exp_avg, rho));
-      J.v = reinterpret_cast<float*>(ctx->rank_ptr(adam->exp_avg_sq, rho));
-      J.pbf16 = adam->param_bf16.stride ? reinterpret_cast<uint16_t*>(ctx->rank_ptr(adam->param_bf16, rho)) : nullptr;
-      J.gout = adam->write_grad ? J.own : nullptr;
-      J.my_flags = reinterpret_cast<uint64_t*>(ctx->rank_ptr(st->bflags, rho));
-      J.elems = st->shard_elems;
-      J.sub = sub;
-      J.r = uint32_t(r);
-      J.pos = uint32_t(rho / p);
-      J.nblk = nblk;
-      jobs.push_back(J);
-      ptrs.push_back(pp);
-    }
-    out.ag = make_boundary_launch(ctx, jobs, ptrs,
-                                  make_adam_scalars(adam->lr, adam->beta1, adam->beta2, adam->eps, adam->weight_decay,
-                                                    adam->step, adam->grad_scale),
-                                  ctx->barrier(rmask | pmask, 1, 1), persistent);
-    out.has_ag = true;
-    return out;
   }
   if (r > 1) {  // reduce-scatter in place: position i folds slice i of every replica's shard
     RedPlan rs(st->acc_t);
@@ -332,7 +285,6 @@ BoundaryLaunches build_boundary_range(mics_sync* st, const mics_adam* adam, mics
 void boundary(mics_sync* st, const mics_adam* adam) {
   check_window(st, true);
   BoundaryLaunches b = build_boundary(st, adam, false, true);
-  b.ag.epoch = ++st->epoch;
   if (b.has_rs) enqueue(st->ctx, b.rs);
   if (b.has_ag) enqueue(st->ctx, b.ag);
   const int r = st->n / st->p;

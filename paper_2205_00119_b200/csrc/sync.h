@@ -15,11 +15,6 @@ struct mics_sync {
   mics_buf shard{};
   int micro_step = 0;
   std::vector<std::array<int64_t, 4>> events;
-  // fused boundary: per-tile publication flags [r][nblk] per rank (lazily allocated), monotone epoch
-  bool fusable = false;
-  bool bflags_ready = false;
-  mics_buf bflags{};
-  uint64_t epoch = 0;
   // alternative schedule scratch (lazily allocated)
   bool alt_ready = false;
   mics_buf alt{};
@@ -65,11 +60,6 @@ struct mics_step {
   mics_buf pbf16{}, master{}, m{}, v{}, gathered{}, grads{};
   uint64_t gathered_half = 0;                 // bytes of one gathered buffer (slot)
   int gather_slots = 2;                       // layer l gathers into slot l % gather_slots
-  // slot ordering by device counters instead of fences (MICS_GATHER_CTR; comm-only step)
-  bool gather_ctr = false;
-  uint64_t* d_slot_ctr = nullptr;             // [gather_slots] completed gathers per slot this step
-  unsigned* d_slot_tickets = nullptr;         // [2 L] CTA tickets per (direction, layer) gather
-  std::vector<uint64_t> slot_host;            // gathers enqueued per slot this step
   std::vector<std::vector<mics::Launch>> ag;  // per layer: 1 launch (flat) or 2 (hierarchical)
   // hierarchical gathers of one micro-step (forward 0..L-1, backward L-1..0) with phase 2
   // of each visit merged into the launch of the next visit's phase 1: 2L+1 launches
@@ -83,19 +73,8 @@ struct mics_step {
   int adam_step = 0;
   mics_step_stats stats{};
   uint64_t host_result_elems = 4096;
-  // Pipelined boundary (2-hop): step k's boundary runs on the side stream (barrier
-  // channel 1), one layer group at a time, while step k+1's micro-steps proceed on
-  // the main stream; layer group g's first gather waits for its Adam.  The gradient
-  // accumulator is double buffered so step k+1's reduce-scatters never overwrite
-  // what step k's boundary is still reading.
-  bool pipelined = false;
-  mics_buf gacc1{};                                   // second accumulator buffer
-  std::vector<std::vector<mics::Launch>> micro1;      // micro-step launches into gacc1
-  std::vector<std::pair<uint64_t, uint64_t>> group_range;  // shard range of each boundary group
+  std::vector<std::pair<uint64_t, uint64_t>> group_range;  // shard range of each tail layer group
   std::vector<int> group_first_layer;
-  std::vector<mics::BoundaryLaunches> bndg[2];        // [buffer][group]
-  cudaEvent_t ev_rs = nullptr, ev_done[2] = {nullptr, nullptr};
-  std::vector<cudaEvent_t> ev_bnd;
   uint64_t step_idx = 0;
   // Overlapped tail (2-hop, partition groups inside a GPU, replication groups across
   // GPUs — N=2/4 of the 8-rank job): the last micro-step's reduce-scatter (HBM) runs
@@ -112,8 +91,8 @@ struct mics_step {
   cudaEvent_t ev_tail_done = nullptr;
   cudaStream_t tail_rs_stream = nullptr;          // boundary reduce-scatters (channel 2), ahead of Adam
   // CUDA-graph replay (default; MICS_GRAPH=0 enqueues every kernel per step):
-  // one captured step whose boundary kernels read the per-step Adam scalars and
-  // flag epoch from d_scalars, set by one small kernel before each replay.
+  // one captured step whose boundary kernels read the per-step Adam scalars from
+  // d_scalars, set by one small kernel before each replay.
   bool graph_tried = false, capturing = false;
   cudaGraphExec_t gexec = nullptr;
   mics::DevScalars* d_scalars = nullptr;

@@ -7,6 +7,7 @@ import ctypes as C
 from dataclasses import dataclass, field
 
 from ._lib import Cluster, check, lib
+from .workloads import transformer_layer_params  # noqa: F401  (re-exported)
 
 
 @dataclass
@@ -93,12 +94,3 @@ def min_feasible_partition(model_state_bytes: int, cluster: ClusterSpec, node_gr
     check(lib.mics_min_feasible_partition(model_state_bytes, C.byref(c), int(node_granular), headroom_fraction,
                                           C.byref(out)))
     return out.value
-
-
-def transformer_layer_params(hidden: int, intermediate: int, layers: int, vocab: int, seq_len: int) -> list:
-    """Parameters per layer as the reference's derive_layers_from_transformer
-    counts them (simulator.cpp:317-358): embedding (V + l) * h, then `layers`
-    blocks of 4h^2 + 2h*i + 9h + i."""
-    emb = (vocab + seq_len) * hidden
-    block = 4 * hidden * hidden + 2 * hidden * intermediate + 9 * hidden + intermediate
-    return [emb] + [block] * layers

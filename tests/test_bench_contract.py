@@ -36,6 +36,32 @@ def test_reference_arm_contract():
     assert d["value"] > 0 and d["unit"] == "samples/s" and d["higher_is_better"] is True
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    # the timed samples fit the run (ms_per_step is the sample actually timed per step)
+    assert d["extrapolated"] is True and d["ms_per_step"] == d["extrapolation"]["sample_ms_per_step"]
+    # the same config dict the GPU arm prints (one function builds both)
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2205_00119_b200.workloads import workloads
+
+    class A:
+        ranks, schedule = 8, "two_hop"
+    assert d["config"] == bench.config_for(workloads()["C1"], A, 1)
+
+
+def test_reference_arm_never_maps_libmics():
+    """The reference arm runs the reference's CPU code only: libmics.so (and the
+    oracle's C restatement) are never mapped into its process."""
+    from oracle.oracle import RefLib
+    if not RefLib.available():
+        pytest.skip("oracle/_ref not built")
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--workload', 'C1', '--steps', '1', "
+            "'--warmup', '0']; runpy.run_path('bench.py', run_name='__main__'); "
+            "print('MAPS', sorted({l.split()[-1] for l in open('/proc/self/maps') if l.rstrip().endswith('.so')}))")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    maps = [ln for ln in out.stdout.splitlines() if ln.startswith("MAPS")][0]
+    assert "libmics.so" not in maps and "liboracle.so" not in maps, maps
+    assert "libsdpsim_ref.so" in maps, maps
 
 
 @pytest.mark.gpu

@@ -98,23 +98,6 @@ def test_gemm_rejects_bad_args(eng):
         gemm_bf16(eng, x.data_ptr() + 2, 64, False, x.data_ptr(), 64, False, x.data_ptr(), 64, "bf16", 64, 64, 64)
 
 
-@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True), (True, False)])
-def test_gemm_bn128_tiles(eng, monkeypatch, a_mn, b_mn):
-    """The opt-in 256 x 128 pair tile (MICS_GEMM_BN=128)."""
-    monkeypatch.setenv("MICS_GEMM_BN", "128")
-    run(eng, 300, 424, 200, a_mn, b_mn, "f32", seed=4)
-    run(eng, 256, 1600, 128, a_mn, b_mn, "bf16", seed=5)
-
-
 def test_gemm_hidden_1600_accumulate(eng):
     """N = 1600 (GPT-2 1.5B hidden: 6.25 tiles of 256, a ragged last column of tiles); accumulate."""
     run(eng, 512, 1600, 320, False, True, "f32", accumulate=True, seed=6)
-
-
-@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (True, True), (False, True)])
-def test_gemm_two_pairs_multicast(eng, monkeypatch, a_mn, b_mn):
-    """Opt-in 4-CTA clusters (MICS_GEMM_PAIRS=2): two CTA pairs share the B tile by TMA
-    multicast (odd number of 256-row blocks included)."""
-    monkeypatch.setenv("MICS_GEMM_PAIRS", "2")
-    run(eng, 700, 600, 200, a_mn, b_mn, "f32", seed=8)
-    run(eng, 1024, 1032, 136, a_mn, b_mn, "bf16", seed=9)
