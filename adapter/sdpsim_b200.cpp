@@ -43,6 +43,10 @@ mics_ctx* ctx() {
   return c;
 }
 
+// The caller's worker count (VirtualRankEngine(num_threads)) becomes the CTAs per
+// SM of the call's kernels; results do not depend on it (collectives.hpp:38-41).
+void use(const VirtualRankEngine& engine) { check(mics_set_parallelism(ctx(), engine.num_threads(), 0)); }
+
 // Move the traffic libmics recorded for one call into the caller's engine log.
 void collect_traffic(VirtualRankEngine& engine) {
   uint64_t n = 0;
@@ -159,6 +163,7 @@ void VirtualRankEngine::clear_traffic() {
 // ---------------------------------------------------------------- collectives -> libmics kernels
 std::vector<Bytes> all_gather(VirtualRankEngine& engine, const CollectiveGroup& group,
                               const std::vector<Bytes>& shards) {
+  use(engine);
   group.validate();
   const int p = group.size();
   if (int(shards.size()) != p)
@@ -179,6 +184,7 @@ std::vector<Bytes> all_gather(VirtualRankEngine& engine, const CollectiveGroup& 
 
 std::vector<Bytes> reduce_scatter(VirtualRankEngine& engine, const CollectiveGroup& group,
                                   const std::vector<Bytes>& buffers, DType dtype) {
+  use(engine);
   group.validate();
   const int p = group.size();
   if (int(buffers.size()) != p)
@@ -199,6 +205,7 @@ std::vector<Bytes> reduce_scatter(VirtualRankEngine& engine, const CollectiveGro
 
 std::vector<Bytes> all_reduce(VirtualRankEngine& engine, const CollectiveGroup& group,
                               const std::vector<Bytes>& buffers, DType dtype) {
+  use(engine);
   group.validate();
   const int p = group.size();
   if (int(buffers.size()) != p)
@@ -220,6 +227,7 @@ std::vector<Bytes> all_reduce(VirtualRankEngine& engine, const CollectiveGroup& 
 std::vector<Bytes> hierarchical_all_gather(VirtualRankEngine& engine, const GroupLayout& layout,
                                            const ClusterSpec& cluster, const std::vector<Bytes>& shards,
                                            const HierarchicalOptions& opts) {
+  use(engine);
   const int n = layout.n;
   if (cluster.total_ranks() != n)
     raise(Errc::ShapeError, "cluster has " + std::to_string(cluster.total_ranks()) + " ranks but layout expects " +
@@ -244,6 +252,7 @@ std::vector<Bytes> hierarchical_all_gather(VirtualRankEngine& engine, const Grou
 std::vector<std::vector<Bytes>> batched_all_gather(VirtualRankEngine& engine,
                                                    const std::vector<CollectiveGroup>& groups,
                                                    const std::vector<std::vector<Bytes>>& shard_sets) {
+  use(engine);
   if (groups.size() != shard_sets.size())
     raise(Errc::SizeMismatch, "batched_all_gather: " + std::to_string(groups.size()) + " groups vs " +
                                   std::to_string(shard_sets.size()) + " shard sets");
@@ -279,6 +288,7 @@ std::vector<std::vector<Bytes>> batched_reduce_scatter(VirtualRankEngine& engine
                                                        const std::vector<CollectiveGroup>& groups,
                                                        const std::vector<std::vector<Bytes>>& buffer_sets,
                                                        DType dtype) {
+  use(engine);
   if (groups.size() != buffer_sets.size())
     raise(Errc::SizeMismatch, "batched_reduce_scatter: " + std::to_string(groups.size()) + " groups vs " +
                                   std::to_string(buffer_sets.size()) + " buffer sets");

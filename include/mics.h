@@ -104,6 +104,13 @@ mics_status mics_ipc_export(mics_ctx* ctx, void* handle /* MICS_IPC_HANDLE_BYTES
 mics_status mics_ipc_import(mics_ctx* ctx, const void* handles /* world * MICS_IPC_HANDLE_BYTES */);
 mics_status mics_rank_process(mics_ctx* ctx, int rank, int* world_rank);
 mics_status mics_local_ranks(mics_ctx* ctx, int* first, int* count);
+/* The engine's worker count — VirtualRankEngine(num_threads) (collectives.hpp:42-47)
+ * on the GPU: every collective planned from now on runs at most `ctas_per_sm` CTAs per
+ * SM (0 = one resident wave at the kernel's occupancy) and at most `max_ctas` CTAs per
+ * launch (0 = no cap).  Like the reference's thread count it changes only how the work
+ * is spread: results and the traffic log are bit-identical for every setting
+ * (collectives.hpp:38-41; tests/test_gpu_determinism.py). */
+mics_status mics_set_parallelism(mics_ctx* ctx, int ctas_per_sm, int max_ctas);
 
 /* Symmetric allocation: every process must make the same sequence of calls. */
 mics_status mics_alloc(mics_ctx* ctx, uint64_t bytes_per_rank, mics_buf* out);

@@ -97,6 +97,7 @@ _SIGS = [
     ("mics_ipc_import", I, [VP, VP]),
     ("mics_rank_process", I, [VP, I, PI]),
     ("mics_local_ranks", I, [VP, PI, PI]),
+    ("mics_set_parallelism", I, [VP, I, I]),
     ("mics_alloc", I, [VP, U64, C.POINTER(Buf)]),
     ("mics_arena_mark", I, [VP, PU64]),
     ("mics_arena_release", I, [VP, U64]),

@@ -172,6 +172,14 @@ mics_status mics_local_ranks(mics_ctx* ctx, int* first, int* count) {
     if (count) *count = ctx->per;
   });
 }
+mics_status mics_set_parallelism(mics_ctx* ctx, int ctas_per_sm, int max_ctas) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (ctas_per_sm < 0 || max_ctas < 0) mics::raise(MICS_OUT_OF_RANGE, "parallelism must be >= 0");
+    ctx->par_ctas_per_sm = ctas_per_sm;
+    ctx->par_max_ctas = max_ctas;
+  });
+}
 mics_status mics_alloc(mics_ctx* ctx, uint64_t bytes, mics_buf* out) {
   return guard([&] {
     need(ctx, "ctx");

@@ -294,7 +294,7 @@ Launch build_all_gather(mics_ctx* ctx, const int* ranks, int p, const void* cons
   check_ptrs(const_cast<const void* const*>(out), p, ctx, ranks, true, "all_gather output");
   CopyPlan plan;
   plan_all_gather(ctx, plan, ranks, p, shard, chunk, out);
-  return make_copy_launch(ctx, plan, ctx->barrier(ctx->peer_mask(ranks, p), 1, 1), persistent);
+  return make_copy_launch(ctx, plan, ctx->barrier(ctx->peer_mask(ranks, p), 1, 1, 0, 0), persistent);
 }
 
 void all_gather(mics_ctx* ctx, const int* ranks, int p, const void* const* shard, uint64_t chunk, void* const* out) {
@@ -315,7 +315,7 @@ Launch build_reduce_scatter(mics_ctx* ctx, const int* ranks, int p, const void* 
   check_ptrs(const_cast<const void* const*>(out), p, ctx, ranks, true, "reduce_scatter output");
   RedPlan plan(in_t);
   plan_reduce_scatter(ctx, plan, ranks, p, in, in_elems, valid, in_t, out);
-  return make_reduce_launch(ctx, plan, in_t, acc_t, scale, mode, ctx->barrier(ctx->peer_mask(ranks, p), 1, 1),
+  return make_reduce_launch(ctx, plan, in_t, acc_t, scale, mode, ctx->barrier(ctx->peer_mask(ranks, p), 1, 1, 0, 0),
                             persistent);
 }
 
@@ -359,7 +359,7 @@ void all_reduce(mics_ctx* ctx, const int* ranks, int p, void* const* buf, uint64
     if (!dsts.empty()) items.emplace_back(static_cast<const char*>(buf[i]) + uint64_t(i) * cb, std::move(dsts));
   }
   ag.add_group(items, cb);
-  enqueue(ctx, make_copy_launch(ctx, ag, ctx->barrier(mask, 0, 1), false));
+  enqueue(ctx, make_copy_launch(ctx, ag, ctx->barrier(mask, 0, 1, 0, 0), false));
 }
 
 // Hierarchical all-gather.  For partition group g (base = g*p) with q = p/k
@@ -399,7 +399,7 @@ void hier_all_gather(mics_ctx* ctx, int n, int p, int k, const void* const* shar
       plan_all_gather(ctx, plan, all.data() + g * p, p, shard + g * p, chunk, out + g * p);
       mask |= ctx->peer_mask(all.data() + g * p, p);
     }
-    enqueue(ctx, make_copy_launch(ctx, plan, ctx->barrier(mask, 1, 1), false));
+    enqueue(ctx, make_copy_launch(ctx, plan, ctx->barrier(mask, 1, 1, 0, 0), false));
     return;
   }
   const int q = p / k;
@@ -439,7 +439,7 @@ void hier_all_gather(mics_ctx* ctx, int n, int p, int k, const void* const* shar
     }
   }
   enqueue(ctx, make_copy_launch(ctx, ph1, ctx->barrier(mask, 1, 1), false));
-  enqueue(ctx, make_copy_launch(ctx, ph2, ctx->barrier(mask, 0, 1), false));
+  enqueue(ctx, make_copy_launch(ctx, ph2, ctx->barrier(mask, 0, 1, 0, 0), false));
 }
 
 void batched_all_gather(mics_ctx* ctx, const mics_ag_desc* d, int count) {
@@ -453,7 +453,7 @@ void batched_all_gather(mics_ctx* ctx, const mics_ag_desc* d, int count) {
     plan_all_gather(ctx, plan, d[b].ranks, d[b].p, d[b].d_shard, d[b].chunk_bytes, d[b].d_out);
     mask |= ctx->peer_mask(d[b].ranks, d[b].p);
   }
-  enqueue(ctx, make_copy_launch(ctx, plan, ctx->barrier(mask, 1, 1), false));
+  enqueue(ctx, make_copy_launch(ctx, plan, ctx->barrier(mask, 1, 1, 0, 0), false));
 }
 
 void batched_reduce_scatter(mics_ctx* ctx, const mics_rs_desc* d, int count, mics_dtype in_t, mics_dtype acc_t,
@@ -474,7 +474,7 @@ void batched_reduce_scatter(mics_ctx* ctx, const mics_rs_desc* d, int count, mic
     plan_reduce_scatter(ctx, plan, d[b].ranks, d[b].p, d[b].d_in, d[b].in_elems, d[b].valid_elems, in_t, d[b].d_out);
     mask |= ctx->peer_mask(d[b].ranks, d[b].p);
   }
-  enqueue(ctx, make_reduce_launch(ctx, plan, in_t, acc_t, scale, mode, ctx->barrier(mask, 1, 1), false));
+  enqueue(ctx, make_reduce_launch(ctx, plan, in_t, acc_t, scale, mode, ctx->barrier(mask, 1, 1, 0, 0), false));
 }
 
 // ---------------------------------------------------------------------------

@@ -143,6 +143,13 @@ struct BarrierArg {
   // 1 = full system fences around every signal (the conservative protocol, kept
   // for A/B runs: MICS_BAR_STRICT=1); 0 = relaxed signals, see bar_entry/bar_exit
   int strict;
+  // 1 = the exit barrier also publishes this launch's stores to the peers (a fence per
+  // CTA + one system fence, kernels.cu bar_exit): set where a peer reads what this
+  // launch wrote without an entry barrier of its own in between (all-reduce's
+  // reduce-scatter phase, hierarchical phase 1, the boundary's reduce-scatter and Adam).
+  // 0 for launches whose outputs are only read by later launches that enter through
+  // their own barrier (plain all-gather / reduce-scatter, the micro-step reduce-scatter).
+  int publish = 1;
 };
 
 // --------------------------------------------------------------------------
@@ -193,6 +200,8 @@ struct mics_ctx {
   int occ_copy = 2, occ_adam = 4, occ_reduce[4][4] = {};
   int occ_copy_indep = 1;  // CTAs/SM of barrier-free gathers chained with PDL
   int bar_strict = 0;      // BarrierArg::strict (MICS_BAR_STRICT)
+  int par_ctas_per_sm = 0; // mics_set_parallelism: CTAs per SM cap (0 = occupancy)
+  int par_max_ctas = 0;    // mics_set_parallelism: CTAs per launch cap (0 = none)
   int reduce_occ(mics_dtype t, uint32_t max_p) const {
     const int pc = mics::reduce_class(max_p);
     return occ_reduce[t][pc == 2 ? 0 : pc == 4 ? 1 : pc == 8 ? 2 : 3];
@@ -231,7 +240,10 @@ struct mics_ctx {
     traffic[{from, to}] += bytes;
   }
   int grid_for(uint64_t tiles, int per_sm = 0) const {
-    uint64_t g = uint64_t(nsm) * (per_sm ? per_sm : blocks_per_sm);
+    int k = per_sm ? per_sm : blocks_per_sm;
+    if (par_ctas_per_sm > 0 && par_ctas_per_sm < k) k = par_ctas_per_sm;
+    uint64_t g = uint64_t(nsm) * uint64_t(k);
+    if (par_max_ctas > 0 && uint64_t(par_max_ctas) < g) g = uint64_t(par_max_ctas);
     if (tiles < g) g = tiles;
     return g ? int(g) : 1;
   }
@@ -239,7 +251,7 @@ struct mics_ctx {
   void* ring_put(const void* host, uint64_t bytes);
   void* ring_reserve(uint64_t bytes);
   void ring_upload(void* dev, const void* host, uint64_t bytes);
-  mics::BarrierArg barrier(uint64_t mask, int entry, int exit, int chan = 0) const {
+  mics::BarrierArg barrier(uint64_t mask, int entry, int exit, int chan = 0, int publish = 1) const {
     mics::BarrierArg b;
     b.tab = d_tab + chan;
     b.nbar = d_nbar + chan * MICS_MAX_WORLD;
@@ -249,6 +261,7 @@ struct mics_ctx {
     b.exit = exit;
     b.dep_first = 1;
     b.strict = bar_strict;
+    b.publish = publish;
     return b;
   }
   // processes hosting any of `ranks`, minus self (0 when self hosts none)

@@ -89,7 +89,8 @@ __device__ __forceinline__ void pdl_end(const BarrierArg& b) {
 //    ticket), and the last CTA — which has observed every ticket — issues one
 //    system-scope fence before its relaxed signals: fence-to-fence synchronisation
 //    through the ticket chain, then a release pattern (fence.sys; st.relaxed.sys)
-//    towards the peers.  One MEMBAR.GPU per CTA and one MEMBAR.SYS per launch.
+//    towards the peers.  One MEMBAR.GPU per CTA and one MEMBAR.SYS per launch, only
+//    for launches that publish (BarrierArg::publish; 2 us of a 1 MiB all-gather).
 // The waiter polls relaxed and acquires once, so its L1 holds nothing stale.
 // strict = 1 (MICS_BAR_STRICT) adds system fences around every signal (A/B runs).
 __device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
@@ -134,13 +135,13 @@ __device__ void bar_exit(const BarrierArg& b) {
   if (b.mask == 0) return;
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (b.exit) __threadfence();  // this CTA's stores before its ticket (publication, see above)
+    if (b.exit && b.publish) __threadfence();  // this CTA's stores before its ticket (publication, see above)
     if (b.strict) __threadfence_system();
     const unsigned t = atomicAdd(&b.tickets[1], 1u);
     if (t == gridDim.x - 1) {  // last CTA: every CTA of this GPU finished its accesses
       const uint64_t k = uint64_t(b.entry ? 1 : 0) + uint64_t(b.exit ? 1 : 0);
       if (b.exit) {
-        __threadfence_system();  // every CTA's fenced stores, observed through the tickets, before the signal
+        if (b.publish) __threadfence_system();  // every CTA's fenced stores, seen through the tickets, first
         bar_signal(b, k);
         bar_wait(b, k);
       }

@@ -113,7 +113,10 @@ Launch build_micro_launch(mics_sync* st, mics_buf grads, uint64_t goff, mics_dty
       }
     }
   }
-  return make_reduce_launch(ctx, plan, grad_t, st->acc_t, scale, mode, ctx->barrier(mask, entry, exit), persistent);
+  // later readers of the accumulated shards (the boundary's reduce-scatter) enter through
+  // their own barrier: no publication needed
+  return make_reduce_launch(ctx, plan, grad_t, st->acc_t, scale, mode, ctx->barrier(mask, entry, exit, 0, 0),
+                            persistent);
 }
 
 void micro_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode) {

@@ -4,8 +4,11 @@
 An :class:`Engine` owns one ``mics_ctx``: n virtual ranks laid out node-major
 over ``world`` processes (one per GPU), a symmetric device arena, a CUDA
 stream and the per-(sender, receiver) traffic log the reference keeps.
-``num_threads`` is accepted for API parity; results never depend on it (the
-reference's contract, collectives.hpp:38-41).
+``num_threads`` is the engine's worker count, as in the reference: here the CTAs
+per SM every collective runs with (``None`` = one resident wave at each kernel's
+occupancy; ``set_parallelism`` also caps CTAs per launch).  Results and traffic
+never depend on it — the reference's contract (collectives.hpp:38-41), pinned by
+tests/test_gpu_determinism.py.
 """
 from __future__ import annotations
 
@@ -27,9 +30,9 @@ def dtype_code(dtype) -> int:
 
 
 class Engine:
-    def __init__(self, num_threads: int = 1, *, n_ranks: int = 64, world: int = 1, world_rank: int = 0,
+    def __init__(self, num_threads: int | None = None, *, n_ranks: int = 64, world: int = 1, world_rank: int = 0,
                  device: int = 0, arena_bytes: int = 1 << 30):
-        self.num_threads = max(1, int(num_threads))
+        self.num_threads = None if num_threads is None else max(1, int(num_threads))
         self.n = n_ranks
         self.world = world
         self.world_rank = world_rank
@@ -41,6 +44,13 @@ class Engine:
         first, count = C.c_int(0), C.c_int(0)
         check(lib.mics_local_ranks(self.ctx, C.byref(first), C.byref(count)))
         self.local_ranks = list(range(first.value, first.value + count.value))
+        if self.num_threads is not None:
+            self.set_parallelism(self.num_threads)
+
+    def set_parallelism(self, ctas_per_sm: int = 0, max_ctas: int = 0) -> None:
+        """Worker CTAs per SM (0 = occupancy) and per launch (0 = no cap) of every
+        collective planned from now on (mics_set_parallelism)."""
+        check(lib.mics_set_parallelism(self.ctx, int(ctas_per_sm), int(max_ctas)))
 
     # ------------------------------------------------------------ lifetime
     def close(self) -> None:

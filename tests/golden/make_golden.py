@@ -146,6 +146,16 @@ def main():
     g = grads_f32(4, 8, 1001, 2205)
     arr["sched/c1probe/two_hop"] = ref.schedule("two_hop", g, 8, 2, "f32")[0]
     arr["sched/c1probe/alternative"] = ref.schedule("alternative", g, 8, 2, "f32")[0]
+    # BASELINE config C1 at full size (4 x 1,049,600 = 4,198,400 params as
+    # one gradient segment, n=8, p=2, s=4, fp32 U(-1,1) from mt19937(2205)): per-rank
+    # digests of the shards after the reference's two_hop and alternative schedules
+    # (8 engine threads; the reference pins results for any thread count)
+    g = grads_f32(4, 8, 4_198_400, 2205)
+    for mode in ("two_hop", "alternative"):
+        out = ref.schedule(mode, g, 8, 2, "f32", threads=8)[0]
+        dig[f"cfg/c1_full/{mode}"] = [digest(o) for o in out]
+        arr[f"cfg/c1_full/{mode}_every_9973"] = out[:, ::9973].copy()
+    del g
     # f64 case
     g64 = grads_f32(2, 4, 10, 77).astype(np.float64)
     arr["sched/f64/two_hop"] = ref.schedule("two_hop", g64, 4, 2, "f64")[0]

@@ -212,3 +212,19 @@ def test_live_against_reference(oracle):
             assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
             assert np.array_equal(ev_a, ev_b)
             assert {(x, y): int(tr_a[x, y]) for x in range(n) for y in range(n) if tr_a[x, y]} == tr_b
+
+
+def test_oracle_c1_full_size_matches_reference_digests(oracle, golden):
+    """BASELINE config C1 at full size (4,198,400 params, n=8, p=2, s=4, mt19937(2205)
+    U(-1,1)): the C restatement's two_hop and alternative shards hash to the digests
+    the unmodified reference produced."""
+    import hashlib
+    arr, dig = golden
+    n, p, s, length = 8, 2, 4, 4_198_400
+    g = oracle.random_f32(s * n * length, -1.0, 1.0, 2205).reshape(s, n, length)
+    for mode in ("two_hop", "alternative"):
+        out = getattr(oracle, mode)(g, n, p, "f32")[0]
+        assert [hashlib.sha256(np.ascontiguousarray(o).tobytes()).hexdigest()[:32] for o in out] == \
+            dig[f"cfg/c1_full/{mode}"], mode
+        assert np.array_equal(out[:, ::9973].view(np.uint32), arr[f"cfg/c1_full/{mode}_every_9973"].view(np.uint32))
+
