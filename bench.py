@@ -333,9 +333,33 @@ def run_reference(args, wl, rank, world):
 
 
 # ----------------------------------------------------------------------------- NCCL comparator
+def graph_or_eager(fn, warmup):
+    """The comparator's step captured once in a CUDA graph and replayed (no per-call
+    host launch cost inside the timed region, like libmics' graph-replayed step);
+    `warmup` eager calls on a side stream first.  Falls back to eager calls if the
+    capture is refused.  Returns (callable, "cuda_graph" | "eager")."""
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(max(1, warmup)):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        torch.cuda.synchronize()
+        return g.replay, "cuda_graph"
+    except Exception:  # noqa: BLE001
+        torch.cuda.synchronize()
+        return fn, "eager"
+
+
 def nccl_step(wl, rank, world, steps, warmup):
     """The same MiCS step with stock NCCL collectives on split communicators and
-    torch's fused Adam (only meaningful with one rank per GPU)."""
+    torch's fused Adam (only meaningful with one rank per GPU), graph-captured."""
     import torch
     import torch.distributed as dist
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -352,7 +376,8 @@ def nccl_step(wl, rank, world, steps, warmup):
     acc = torch.zeros(S, dtype=torch.float32, device=dev)
     tmp = torch.empty(S, dtype=gdt, device=dev)
     master = torch.nn.Parameter(torch.randn(S, device=dev))
-    opt = torch.optim.Adam([master], lr=1e-4, fused=True)
+    opt = torch.optim.Adam([master], lr=1e-4, fused=True, capturable=True)
+    master.grad = acc
     offs = [0]
     for c in chunks:
         offs.append(offs[-1] + c)
@@ -368,24 +393,22 @@ def nccl_step(wl, rank, world, steps, warmup):
             acc.add_(tmp.float()) if t else acc.copy_(tmp.float())
         if n // p > 1:
             dist.all_reduce(acc, group=my_rg)
-        master.grad = acc
         opt.step()
         shard.copy_(master.detach().to(torch.bfloat16))
 
-    for _ in range(warmup):
-        one()
+    run, mode = graph_or_eager(one, warmup)
     torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(steps):
-        one()
+        run()
     e1.record()
     e1.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
-    return {"value": n * MICRO_BATCH * s / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
+    return {"value": n * MICRO_BATCH * s / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms, "launch": mode,
             "what": "torch.distributed NCCL all_gather_into_tensor / reduce_scatter_tensor / all_reduce on split "
-                    "groups + torch.optim.Adam(fused=True), same shapes"}
+                    "groups + torch.optim.Adam(fused, capturable), same shapes, one CUDA graph per step"}
 
 
 def nccl_compute_step(wl, rank, world, steps, warmup):
@@ -421,7 +444,8 @@ def nccl_compute_step(wl, rank, world, steps, warmup):
     acc = torch.zeros(S, dtype=torch.float32, device=dev)
     tmp = torch.empty(S, dtype=gdt, device=dev)
     master = torch.nn.Parameter(shard.float())
-    opt = torch.optim.Adam([master], lr=1e-4, fused=True)
+    opt = torch.optim.Adam([master], lr=1e-4, fused=True, capturable=True)
+    master.grad = acc
     side = torch.cuda.Stream()
     ev_g = [torch.cuda.Event() for _ in range(2)]
     ev_free = [torch.cuda.Event() for _ in range(2)]
@@ -468,22 +492,20 @@ def nccl_compute_step(wl, rank, world, steps, warmup):
             acc.add_(tmp.float()) if t else acc.copy_(tmp.float())
         if n // p > 1:
             dist.all_reduce(acc, group=my_rg)
-        master.grad = acc
         opt.step()
         shard.copy_(master.detach().to(torch.bfloat16))
 
-    for _ in range(warmup):
-        one()
+    run, mode = graph_or_eager(one, warmup)
     torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(steps):
-        one()
+        run()
     e1.record()
     e1.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
-    return {"value": n * MICRO_BATCH * s / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
+    return {"value": n * MICRO_BATCH * s / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms, "launch": mode,
             "what": "same model and schedule on torch.matmul (cuBLAS, rows padded to 8) + NCCL all_gather (side "
                     "stream, one layer ahead) / reduce_scatter / all_reduce + torch.optim.Adam(fused=True)"}
 

@@ -105,7 +105,7 @@ def test_two_hop_sync_identical_for_any_parallelism(m, oracle):
                            adam=make_adam(st, AdamConfig(lr=1e-3, grad_scale=1.0 / (n * s), write_grad=True), *bufs))
         eng.synchronize()
         got = [u8(eng.d2h(b, r, c)) for b in bufs for r in range(n)] + [u8(st.shard(r)) for r in range(n)]
-        res.append((got, [(e.step, e.phase, e.group, e.bytes_received_per_rank) for e in st.events()]))
+        res.append((got, [(e.step, e.phase, e.group_id, e.bytes) for e in st.events()]))
         for r in range(n):
             assert np.array_equal(u8(st.shard(r)), u8(red[r])), (cps, cap, r)
         eng.close()

@@ -6,6 +6,8 @@ n/p groups concurrent — libmics (persistent plans) vs NCCL on split communicat
 
 busBW = (p-1) * M / p / t per rank; one JSON line per point, times are
 CUDA-event averages over back-to-back calls (median of 3 trials), max over ranks.
+NCCL's calls are captured in a CUDA graph and replayed (no per-call host launch in
+the timed region), like libmics' persistent plans.
 """
 from __future__ import annotations
 
@@ -38,6 +40,33 @@ def _time(fn, stream_ext, reps, world, gloo, trials=3):
         dist.all_reduce(x, op=dist.ReduceOp.MAX, group=gloo)
         t = float(x.item())
     return t * 1e3  # us
+
+
+def nccl_runner(call, reps, world):
+    """NCCL timed without host launch cost: `reps` back-to-back calls captured once in
+    a CUDA graph (torch.cuda.graph) and replayed, as libmics replays its persistent
+    plans.  Returns (fn(k) running the reps calls, "cuda_graph"), or the eager loop
+    ("eager") when the capture is refused."""
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up (communicator setup) outside the capture
+        for _ in range(3):
+            call()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(reps):
+                call()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        return (lambda k: g.replay()), "cuda_graph"
+    except Exception:  # noqa: BLE001  (capture unsupported on this stack: time the eager loop)
+        torch.cuda.synchronize()
+        return (lambda k: [call() for _ in range(k)]), "eager"
 
 
 def run_sweep(args, rank, world, local, sizes=None, quiet=False):
@@ -85,22 +114,22 @@ def run_sweep(args, rank, world, local, sizes=None, quiet=False):
                 eng.synchronize()
                 bench.barrier(world)
                 us = _time(plan.run, ext, reps, world, gloo)
+                nmode = None
                 if pg is not None:
                     a_in, a_out = t_in.view(torch.uint8)[:chunk], t_out.view(torch.uint8)[:m]
                     r_in, r_out = t_in[:m // 4], t_out[:m // 4 // p]
                     nccl = (lambda: dist.all_gather_into_tensor(a_out, a_in, group=pg)) if op == "allgather" else \
                         (lambda: dist.reduce_scatter_tensor(r_out, r_in, group=pg))
-                    for _ in range(3):
-                        nccl()
-                    torch.cuda.synchronize()
+                    run, nmode = nccl_runner(nccl, reps, world)
                     bench.barrier(world)
-                    nus = _time(lambda k: [nccl() for _ in range(k)], torch.cuda.current_stream(), reps, world, gloo)
+                    nus = _time(run, torch.cuda.current_stream(), reps, world, gloo)
                 else:
                     nus = None
                 bus = (p - 1) * m / p / (us * 1e-6) / 1e9
                 line = {"sweep": "C2", "op": op, "p": p, "gpus": world, "bytes": m, "mics_us": us,
                         "mics_busbw_GBps": bus, "frac_nvlink_770": bus / NVLINK,
-                        "nccl_us": nus, "nccl_busbw_GBps": (p - 1) * m / p / (nus * 1e-6) / 1e9 if nus else None}
+                        "nccl_us": nus, "nccl_busbw_GBps": (p - 1) * m / p / (nus * 1e-6) / 1e9 if nus else None,
+                        "nccl_launch": nmode}
                 results.append(line)
                 if rank == 0 and not quiet:
                     print(json.dumps(line), flush=True)
