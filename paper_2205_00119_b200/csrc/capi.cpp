@@ -206,7 +206,7 @@ mics_status mics_arena_used(mics_ctx* ctx, uint64_t* used, uint64_t* capacity) {
   return guard([&] {
     need(ctx, "ctx");
     if (used) *used = ctx->used;
-    if (capacity) *capacity = ctx->cap;
+    if (capacity) *capacity = ctx->top;  // what the bump allocator may use
   });
 }
 mics_status mics_buf_ptr(mics_ctx* ctx, mics_buf buf, int rank, void** out) {

@@ -50,6 +50,70 @@ void CopyPlan::add_group(const std::vector<std::pair<const void*, std::vector<vo
   tiles = t0 + k * uint32_t(ceil_div(bytes, kCopyTile));
 }
 
+void HierPlan::add_group(int stage, const std::vector<std::tuple<const void*, void*, uint64_t*>>& items,
+                         uint64_t bytes) {
+  if (bytes == 0 || items.empty()) return;
+  const uint32_t t0 = tiles, per = uint32_t(ceil_div(bytes, kCopyTile)), k = uint32_t(items.size());
+  for (const auto& [s, d, f] : items) {
+    HierSeg g;
+    std::memset(&g, 0, sizeof(g));
+    g.src = static_cast<const uint8_t*>(s);
+    g.dst = static_cast<uint8_t*>(d);
+    g.flags = f;
+    g.bytes = bytes;
+    g.tile0 = t0;
+    g.gsize = k;
+    g.stage = uint32_t(stage);
+    segs.push_back(g);
+  }
+  tiles = t0 + k * per;
+}
+
+// Stage 1 (collectives.cpp:229-241): rank r = base + m*k + j gathers channel j's chunks
+// from the q ranks base + m2*k + j, stage 2 (:243-265) folded into the store position
+// (m2*k + j, or j*q + m2 with corrupt_stage2); stage 3 (:267-288): r pulls positions
+// t*k + j2 (corrupt: j2*q + t) from each node peer base + m*k + j2, j2 != j — the
+// peer's stage-1 chunk t, guarded by that chunk's tile flags.
+HierPlan plan_hier(mics_ctx* ctx, int n, int p, int k, uint64_t chunk, int corrupt,
+                   const std::function<const void*(int)>& src, const std::function<char*(int, uint64_t)>& dst,
+                   const std::function<uint64_t*(int)>& flags, uint64_t ftiles) {
+  HierPlan plan;
+  const int q = p / k;
+  using Item = std::tuple<const void*, void*, uint64_t*>;
+  std::vector<std::vector<Item>> st3;
+  for (int g = 0; g < n / p; ++g) {
+    const int base = g * p;
+    for (int m = 0; m < q; ++m)
+      for (int j = 0; j < k; ++j) {
+        const int r = base + m * k + j;
+        if (!ctx->local(r)) continue;
+        std::vector<Item> s1, s3;
+        for (int m2 = 0; m2 < q; ++m2) {
+          const uint64_t pos = corrupt ? uint64_t(j) * q + m2 : uint64_t(m2) * k + j;
+          const int from = base + m2 * k + j;
+          s1.emplace_back(src(from), dst(r, pos), flags(r) + uint64_t(m2) * ftiles);
+          (ctx->local(from) ? plan.hbm_bytes : plan.remote_bytes) += chunk;
+          plan.hbm_bytes += chunk;
+        }
+        for (int j2 = 0; j2 < k; ++j2) {
+          if (j2 == j) continue;
+          const int from = base + m * k + j2;
+          plan.sys |= !ctx->local(from);
+          for (int t = 0; t < q; ++t) {
+            const uint64_t pos = corrupt ? uint64_t(j2) * q + t : uint64_t(t) * k + j2;
+            s3.emplace_back(dst(from, pos), dst(r, pos), flags(from) + uint64_t(t) * ftiles);
+            (ctx->local(from) ? plan.hbm_bytes : plan.remote_bytes) += chunk;
+            plan.hbm_bytes += chunk;
+          }
+        }
+        plan.add_group(1, s1, chunk);
+        st3.push_back(std::move(s3));
+      }
+  }
+  for (const auto& s3 : st3) plan.add_group(3, s3, chunk);  // every stage-1 tile precedes every stage-3 tile
+  return plan;
+}
+
 void RedPlan::add(const std::vector<const void*>& src, void* dst, uint64_t elems, uint64_t valid) {
   if (elems == 0) return;
   RedJob j;
@@ -157,6 +221,26 @@ Launch make_copy_launch(mics_ctx* ctx, const CopyPlan& plan, const BarrierArg& b
   return l;
 }
 
+Launch make_hier_launch(mics_ctx* ctx, const HierPlan& plan, const BarrierArg& bar, int chan, bool persistent) {
+  Launch l;
+  l.kind = Launch::HIER;
+  l.ndesc = int(plan.segs.size());
+  l.ntiles = plan.tiles;
+  // one resident wave: stage-3 tiles wait for stage-1 tiles of other CTAs
+  l.grid = ctx->grid_for(plan.tiles, ctx->occ_hier);
+  l.bar = bar;
+  l.hier_sys = plan.sys ? 1 : 0;
+  l.hier_chan = chan;
+  l.remote_bytes = plan.remote_bytes;
+  l.hbm_bytes = plan.hbm_bytes;
+  if (l.ndesc) {
+    const uint64_t bytes = sizeof(HierSeg) * plan.segs.size();
+    l.d_desc = table_memory(ctx, bytes, persistent);
+    table_upload(ctx, l.d_desc, plan.segs.data(), bytes, persistent);
+  }
+  return l;
+}
+
 Launch make_reduce_launch(mics_ctx* ctx, const RedPlan& plan, mics_dtype in_t, mics_dtype acc_t, double scale,
                           int mode, const BarrierArg& bar, bool persistent) {
   Launch l;
@@ -223,6 +307,10 @@ void enqueue(mics_ctx* ctx, const Launch& l, int dep_first, cudaStream_t stream)
       break;
     case Launch::BARRIER:
       launch_barrier(st, bar);
+      break;
+    case Launch::HIER:
+      launch_hier(st, static_cast<const HierSeg*>(l.d_desc), l.ndesc, l.ntiles, l.grid, ctx->d_hctl + l.hier_chan,
+                  l.hier_sys, bar);
       break;
     case Launch::TAIL:
       launch_tail(st, l.in_t, l.tail_r, l.tail_p, static_cast<const TailJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid,
@@ -403,7 +491,6 @@ void hier_all_gather(mics_ctx* ctx, int n, int p, int k, const void* const* shar
     return;
   }
   const int q = p / k;
-  CopyPlan ph1, ph2;
   for (int g = 0; g < n / p; ++g) {
     const int base = g * p;
     mask |= ctx->peer_mask(all.data() + base, p);
@@ -416,30 +503,15 @@ void hier_all_gather(mics_ctx* ctx, int n, int p, int k, const void* const* shar
       for (int j = 0; j < k; ++j)
         for (int j2 = 0; j2 < k; ++j2)
           if (j2 != j) ctx->record(base + m * k + j, base + m * k + j2, uint64_t(q) * chunk);
-    for (int m = 0; m < q; ++m) {
-      for (int j = 0; j < k; ++j) {
-        const int r = base + m * k + j;
-        if (!ctx->local(r)) continue;
-        std::vector<std::pair<const void*, std::vector<void*>>> g1, g2;
-        for (int m2 = 0; m2 < q; ++m2) {  // phase 1: channel j
-          const uint64_t pos = corrupt ? uint64_t(j) * q + m2 : uint64_t(m2) * k + j;
-          g1.push_back({shard[base + m2 * k + j], {O(r, pos)}});
-        }
-        for (int j2 = 0; j2 < k; ++j2) {  // phase 2: node peers
-          if (j2 == j) continue;
-          const int src = base + m * k + j2;
-          for (int t = 0; t < q; ++t) {
-            const uint64_t pos = corrupt ? uint64_t(j2) * q + t : uint64_t(t) * k + j2;
-            g2.push_back({O(src, pos), {O(r, pos)}});
-          }
-        }
-        ph1.add_group(g1, chunk);
-        ph2.add_group(g2, chunk);
-      }
-    }
   }
-  enqueue(ctx, make_copy_launch(ctx, ph1, ctx->barrier(mask, 1, 1), false));
-  enqueue(ctx, make_copy_launch(ctx, ph2, ctx->barrier(mask, 0, 1, 0, 0), false));
+  // one launch: entry barrier (inputs ready everywhere), stage-1 tiles publish flags,
+  // stage-3 tiles consume them, exit barrier (done reading the peers' buffers)
+  const uint64_t ft = hier_flag_tiles(chunk);
+  const mics_buf fb = hier_flags(ctx, uint64_t(q) * ft * 8);
+  HierPlan plan = plan_hier(
+      ctx, n, p, k, chunk, corrupt, [&](int r) { return shard[r]; }, O,
+      [&](int r) { return reinterpret_cast<uint64_t*>(ctx->rank_ptr(fb, r)); }, ft);
+  enqueue(ctx, make_hier_launch(ctx, plan, ctx->barrier(mask, 1, 1, 0, 0), 0, false));
 }
 
 void batched_all_gather(mics_ctx* ctx, const mics_ag_desc* d, int count) {

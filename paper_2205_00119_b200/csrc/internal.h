@@ -5,8 +5,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <string>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -57,6 +59,30 @@ struct CopySeg {              // 64 B
   uint32_t pad_;
 };
 static_assert(sizeof(CopySeg) == 64, "CopySeg layout");
+
+// Hierarchical all-gather in ONE launch (K3, collectives.cpp:192-291): stage-1
+// segments (the channel all-gather among the q ranks sharing a local index, stage 2's
+// rearrangement folded into the store address) publish one flag per kCopyTile tile
+// once its bytes are stored; stage-3 segments (a node peer's stage-1 chunk, pulled
+// into this rank's output) wait for the flag of the tile they read.  All stage-1
+// tiles precede all stage-3 tiles in tile order, so a CTA never waits before its own
+// stage-1 tiles are done; flags hold the launch's epoch (monotone per channel).
+struct HierSeg {              // 64 B
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t* flags;            // stage 1: the flags this chunk publishes; stage 3: its source chunk's flags
+  uint64_t bytes;
+  uint32_t tile0;             // first tile of this segment's stripe group
+  uint32_t gsize;             // segments in the stripe group (equal sizes, tiles interleaved)
+  uint32_t stage;             // 1 or 3
+  uint32_t pad_[5];
+};
+static_assert(sizeof(HierSeg) == 64, "HierSeg layout");
+struct HierCtl {              // per barrier channel, device memory
+  uint64_t epoch;             // epoch of the last completed hierarchical launch
+  unsigned ticket;            // CTA arrivals of the running launch
+  unsigned pad_;
+};
 
 struct RedJob {               // one output chunk (one destination rank, one segment)
   const uint8_t* const* srcs; // p source pointers, already offset to this chunk
@@ -155,13 +181,16 @@ struct BarrierArg {
 // --------------------------------------------------------------------------
 // kernel launchers (kernels.cu)
 void launch_copy(cudaStream_t s, const CopySeg* segs, int nseg, uint32_t ntiles, int grid, const BarrierArg& bar);
+// sys_scope: some stage-3 reader of a flag is on another GPU (system-scope publication)
+void launch_hier(cudaStream_t s, const HierSeg* segs, int nseg, uint32_t ntiles, int grid, HierCtl* ctl,
+                 int sys_scope, const BarrierArg& bar);
 // `table_bytes`: size of the uploaded job table + source-pointer arrays (staged in smem when small)
 void launch_reduce(cudaStream_t s, mics_dtype in_t, mics_dtype acc_t, const RedJob* jobs, int njobs,
                    uint64_t table_bytes, uint32_t max_p, uint32_t ntiles, int grid, double scale, int mode,
                    const BarrierArg& bar);
 uint32_t reduce_tile_elems(mics_dtype in_t);
 int reduce_class(uint32_t max_p);  // 2, 4, 8 or 9 (> 8 sources)
-int resident_ctas(int kind /* 0 copy, 1 reduce, 2 adam */, mics_dtype in_t, int pclass = 2);
+int resident_ctas(int kind /* 0 copy, 1 reduce, 2 adam, 4 hier */, mics_dtype in_t, int pclass = 2);
 void launch_adam(cudaStream_t s, const AdamJob* jobs, int njobs, uint32_t ntiles, int grid, const AdamScalars& sc,
                  const DevScalars* dyn, const BarrierArg& bar);
 void launch_set_scalars(cudaStream_t s, DevScalars* dst, const DevScalars& v);
@@ -199,6 +228,7 @@ struct mics_ctx {
   // resident CTAs/SM per kernel: copy, adam, reduce by [input dtype][source class 2/4/8/9]
   int occ_copy = 2, occ_adam = 4, occ_reduce[4][4] = {};
   int occ_copy_indep = 1;  // CTAs/SM of barrier-free gathers chained with PDL
+  int occ_hier = 2;        // CTAs/SM of the one-launch hierarchical all-gather (one resident wave)
   int bar_strict = 0;      // BarrierArg::strict (MICS_BAR_STRICT)
   int par_ctas_per_sm = 0; // mics_set_parallelism: CTAs per SM cap (0 = occupancy)
   int par_max_ctas = 0;    // mics_set_parallelism: CTAs per launch cap (0 = none)
@@ -217,11 +247,14 @@ struct mics_ctx {
   cudaStream_t side_stream = nullptr;  // channel 1: the overlapped tail's Adam
   char* base = nullptr;           // local arena (IPC-exportable)
   uint64_t cap = 0, used = 0;
+  uint64_t top = 0;  // [top, cap): long-lived symmetric regions carved from the arena's end (hier_flags)
   char* peer_base[MICS_MAX_WORLD] = {};
   bool ipc_ready = false;
   mics::PeerTab* d_tab = nullptr;   // [kChannels]
   uint64_t* d_nbar = nullptr;       // [kChannels][MICS_MAX_WORLD]
   unsigned* d_tickets = nullptr;    // [kChannels][2]
+  mics::HierCtl* d_hctl = nullptr;  // [kChannels] hierarchical all-gather epochs
+  mics_buf hflags{};                // stage-1 tile flags of ad-hoc hierarchical all-gathers (grown on demand)
   // descriptor ring for ad-hoc calls
   char* ring = nullptr;
   uint64_t ring_cap = 0, ring_head = 0;
@@ -293,6 +326,26 @@ struct RedPlan {
   explicit RedPlan(mics_dtype in_t) : tile_elems(reduce_tile_elems(in_t)) {}
   void add(const std::vector<const void*>& src, void* dst, uint64_t elems, uint64_t valid);
 };
+// One hierarchical all-gather (K3) over every partition group of an n-rank cluster:
+// stage-1 then stage-3 segments of every local rank (HierSeg).
+struct HierPlan {
+  std::vector<HierSeg> segs;
+  uint32_t tiles = 0;
+  bool sys = false;  // a node peer of a local rank lives in another process
+  uint64_t remote_bytes = 0, hbm_bytes = 0;
+  // items: (src, dst, flags); equal sizes, tiles interleaved (stripe group)
+  void add_group(int stage, const std::vector<std::tuple<const void*, void*, uint64_t*>>& items, uint64_t bytes);
+};
+// The ad-hoc hierarchical all-gathers' flag array (>= bytes per rank, zeroed), carved
+// from the top of the arena so mark/release of the bump allocator never frees it.
+mics_buf hier_flags(mics_ctx* ctx, uint64_t bytes_per_rank);
+// Tiles per chunk of the flag array of one rank: q chunks x this many u64 flags.
+inline uint64_t hier_flag_tiles(uint64_t chunk_bytes) { return ceil_div(chunk_bytes, kCopyTile); }
+// src(r): rank r's input chunk; dst(r, pos): position `pos` of rank r's output; flags(r):
+// rank r's flag array ([q][ftiles] u64, peer-mapped for remote ranks).
+HierPlan plan_hier(mics_ctx* ctx, int n, int p, int k, uint64_t chunk, int corrupt,
+                   const std::function<const void*(int)>& src, const std::function<char*(int, uint64_t)>& dst,
+                   const std::function<uint64_t*(int)>& flags, uint64_t ftiles);
 struct AdamPlan {
   std::vector<AdamJob> jobs;
   std::vector<std::vector<const void*>> srcs;
@@ -305,8 +358,9 @@ struct AdamPlan {
 
 // A device-resident, replayable launch (built once, launched many times).
 struct Launch {
-  enum Kind { COPY, REDUCE, ADAM, BARRIER, TAIL } kind = COPY;
+  enum Kind { COPY, REDUCE, ADAM, BARRIER, TAIL, HIER } kind = COPY;
   int tail_r = 0, tail_p = 0;  // TAIL: replicas and group size (mode = 1 zero-accumulate)
+  int hier_sys = 0, hier_chan = 0;  // HIER: system-scope flags; channel of its epoch counter
   void* d_desc = nullptr;  // owned device table (cudaMalloc)
   uint64_t table_bytes = 0;
   uint32_t max_p = 1;
@@ -325,6 +379,8 @@ struct Launch {
   void release();
 };
 Launch make_copy_launch(mics_ctx* ctx, const CopyPlan& plan, const BarrierArg& bar, bool persistent);
+// chan: barrier channel whose HierCtl epoch counter the launch advances
+Launch make_hier_launch(mics_ctx* ctx, const HierPlan& plan, const BarrierArg& bar, int chan, bool persistent);
 Launch make_reduce_launch(mics_ctx* ctx, const RedPlan& plan, mics_dtype in_t, mics_dtype acc_t, double scale, int mode,
                           const BarrierArg& bar, bool persistent);
 Launch make_adam_launch(mics_ctx* ctx, const AdamPlan& plan, const AdamScalars& sc, const BarrierArg& bar,

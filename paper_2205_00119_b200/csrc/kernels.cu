@@ -1,6 +1,8 @@
 // sm_100a kernels of the MiCS hot path.
 //
-//  k_copy    — pull all-gather engine (K1/K3/K4): 16 B ld.global.nc from local or
+//  k_hier    — hierarchical all-gather in one launch (K3): stage-1 tiles publish per-tile
+//              flags, stage-3 tiles wait for the node peer's flag of the tile they read.
+//  k_copy    — pull all-gather engine (K1/K4): 16 B ld.global.nc from local or
 //              NVLink-peer memory, one read feeding up to kMaxDst coalesced stores.
 //              Replaces all_gather / hierarchical_all_gather / batched_all_gather
 //              (collectives.cpp:103-134, :192-306).
@@ -230,6 +232,115 @@ __global__ void __launch_bounds__(kThreads) k_copy(const CopySeg* __restrict__ g
   }
   bar_exit(bar);
   pdl_end(bar);
+}
+
+// ---------------------------------------------------------------- K3: hierarchical all-gather, one launch
+// Loads of data another CTA or GPU stores during this kernel (published by a flag)
+// bypass L1 and the non-coherent path: ld.global.cg, served by the owner's L2.
+__device__ __forceinline__ uint4 ld_cg(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ uint8_t ld_cg_u8(const uint8_t* p) {
+  uint16_t v;
+  asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+  return uint8_t(v);
+}
+
+// one tile (<= kCopyTile bytes) from src to dst; `coherent`: src is written during this kernel
+template <bool kCoherent>
+__device__ __forceinline__ void copy_tile(const uint8_t* src, uint8_t* dst, uint32_t nb) {
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    const uint32_t nv = nb >> 4;
+    uint4 v[kCopyUnroll];
+#pragma unroll
+    for (int u = 0; u < kCopyUnroll; ++u) {
+      const uint32_t i = threadIdx.x + u * kThreads;
+      if (i < nv) v[u] = kCoherent ? ld_cg(src + 16ull * i) : ld_stream(src + 16ull * i);
+    }
+#pragma unroll
+    for (int u = 0; u < kCopyUnroll; ++u) {
+      const uint32_t i = threadIdx.x + u * kThreads;
+      if (i < nv) st_vec(dst + 16ull * i, v[u]);
+    }
+    for (uint32_t b = nv * 16 + threadIdx.x; b < nb; b += kThreads) dst[b] = kCoherent ? ld_cg_u8(src + b) : src[b];
+  } else {  // byte-granular chunks (the reference tests' 1/7/9-byte shards)
+    for (uint32_t b = threadIdx.x; b < nb; b += kThreads) dst[b] = kCoherent ? ld_cg_u8(src + b) : src[b];
+  }
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Stage 1 and stage 3 of every local rank's hierarchical all-gather in one grid (see
+// HierSeg).  PDL: the launch waits for its predecessor before anything (the epoch and,
+// in the step, the write-after-read order of the gather slots: a rank's visit i+1
+// completes only after every node peer started visit i+1, i.e. finished reading
+// visit i), and lets its successor launch only at its very end — an early successor's
+// CTAs would hold SM slots a not-yet-resident CTA of this grid needs to publish the
+// flags resident CTAs are waiting for.  The grid is one resident wave.
+__global__ void __launch_bounds__(kThreads) k_hier(const HierSeg* __restrict__ gsegs, int nseg, uint32_t table_bytes,
+                                                   uint32_t ntiles, HierCtl* ctl, int sys_scope, BarrierArg bar) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const bool staged = table_bytes != 0;
+  if (staged) {
+    const uint4* s = reinterpret_cast<const uint4*>(gsegs);
+    uint4* d = reinterpret_cast<uint4*>(smem);
+    for (uint32_t i = threadIdx.x; i < table_bytes / 16; i += kThreads) d[i] = s[i];
+  }
+  __syncthreads();
+  const HierSeg* segs = staged ? reinterpret_cast<const HierSeg*>(smem) : gsegs;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  bar_entry(bar);
+  const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(&ctl->epoch) + 1;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int idx = find_desc(segs, nseg, tile);
+    uint32_t rel = tile - segs[idx].tile0;
+    const uint32_t k = segs[idx].gsize;
+    if (k > 1) {
+      idx = idx - int(k) + 1 + int(rel % k);
+      rel /= k;
+    }
+    const HierSeg& s = segs[idx];
+    const uint64_t off = uint64_t(rel) * kCopyTile;
+    const uint64_t rem = s.bytes - off;
+    const uint32_t nb = rem < kCopyTile ? uint32_t(rem) : kCopyTile;
+    if (s.stage == 3) {  // the node peer's stage-1 tile must be published first
+      if (threadIdx.x == 0) {
+        const uint64_t* f = s.flags + rel;
+        if (sys_scope) {
+          while (ld_relaxed_sys(f) < epoch) __nanosleep(64);
+          (void)ld_acquire_sys(f);
+        } else {
+          while (ld_acquire_gpu(f) < epoch) __nanosleep(64);
+        }
+      }
+      __syncthreads();
+      copy_tile<true>(s.src + off, s.dst + off, nb);
+    } else {
+      copy_tile<false>(s.src + off, s.dst + off, nb);
+      __syncthreads();  // every thread's stores of the tile before the publication
+      if (threadIdx.x == 0) {
+        if (sys_scope) __threadfence_system(); else __threadfence();
+        uint64_t* f = s.flags + rel;
+        if (sys_scope) st_relaxed_sys(f, epoch);
+        else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1) {  // last CTA: the launch is done
+    ctl->ticket = 0;
+    ctl->epoch = epoch;
+    __threadfence();
+  }
+  bar_exit(bar);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- K2: reduce engine
@@ -810,6 +921,9 @@ int resident_ctas(int kind, mics_dtype in_t, int pc) {
     case 0:
       MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_copy, kThreads, kSmemTable));
       break;
+    case 4:
+      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_hier, kThreads, kSmemTable));
+      break;
     case 1:
       if (in_t == MICS_BF16) n = reduce_occupancy<uint16_t, float>(pc);
       else if (in_t == MICS_F64) n = reduce_occupancy<double, double>(pc);
@@ -826,6 +940,12 @@ int resident_ctas(int kind, mics_dtype in_t, int pc) {
 void launch_copy(cudaStream_t s, const CopySeg* segs, int nseg, uint32_t ntiles, int grid, const BarrierArg& bar) {
   const uint32_t tb = uint64_t(nseg) * sizeof(CopySeg) <= uint64_t(kSmemTable) ? uint32_t(nseg * sizeof(CopySeg)) : 0u;
   launch_ex(k_copy, grid, kThreads, tb, s, segs, nseg, tb, ntiles, bar);
+}
+
+void launch_hier(cudaStream_t s, const HierSeg* segs, int nseg, uint32_t ntiles, int grid, HierCtl* ctl,
+                 int sys_scope, const BarrierArg& bar) {
+  const uint32_t tb = uint64_t(nseg) * sizeof(HierSeg) <= uint64_t(kSmemTable) ? uint32_t(nseg * sizeof(HierSeg)) : 0u;
+  launch_ex(k_hier, grid, kThreads, tb, s, segs, nseg, tb, ntiles, ctl, sys_scope, bar);
 }
 
 uint32_t reduce_tile_elems(mics_dtype in_t) {

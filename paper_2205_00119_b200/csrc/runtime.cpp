@@ -79,8 +79,8 @@ uint64_t mics_ctx::local_alloc(uint64_t bytes) {
   if (world != 1) raise(MICS_CONFIG_ERROR, "host-buffer API needs a single-process context");
   const uint64_t off = used;
   const uint64_t sz = mics::round_up(bytes ? bytes : 1, mics::kAlign);
-  if (off + sz > cap)
-    raise(MICS_INFEASIBLE, "arena exhausted: need " + std::to_string(sz) + " bytes, " + std::to_string(cap - off) +
+  if (off + sz > top)
+    raise(MICS_INFEASIBLE, "arena exhausted: need " + std::to_string(sz) + " bytes, " + std::to_string(top - off) +
                                " free (raise arena_bytes)");
   used += sz;
   return off;
@@ -141,6 +141,9 @@ mics_ctx* create_ctx(const mics_init_args* a) {
       c->occ_copy_indep = std::max(1, std::min(c->occ_copy, std::atoi(e)));
     if (const char* e = std::getenv("MICS_BAR_STRICT")) c->bar_strict = std::atoi(e) != 0;
     c->occ_adam = resident_ctas(2, MICS_F32);
+    // the one-launch hierarchical all-gather must be one resident wave (its stage-3
+    // tiles wait for other CTAs' stage-1 tiles): at most its occupancy, 3 like the chain
+    c->occ_hier = std::min(resident_ctas(4, MICS_F32), 3);
     const int classes[4] = {2, 4, 8, 9};
     for (int t = 0; t < 4; ++t)
       for (int k = 0; k < 4; ++k) c->occ_reduce[t][k] = resident_ctas(1, mics_dtype(t), classes[k]);
@@ -148,6 +151,7 @@ mics_ctx* create_ctx(const mics_init_args* a) {
     MICS_CUDA(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
     c->cap = (a->arena_bytes ? a->arena_bytes : (1ull << 30)) + kFlagsBytes;
     c->cap = round_up(c->cap, 2ull << 20);
+    c->top = c->cap;
     MICS_CUDA(cudaMalloc(&c->base, c->cap));
     MICS_CUDA(cudaMemset(c->base, 0, kFlagsBytes));
     c->used = kFlagsBytes;
@@ -160,6 +164,8 @@ mics_ctx* create_ctx(const mics_init_args* a) {
     MICS_CUDA(cudaMemset(c->d_nbar, 0, K * sizeof(uint64_t) * MICS_MAX_WORLD));
     MICS_CUDA(cudaMalloc(&c->d_tickets, K * 2 * sizeof(unsigned)));
     MICS_CUDA(cudaMemset(c->d_tickets, 0, K * 2 * sizeof(unsigned)));
+    MICS_CUDA(cudaMalloc(&c->d_hctl, K * sizeof(HierCtl)));
+    MICS_CUDA(cudaMemset(c->d_hctl, 0, K * sizeof(HierCtl)));
     c->ring_cap = kRingBytes;
     MICS_CUDA(cudaMalloc(&c->ring, c->ring_cap));
     MICS_CUDA(cudaDeviceSynchronize());
@@ -179,6 +185,7 @@ void destroy_ctx(mics_ctx* c) {
     if (w != c->wrank && c->peer_base[w]) cudaIpcCloseMemHandle(c->peer_base[w]);
   cudaFree(c->ring);
   cudaFree(c->d_tickets);
+  cudaFree(c->d_hctl);
   cudaFree(c->d_nbar);
   cudaFree(c->d_tab);
   cudaFree(c->base);
@@ -221,11 +228,27 @@ mics_buf alloc_sym(mics_ctx* c, uint64_t bytes_per_rank) {
   mics_buf b;
   b.stride = round_up(bytes_per_rank ? bytes_per_rank : 1, kAlign);
   const uint64_t total = b.stride * uint64_t(c->per);
-  if (c->used + total > c->cap)
+  if (c->used + total > c->top)
     raise(MICS_INFEASIBLE, "arena exhausted: need " + std::to_string(total) + " bytes, " +
-                               std::to_string(c->cap - c->used) + " free (raise arena_bytes)");
+                               std::to_string(c->top - c->used) + " free (raise arena_bytes)");
   b.offset = c->used;
   c->used += total;
+  return b;
+}
+
+mics_buf hier_flags(mics_ctx* c, uint64_t bytes_per_rank) {
+  if (c->hflags.stride >= bytes_per_rank) return c->hflags;
+  // SPMD: every process grows at the same call; the old region is simply abandoned
+  mics_buf b;
+  b.stride = round_up(std::max<uint64_t>(bytes_per_rank, 4096), kAlign);
+  const uint64_t total = b.stride * uint64_t(c->per);
+  if (c->top < c->used + total)
+    raise(MICS_INFEASIBLE, "arena exhausted: hierarchical all-gather flags need " + std::to_string(total) +
+                               " bytes (raise arena_bytes)");
+  c->top -= total;
+  b.offset = c->top;
+  MICS_CUDA(cudaMemsetAsync(c->base + b.offset, 0, total, c->stream));
+  c->hflags = b;
   return b;
 }
 

@@ -36,7 +36,6 @@ constexpr uint32_t kAlignElems = 8;
 void release(mics_step* st) {
   for (auto& v : st->ag)
     for (auto& l : v) l.release();
-  for (auto& l : st->agm) l.release();
   for (auto& v : st->micro)
     for (auto& l : v) l.release();
   st->bnd.rs.release();
@@ -67,9 +66,10 @@ void release(mics_step* st) {
   if (st->d_scalars) cudaFree(st->d_scalars);
 }
 
-// flat all-gather of layer l into gathered slot (l % gather_slots) of every local rank
-std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan, CopyPlan* ph1_out = nullptr,
-                                   CopyPlan* ph2_out = nullptr, uint64_t* mask_out = nullptr) {
+// all-gather of layer l into gathered slot (l % gather_slots) of every local rank:
+// flat (one k_copy stripe-group launch) or hierarchical (one k_hier launch; its epoch
+// counter lives on barrier channel `chan`)
+std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan) {
   mics_ctx* ctx = st->ctx;
   mics_sync* sy = st->sync;
   const int p = sy->p, n = sy->n;
@@ -98,83 +98,16 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan, CopyPlan* ph1
     out.push_back(l);
     return out;
   }
-  // hierarchical: stage 1 (channels) with stage 2 folded into addressing, then stage 3
-  const int q = p / k;
-  CopyPlan ph1, ph2;
-  uint64_t mask = 0;
-  for (int g = 0; g < n / p; ++g) {
-    const int base = g * p;
-    std::vector<int> ranks(static_cast<size_t>(p));
-    for (int i = 0; i < p; ++i) ranks[size_t(i)] = base + i;
-    mask |= ctx->peer_mask(ranks.data(), p);
-    for (int mm = 0; mm < q; ++mm)
-      for (int j = 0; j < k; ++j) {
-        const int r = base + mm * k + j;
-        if (!ctx->local(r)) continue;
-        std::vector<std::pair<const void*, std::vector<void*>>> g1, g2;
-        for (int m2 = 0; m2 < q; ++m2)
-          g1.push_back({ctx->rank_ptr(st->pbf16, base + m2 * k + j) + soff, {G(r, uint64_t(m2) * k + j)}});
-        for (int j2 = 0; j2 < k; ++j2) {
-          if (j2 == j) continue;
-          for (int t = 0; t < q; ++t) {
-            const uint64_t pos = uint64_t(t) * k + j2;
-            g2.push_back({G(base + mm * k + j2, pos), {G(r, pos)}});
-          }
-        }
-        ph1.add_group(g1, cb);
-        ph2.add_group(g2, cb);
-      }
-  }
-  if (ph1_out) {
-    *ph1_out = ph1;
-    *ph2_out = ph2;
-    *mask_out = mask;
-  }
-  // phase 1's exit barrier publishes every rank's stage-1 chunks before phase 2
-  // reads them.  Phase 2 needs no barrier of its own: the next overwrite of a
-  // gathered buffer (phase 1 of layer l+2) sits behind layer l+1's phase-1
-  // barrier, which every node peer only reaches after finishing phase 2 of l.
-  out.push_back(make_copy_launch(ctx, ph1, ctx->barrier(mask, 0, 1, chan), true));
-  out.push_back(make_copy_launch(ctx, ph2, ctx->barrier(0, 0, 0), true));
+  // hierarchical, one launch per layer visit: stage-1 tiles publish flags, stage-3 tiles
+  // wait for them (kernels.cu k_hier).  No barrier: stage 1 reads the static shards; the
+  // gather slots' write-after-read order follows from the flags (a rank completes visit
+  // i+1 only after every node peer started it, i.e. finished visit i) and at most every
+  // third visit reusing a slot — see k_hier and DESIGN §8 item 12.
+  HierPlan plan = plan_hier(
+      ctx, n, p, k, cb, 0, [&](int r) { return static_cast<const void*>(ctx->rank_ptr(st->pbf16, r) + soff); }, G,
+      [&](int r) { return reinterpret_cast<uint64_t*>(ctx->rank_ptr(st->hflags, r)); }, st->hflag_tiles);
+  out.push_back(make_hier_launch(ctx, plan, ctx->barrier(0, 0, 0), chan, true));
   return out;
-}
-
-// tiles of `b` follow those of `a` in one launch
-CopyPlan concat_plans(const CopyPlan& a, const CopyPlan& b) {
-  CopyPlan c = a;
-  for (CopySeg sg : b.segs) {
-    sg.tile0 += a.tiles;
-    c.segs.push_back(sg);
-  }
-  c.tiles = a.tiles + b.tiles;
-  return c;
-}
-
-// Hierarchical gathers of one micro-step as 2L+1 launches: phase 1 of visit 0; then
-// phase 2 of visit i-1 together with phase 1 of visit i (one launch, phase 1's exit
-// barrier); then phase 2 of the last visit.  Safe: phase 2 of visit i-1 reads the node
-// peers' stage-1 chunks published by the previous launch's exit barrier; phase 1 of
-// visit i writes slot (layer % gather_slots), whose last readers (the peers' phase 2
-// of an earlier visit to a layer of that slot, at least two visits back for any slot
-// count >= 2) finished before they reached that same barrier; when consecutive visits
-// are the same layer (the forward/backward turn) phase 1 rewrites identical bytes.
-void build_hier_merged(mics_step* st) {
-  mics_ctx* ctx = st->ctx;
-  const int L = st->cfg.nlayers;
-  std::vector<CopyPlan> p1(static_cast<size_t>(L)), p2(static_cast<size_t>(L));
-  uint64_t mask = 0;
-  for (int l = 0; l < L; ++l) {
-    std::vector<Launch> tmp = build_layer_ag(st, l, 0, &p1[size_t(l)], &p2[size_t(l)], &mask);
-    for (auto& x : tmp) x.release();
-  }
-  std::vector<int> visits;
-  for (int l = 0; l < L; ++l) visits.push_back(l);
-  for (int l = L; l-- > 0;) visits.push_back(l);
-  st->agm.push_back(make_copy_launch(ctx, p1[size_t(visits[0])], ctx->barrier(mask, 0, 1), true));
-  for (size_t i = 1; i < visits.size(); ++i)
-    st->agm.push_back(make_copy_launch(ctx, concat_plans(p2[size_t(visits[i - 1])], p1[size_t(visits[i])]),
-                                       ctx->barrier(mask, 0, 1), true));
-  st->agm.push_back(make_copy_launch(ctx, p2[size_t(visits.back())], ctx->barrier(0, 0, 0), true));
 }
 
 void enqueue_generate(mics_step* st, int t) {
@@ -362,10 +295,6 @@ void enqueue_fused_tail(mics_step* st) {
 // the fence positions are the ones counted here.
 void enqueue_gathers(mics_step* st, int t) {
   mics_ctx* ctx = st->ctx;
-  if (!st->agm.empty()) {  // merged hierarchical sequence
-    for (size_t i = 0; i < st->agm.size(); ++i) enqueue(ctx, st->agm[i], i == 0 && t == 0 ? 1 : -1);
-    return;
-  }
   bool first = true;
   const int m = st->gather_slots - 1;
   int pos = 0;
@@ -849,6 +778,13 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
       for (int t = 0; t < cfg->s; ++t) enqueue_generate(st, t);
     }
     // plans
+    if (cfg->hier_k > 0 && cfg->p > cfg->hier_k) {  // stage-1 tile flags of the hierarchical gathers
+      uint64_t cmax = 0;
+      for (uint64_t c : sy->chunk) cmax = std::max(cmax, c * 2);
+      st->hflag_tiles = hier_flag_tiles(cmax);
+      st->hflags = alloc_sym(ctx, uint64_t(cfg->p / cfg->hier_k) * st->hflag_tiles * 8);
+      MICS_CUDA(cudaMemsetAsync(ctx->base + st->hflags.offset, 0, st->hflags.stride * uint64_t(ctx->per), ctx->stream));
+    }
     for (int l = 0; l < cfg->nlayers; ++l) st->ag.push_back(build_layer_ag(st, l, cfg->compute ? 1 : 0));
     for (int t = 0; t < cfg->s; ++t) {
       const uint64_t goff = uint64_t(t % st->gslots) * sy->grad_elems * szg;
@@ -870,11 +806,6 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     st->adam.exp_avg_sq = st->v;
     st->adam.param_bf16 = st->pbf16;
     st->adam.write_grad = 0;
-    {
-      const char* me = std::getenv("MICS_HIER_MERGE");
-      if (cfg->hier_k > 0 && cfg->p > cfg->hier_k && !st->compute && !(me && me[0] == '0'))
-        build_hier_merged(st);
-    }
     if (!cfg->alternative) {
       st->bnd = build_boundary(sy, &st->adam, true, false);
       // overlapped tail (MICS_TAIL_OVERLAP=0/1 forces it)
@@ -949,20 +880,12 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     // kernels and algorithmic bytes of one step on this process (enqueue() skips empty launches)
     auto runs = [](const Launch& x) -> uint64_t { return (x.ndesc || x.bar.mask) ? 1 : 0; };
     mics_step_stats& S2 = st->stats;
-    if (!st->agm.empty()) {
-      for (auto& x : st->agm) {  // one micro-step's merged forward + backward sequence
-        S2.ag_launches += uint64_t(cfg->s) * runs(x);
-        S2.ag_remote_bytes += uint64_t(cfg->s) * x.remote_bytes;
-        S2.ag_hbm_bytes += uint64_t(cfg->s) * x.hbm_bytes;
+    for (auto& v : st->ag)
+      for (auto& x : v) {  // forward + backward pass, every micro-step
+        S2.ag_launches += 2 * uint64_t(cfg->s) * runs(x);
+        S2.ag_remote_bytes += 2 * uint64_t(cfg->s) * x.remote_bytes;
+        S2.ag_hbm_bytes += 2 * uint64_t(cfg->s) * x.hbm_bytes;
       }
-    } else {
-      for (auto& v : st->ag)
-        for (auto& x : v) {  // forward + backward pass, every micro-step
-          S2.ag_launches += 2 * uint64_t(cfg->s) * runs(x);
-          S2.ag_remote_bytes += 2 * uint64_t(cfg->s) * x.remote_bytes;
-          S2.ag_hbm_bytes += 2 * uint64_t(cfg->s) * x.hbm_bytes;
-        }
-    }
     for (size_t t = 0; t < st->micro.size(); ++t) {
       if ((st->tail || st->fused_tail) && t + 1 == st->micro.size()) continue;  // replaced by the tail launches
       for (auto& x : st->micro[t]) {

@@ -60,11 +60,10 @@ struct mics_step {
   mics_buf pbf16{}, master{}, m{}, v{}, gathered{}, grads{};
   uint64_t gathered_half = 0;                 // bytes of one gathered buffer (slot)
   int gather_slots = 2;                       // layer l gathers into slot l % gather_slots
-  std::vector<std::vector<mics::Launch>> ag;  // per layer: 1 launch (flat) or 2 (hierarchical)
-  // hierarchical gathers of one micro-step (forward 0..L-1, backward L-1..0) with phase 2
-  // of each visit merged into the launch of the next visit's phase 1: 2L+1 launches
-  // instead of 4L (MICS_HIER_MERGE=0 keeps the per-layer pairs)
-  std::vector<mics::Launch> agm;
+  std::vector<std::vector<mics::Launch>> ag;  // per layer: 1 launch (k_copy flat or k_hier)
+  // hierarchical gathers (k_hier): per rank [q][hflag_tiles] u64 stage-1 tile flags
+  mics_buf hflags{};
+  uint64_t hflag_tiles = 0;
   // per micro-step: the 2-hop reduce-scatter, or the alternative schedule's
   // all-n reduce-scatter + all-gather + owned-chunk accumulate
   std::vector<std::vector<mics::Launch>> micro;

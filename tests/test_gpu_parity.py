@@ -185,6 +185,24 @@ def test_hierarchical_multigroup_and_corrupt(m, engines, oracle, golden):
     assert e.value.code == m.Errc.ShapeError
 
 
+@pytest.mark.parametrize("corrupt", [False, True])
+def test_hierarchical_multi_tile_vs_oracle(m, oracle, corrupt):
+    """k_hier with chunks of many 32 KiB tiles (stage-3 tiles wait on per-tile flags of
+    the node peers' stage-1 tiles), aligned and byte-ragged, several partition groups,
+    the wrong-layout hook included, under full and tiny grids."""
+    eng = m.Engine(n_ranks=16, device=0, arena_bytes=1 << 30)
+    for n, p, k, chunk in ((16, 8, 4, (1 << 20) + 3), (16, 8, 2, 4 << 20), (16, 16, 4, 300_000), (8, 4, 2, 65_536)):
+        shards = oracle.random_shards(n, chunk, n + p + k)
+        want = oracle.hier_all_gather(shards, p, k, corrupt)
+        cl = m.ClusterSpec(num_nodes=n // k, devices_per_node=k, intra_node_bandwidth=1,
+                           inter_node_bandwidth_per_node=1)
+        for cps, cap in ((0, 0), (1, 0), (0, 3)):
+            eng.set_parallelism(cps, cap)
+            got = m.hierarchical_all_gather(eng, m.build_group_layout(n, p), cl, list(shards), corrupt_stage2=corrupt)
+            assert np.array_equal(np.stack(got), want), (n, p, k, chunk, cps, cap)
+    eng.close()
+
+
 def test_batched_equals_sequential(m, engines, oracle):
     eng = engines(64)
     groups = [m.CollectiveGroup([0, 1]), m.CollectiveGroup([2, 3, 4]), m.CollectiveGroup([5])]
