@@ -104,6 +104,12 @@ __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
   return v;
 }
 
+// acq_rel fences: MEMBAR.ALL.{GPU,SYS} without the L1 invalidation (CCTL.IVALL) and
+// sequential consistency of __threadfence / __threadfence_system (MEMBAR.SC.*); what
+// they order is published by a relaxed store the consumer acquires.
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
 __device__ __forceinline__ void bar_signal(const BarrierArg& b, uint64_t add) {
   if (b.strict) __threadfence_system();
   for (uint64_t m = b.mask; m; m &= m - 1) {
@@ -137,13 +143,13 @@ __device__ void bar_exit(const BarrierArg& b) {
   if (b.mask == 0) return;
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (b.exit && b.publish) __threadfence();  // this CTA's stores before its ticket (publication, see above)
+    if (b.exit && b.publish) fence_gpu();  // this CTA's stores before its ticket (publication, see above)
     if (b.strict) __threadfence_system();
     const unsigned t = atomicAdd(&b.tickets[1], 1u);
     if (t == gridDim.x - 1) {  // last CTA: every CTA of this GPU finished its accesses
       const uint64_t k = uint64_t(b.entry ? 1 : 0) + uint64_t(b.exit ? 1 : 0);
       if (b.exit) {
-        if (b.publish) __threadfence_system();  // every CTA's fenced stores, seen through the tickets, first
+        if (b.publish) fence_sys();  // every CTA's fenced stores, seen through the tickets, first
         bar_signal(b, k);
         bar_wait(b, k);
       }
@@ -276,6 +282,31 @@ __device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// thread 0 after __syncthreads: the CTA's stores of the tile, then the flag (release pattern)
+__device__ __forceinline__ void publish_flag(uint64_t* f, uint64_t v, int sys_scope) {
+  if (sys_scope) {
+    fence_sys();
+    st_relaxed_sys(f, v);
+  } else {
+    fence_gpu();
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
+  }
+}
+// poll relaxed, acquire once (the data loads that follow are ld.global.cg)
+__device__ __forceinline__ void wait_flag(const uint64_t* f, uint64_t v, int sys_scope) {
+  if (sys_scope) {
+    while (ld_relaxed_sys(f) < v) __nanosleep(64);
+    (void)ld_acquire_sys(f);
+  } else {
+    while (ld_relaxed_gpu(f) < v) __nanosleep(64);
+    (void)ld_acquire_gpu(f);
+  }
+}
 
 // Stage 1 and stage 3 of every local rank's hierarchical all-gather in one grid (see
 // HierSeg).  PDL: the launch waits for its predecessor before anything (the epoch and,
@@ -311,36 +342,98 @@ __global__ void __launch_bounds__(kThreads) k_hier(const HierSeg* __restrict__ g
     const uint64_t rem = s.bytes - off;
     const uint32_t nb = rem < kCopyTile ? uint32_t(rem) : kCopyTile;
     if (s.stage == 3) {  // the node peer's stage-1 tile must be published first
-      if (threadIdx.x == 0) {
-        const uint64_t* f = s.flags + rel;
-        if (sys_scope) {
-          while (ld_relaxed_sys(f) < epoch) __nanosleep(64);
-          (void)ld_acquire_sys(f);
-        } else {
-          while (ld_acquire_gpu(f) < epoch) __nanosleep(64);
-        }
-      }
+      if (threadIdx.x == 0) wait_flag(s.flags + rel, epoch, sys_scope);
       __syncthreads();
       copy_tile<true>(s.src + off, s.dst + off, nb);
     } else {
       copy_tile<false>(s.src + off, s.dst + off, nb);
       __syncthreads();  // every thread's stores of the tile before the publication
-      if (threadIdx.x == 0) {
-        if (sys_scope) __threadfence_system(); else __threadfence();
-        uint64_t* f = s.flags + rel;
-        if (sys_scope) st_relaxed_sys(f, epoch);
-        else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
-      }
+      if (threadIdx.x == 0) publish_flag(s.flags + rel, epoch, sys_scope);
     }
   }
   __syncthreads();
   if (threadIdx.x == 0 && atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1) {  // last CTA: the launch is done
     ctl->ticket = 0;
     ctl->epoch = epoch;
-    __threadfence();
+    fence_gpu();
   }
   bar_exit(bar);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Pipelined hierarchical gathers of the step (no barrier anywhere): launch x of a
+// micro-step's V+1 launches (V = 2L layer visits) runs stage 1 of visit x and stage 3
+// of visit x-1 (HierPipe), so each visit's NVLink-bound stage 1 overlaps the previous
+// visit's stage 3, and consecutive launches overlap through PDL:
+//  - it triggers its successor at once and waits for its predecessor only at its end
+//    (completion order), except launch 0, which waits first (it follows the
+//    reduce-scatter / boundary that wrote the shards and HierCtl::base);
+//  - read-after-write: a stage-3 tile waits for the node peer's flag of the stage-1
+//    tile it reads (published by launch x-1, epoch base + x);
+//  - write-after-read / write-after-write on the gather slots: before writing, every
+//    CTA waits until each process hosting a node peer, and this one, completed launch
+//    x - dist (done counters): with dist = slots - 1 every earlier reader and writer of
+//    the slot launch x writes (visit x - slots, read by stage 3 in launch x - dist) is done.
+// No tile ever waits on a tile of the same or a later launch, so no CTA can block one
+// that would unblock it; a launch's successor becomes resident only once all its CTAs
+// have started.
+__global__ void __launch_bounds__(kThreads) k_hier_pipe(const HierSeg* __restrict__ gsegs, int nseg,
+                                                        uint32_t table_bytes, uint32_t ntiles, HierCtl* ctl,
+                                                        const PeerTab* __restrict__ tab, uint64_t* my_done,
+                                                        HierPipe hp, int sys_scope) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const bool staged = table_bytes != 0;
+  if (staged) {
+    const uint4* s = reinterpret_cast<const uint4*>(gsegs);
+    uint4* d = reinterpret_cast<uint4*>(smem);
+    for (uint32_t i = threadIdx.x; i < table_bytes / 16; i += kThreads) d[i] = s[i];
+  }
+  __syncthreads();
+  const HierSeg* segs = staged ? reinterpret_cast<const HierSeg*>(smem) : gsegs;
+  if (hp.first) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint64_t base = *reinterpret_cast<volatile uint64_t*>(&ctl->base);
+  const uint64_t epoch = base + hp.x + 1;
+  if (threadIdx.x == 0 && hp.x >= hp.dist) {  // write-after-read / -write gate
+    const uint64_t target = epoch - hp.dist;
+    for (uint64_t m = hp.done_mask; m; m &= m - 1) {
+      const int w = __ffsll(static_cast<long long>(m)) - 1;
+      wait_flag(tab->done[w], target, sys_scope);
+    }
+  }
+  __syncthreads();
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int idx = find_desc(segs, nseg, tile);
+    uint32_t rel = tile - segs[idx].tile0;
+    const uint32_t k = segs[idx].gsize;
+    if (k > 1) {
+      idx = idx - int(k) + 1 + int(rel % k);
+      rel /= k;
+    }
+    const HierSeg& s = segs[idx];
+    const uint64_t off = uint64_t(rel) * kCopyTile;
+    const uint64_t rem = s.bytes - off;
+    const uint32_t nb = rem < kCopyTile ? uint32_t(rem) : kCopyTile;
+    if (s.stage == 3) {  // the previous visit's stage-1 tile of the node peer
+      if (threadIdx.x == 0) wait_flag(s.flags + rel, epoch - 1, sys_scope);
+      __syncthreads();
+      copy_tile<true>(s.src + off, s.dst + off, nb);
+    } else {
+      copy_tile<false>(s.src + off, s.dst + off, nb);
+      __syncthreads();
+      if (threadIdx.x == 0) publish_flag(s.flags + rel, epoch, sys_scope);
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // completion order: the predecessor is done
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_gpu();  // this CTA's stores before its ticket
+    if (atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1) {  // last CTA: launch x (and every earlier one) done
+      ctl->ticket = 0;
+      if (hp.last) ctl->base = epoch;
+      publish_flag(my_done, epoch, sys_scope);
+    }
+  }
 }
 
 // ---------------------------------------------------------------- K2: reduce engine
@@ -946,6 +1039,12 @@ void launch_hier(cudaStream_t s, const HierSeg* segs, int nseg, uint32_t ntiles,
                  int sys_scope, const BarrierArg& bar) {
   const uint32_t tb = uint64_t(nseg) * sizeof(HierSeg) <= uint64_t(kSmemTable) ? uint32_t(nseg * sizeof(HierSeg)) : 0u;
   launch_ex(k_hier, grid, kThreads, tb, s, segs, nseg, tb, ntiles, ctl, sys_scope, bar);
+}
+
+void launch_hier_pipe(cudaStream_t s, const HierSeg* segs, int nseg, uint32_t ntiles, int grid, HierCtl* ctl,
+                      const PeerTab* tab, uint64_t* my_done, const HierPipe& hp, int sys_scope) {
+  const uint32_t tb = uint64_t(nseg) * sizeof(HierSeg) <= uint64_t(kSmemTable) ? uint32_t(nseg * sizeof(HierSeg)) : 0u;
+  launch_ex(k_hier_pipe, grid, kThreads, tb, s, segs, nseg, tb, ntiles, ctl, tab, my_done, hp, sys_scope);
 }
 
 uint32_t reduce_tile_elems(mics_dtype in_t) {

@@ -147,7 +147,8 @@ def main():
     # alternative schedule, bit-exact against the CPU restatement of the step
     from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
     from test_gpu_step import expected_step
-    for p, k, alt, gdt in ((2, 0, False, "f32"), (4, 2, False, "bf16"), (4, 0, True, "f32"), (8, 0, False, "f32")):
+    for p, k, alt, gdt in ((2, 0, False, "f32"), (4, 2, False, "bf16"), (4, 0, True, "f32"), (8, 0, False, "f32"),
+                           (8, 4, False, "bf16")):
         e2 = Engine(n_ranks=n, world=world, world_rank=rank, device=local, arena_bytes=256 << 20)
         mdist.connect(e2)
         wl = Workload("mp", [20_000, 4_099, 65_536], p=p, s=2, grad_dtype=gdt, hier_k=k)
@@ -164,6 +165,29 @@ def main():
                    f"step p={p} k={k} alt={alt} {gdt} r={r}")
         step.close()
         e2.close()
+
+    # ---- pipelined hierarchical gathers (k_hier_pipe: flags + done counters, node peers
+    # across GPUs for p=8, k=4) vs one k_hier launch per visit, over 3 steps: same bits
+    for p, k in ((4, 2), (8, 4)):
+        res = {}
+        for pipe in ("1", "0"):
+            os.environ["MICS_HIER_PIPE"] = pipe
+            e7 = Engine(n_ranks=n, world=world, world_rank=rank, device=local, arena_bytes=256 << 20)
+            mdist.connect(e7)
+            step = MicsStep(e7, Workload("hp", [70_000, 12_345, 40_000, 9_999, 33_333], p=p, s=2, hier_k=k),
+                            StepOptions(seed=5))
+            step.run(3)
+            e7.synchronize()
+            S = step.sync_info()[0].shard_elems
+            b = step.buffers()
+            half = (step.stats().gathered_max_bytes + 255) // 256 * 256
+            res[pipe] = [e7.d2h(b["master"], r, S) for r in e7.local_ranks] + \
+                        [e7.d2h(b["gathered"], r, 3 * half // 2, "bf16") for r in e7.local_ranks]
+            step.close()
+            e7.close()
+        os.environ.pop("MICS_HIER_PIPE")
+        for x, y in zip(res["0"], res["1"]):
+            expect(np.array_equal(x.view(np.uint16), y.view(np.uint16)), f"hier pipe != per-visit (p={p}, k={k})")
 
     # ---- full-size C3 step across processes: sampled elements bit-exact (test_gpu_fullsize)
     from test_gpu_fullsize import check_sampled
