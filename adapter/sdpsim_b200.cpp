@@ -8,8 +8,10 @@
 // including the ones inside the header-only 2-hop schedule templates — executes
 // as libmics kernels on cuda:0.  This is the reference-side binding of
 // INTEGRATION.md §2, exercised for real.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <string>
 
 #include "mics.h"
@@ -30,14 +32,28 @@ void check(mics_status s) {
   if (s != MICS_OK) rethrow(s);
 }
 
-// One process-wide single-GPU context: the reference's engines are in-process
-// virtual ranks, so every VirtualRankEngine maps onto it.
+// One process-wide context: the reference's engines are in-process virtual ranks, so
+// every VirtualRankEngine maps onto it.  MICS_DEVICES="0,1,..." spreads the ranks
+// node-major over those GPUs of this process (mics_init_devices); default: GPU 0.
 constexpr int kMaxRanks = 1024;
 mics_ctx* ctx() {
   static mics_ctx* c = [] {
     mics_init_args a{kMaxRanks, 1, 0, 0, 2ull << 30};
+    std::vector<int> devs;
+    if (const char* e = std::getenv("MICS_DEVICES"))
+      for (const char* p = e; *p;) {
+        char* end = nullptr;
+        devs.push_back(int(std::strtol(p, &end, 10)));
+        p = *end ? end + 1 : end;
+      }
     mics_ctx* out = nullptr;
-    check(mics_init(&a, &out));
+    if (devs.size() > 1) {
+      a.device = devs[0];
+      check(mics_init_devices(&a, devs.data(), int(devs.size()), &out));
+    } else {
+      if (devs.size() == 1) a.device = devs[0];
+      check(mics_init(&a, &out));
+    }
     return out;
   }();
   return c;

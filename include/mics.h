@@ -97,6 +97,14 @@ typedef struct {
 } mics_init_args;
 
 mics_status mics_init(const mics_init_args* args, mics_ctx** out);
+/* One process driving several GPUs (the reference's single in-process engine,
+ * collectives.hpp:42-62, over NVLink): virtual ranks node-major over devices[0..ndev)
+ * (rank r on devices[r / (n_ranks / ndev)]), peer access between every pair, one stream
+ * per device, the same device flag barriers as a multi-process job.  args->world must
+ * be 1.  Every other call takes the returned context like a single-GPU one; the
+ * host-buffer API and the sync / step drivers then span the GPUs. */
+mics_status mics_init_devices(const mics_init_args* args, const int* devices, int ndev, mics_ctx** out);
+mics_status mics_device_count(mics_ctx* ctx, int* ndev); /* GPUs of the context (1 unless mics_init_devices) */
 mics_status mics_destroy(mics_ctx* ctx);
 /* CUDA IPC handle of this process's arena; gather all `world` handles (in world
  * order) with any out-of-band channel (torch.distributed) and import them. */

@@ -92,6 +92,8 @@ _SIGS = [
     ("mics_cluster_validate", I, [C.POINTER(Cluster)]),
     ("mics_min_feasible_partition", I, [U64, C.POINTER(Cluster), I, D, PI]),
     ("mics_init", I, [C.POINTER(InitArgs), C.POINTER(VP)]),
+    ("mics_init_devices", I, [C.POINTER(InitArgs), PI, I, C.POINTER(VP)]),
+    ("mics_device_count", I, [VP, PI]),
     ("mics_destroy", I, [VP]),
     ("mics_ipc_export", I, [VP, VP]),
     ("mics_ipc_import", I, [VP, VP]),

@@ -482,7 +482,8 @@ void all_reduce(mics_ctx* ctx, const int* ranks, int p, void* const* buf, uint64
 // `n` is the cluster's rank count: ctx->n, or (single process) any n <= ctx->n.
 void hier_all_gather(mics_ctx* ctx, int n, int p, int k, const void* const* shard, uint64_t chunk,
                      void* const* out, int corrupt) {
-  if (n < 1 || n > ctx->n || (ctx->world > 1 && n != ctx->n))
+  // (a multi-process job plans the whole cluster: n must be the job's rank count)
+  if (n < 1 || n > ctx->n || (ctx->world > 1 && !ctx->member && n != ctx->n))
     raise(MICS_SHAPE_ERROR, "cluster has " + std::to_string(n) + " ranks but the context has " +
                                 std::to_string(ctx->n));  // collectives.cpp:200-202
   if (p < 1 || p > n)
@@ -572,44 +573,84 @@ void batched_reduce_scatter(mics_ctx* ctx, const mics_rs_desc* d, int count, mic
 }
 
 // ---------------------------------------------------------------------------
-// host-buffer drop-ins (world == 1): stage through the arena, run, copy back.
+// host-buffer drop-ins: stage through the arena, run, copy back.  On a multi-device
+// context (mics_init_devices) every member stages the buffers of the ranks it hosts in
+// blocks at the same arena offset, runs its part of the collective (pulling the other
+// members' blocks over NVLink by UVA pointer) and copies its ranks' results back; the
+// members' kernels meet at the device flag barriers.
 namespace {
-struct Scratch {
-  mics_ctx* ctx;
-  uint64_t mark;
-  explicit Scratch(mics_ctx* c) : ctx(c), mark(c->used) {
-    if (c->world != 1) raise(MICS_CONFIG_ERROR, "host-buffer API needs a single-process context (world == 1)");
-  }
-  ~Scratch() { ctx->used = mark; }
-  char* alloc(uint64_t bytes) { return ctx->base + ctx->local_alloc(bytes); }
-};
 constexpr uint64_t kStage = 256;  // keep every staged buffer 16-byte aligned
+
+class Staging {
+ public:
+  explicit Staging(mics_ctx* ctx) : ctx_(ctx), mem_(members(ctx)) {
+    if (ctx->world != 1 && ctx->subs.empty())
+      raise(MICS_CONFIG_ERROR, "host-buffer API needs a single-process context (one GPU, or mics_init_devices)");
+    for (mics_ctx* m : mem_) marks_.push_back(m->used);
+  }
+  ~Staging() {
+    for (size_t i = 0; i < mem_.size(); ++i) mem_[i]->used = marks_[i];
+  }
+  uint64_t block(uint64_t bytes) {  // the same offset in every member (identical allocation sequences)
+    const uint64_t off = mem_[0]->local_alloc(bytes);
+    for (size_t i = 1; i < mem_.size(); ++i)
+      if (mem_[i]->local_alloc(bytes) != off) raise(MICS_CONFIG_ERROR, "members' arenas diverged");
+    return off;
+  }
+  mics_ctx* owner(int rank) const { return mics::owner(ctx_, rank); }
+  char* at(uint64_t block, int rank, uint64_t off) const { return owner(rank)->base + block + off; }
+  void h2d(int rank, void* dst, const void* src, uint64_t bytes) const {
+    if (!bytes) return;
+    mics_ctx* m = owner(rank);
+    MICS_CUDA(cudaSetDevice(m->device));
+    MICS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, m->stream));
+  }
+  void d2h(int rank, void* dst, const void* src, uint64_t bytes) const {
+    if (!bytes) return;
+    mics_ctx* m = owner(rank);
+    MICS_CUDA(cudaSetDevice(m->device));
+    MICS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, m->stream));
+  }
+  template <typename F>
+  void each(F&& f) const {
+    for (mics_ctx* m : mem_) {
+      MICS_CUDA(cudaSetDevice(m->device));
+      f(m);
+    }
+  }
+  void finish() const {
+    each([](mics_ctx* m) { MICS_CUDA(cudaStreamSynchronize(m->stream)); });
+  }
+
+ private:
+  mics_ctx* ctx_;
+  std::vector<mics_ctx*> mem_;
+  std::vector<uint64_t> marks_;
+};
 }  // namespace
 
 void host_all_gather(mics_ctx* ctx, const int* ranks, int p, const void* const* shards, uint64_t chunk,
                      void* const* out) {
-  Scratch s(ctx);
   check_group(ctx, ranks, p);
+  Staging s(ctx);
   const uint64_t cs = round_up(chunk, kStage), os = round_up(uint64_t(p) * chunk, kStage);
-  char* in = s.alloc(cs * uint64_t(p));
-  char* ob = s.alloc(os * uint64_t(p));
+  const uint64_t in = s.block(cs * uint64_t(p)), ob = s.block(os * uint64_t(p));
   std::vector<const void*> ip(static_cast<size_t>(p));
   std::vector<void*> op(static_cast<size_t>(p));
   for (int i = 0; i < p; ++i) {
-    ip[size_t(i)] = in + uint64_t(i) * cs;
-    op[size_t(i)] = ob + uint64_t(i) * os;
-    if (chunk) MICS_CUDA(cudaMemcpyAsync(in + uint64_t(i) * cs, shards[i], chunk, cudaMemcpyHostToDevice, ctx->stream));
+    ip[size_t(i)] = s.at(in, ranks[i], uint64_t(i) * cs);
+    op[size_t(i)] = s.at(ob, ranks[i], uint64_t(i) * os);
+    s.h2d(ranks[i], const_cast<void*>(ip[size_t(i)]), shards[i], chunk);
   }
-  all_gather(ctx, ranks, p, ip.data(), chunk, op.data());
-  for (int j = 0; j < p; ++j)
-    if (chunk) MICS_CUDA(cudaMemcpyAsync(out[j], op[size_t(j)], uint64_t(p) * chunk, cudaMemcpyDeviceToHost, ctx->stream));
-  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+  s.each([&](mics_ctx* m) { all_gather(m, ranks, p, ip.data(), chunk, op.data()); });
+  for (int j = 0; j < p; ++j) s.d2h(ranks[j], out[j], op[size_t(j)], uint64_t(p) * chunk);
+  s.finish();
 }
 
 void host_reduce_scatter(mics_ctx* ctx, const int* ranks, int p, const void* const* bufs, uint64_t bytes,
                          mics_dtype dt, void* const* out) {
-  Scratch s(ctx);
   check_group(ctx, ranks, p);
+  Staging s(ctx);
   if (dt == MICS_BF16) raise(MICS_TYPE_MISMATCH, "reduce_scatter: bf16 is not a reduction type");
   if (p == 0) return;
   const uint64_t sz = dtype_size(dt);
@@ -617,25 +658,25 @@ void host_reduce_scatter(mics_ctx* ctx, const int* ranks, int p, const void* con
     raise(MICS_TYPE_MISMATCH, "reduce_scatter: buffer of " + std::to_string(bytes) + " bytes is not divisible into " +
                                   std::to_string(p) + " chunks of whole " + std::to_string(sz) + "-byte elements");
   const uint64_t bs = round_up(bytes, kStage), cb = bytes / uint64_t(p), cs = round_up(cb, kStage);
-  char* in = s.alloc(bs * uint64_t(p));
-  char* ob = s.alloc(cs * uint64_t(p));
+  const uint64_t in = s.block(bs * uint64_t(p)), ob = s.block(cs * uint64_t(p));
   std::vector<const void*> ip(static_cast<size_t>(p));
   std::vector<void*> op(static_cast<size_t>(p));
   for (int i = 0; i < p; ++i) {
-    ip[size_t(i)] = in + uint64_t(i) * bs;
-    op[size_t(i)] = ob + uint64_t(i) * cs;
-    if (bytes) MICS_CUDA(cudaMemcpyAsync(in + uint64_t(i) * bs, bufs[i], bytes, cudaMemcpyHostToDevice, ctx->stream));
+    ip[size_t(i)] = s.at(in, ranks[i], uint64_t(i) * bs);
+    op[size_t(i)] = s.at(ob, ranks[i], uint64_t(i) * cs);
+    s.h2d(ranks[i], const_cast<void*>(ip[size_t(i)]), bufs[i], bytes);
   }
-  reduce_scatter(ctx, ranks, p, ip.data(), bytes / sz, bytes / sz, dt, dt, 1.0, MICS_RS_STORE, op.data());
-  for (int j = 0; j < p; ++j)
-    if (cb) MICS_CUDA(cudaMemcpyAsync(out[j], op[size_t(j)], cb, cudaMemcpyDeviceToHost, ctx->stream));
-  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+  s.each([&](mics_ctx* m) {
+    reduce_scatter(m, ranks, p, ip.data(), bytes / sz, bytes / sz, dt, dt, 1.0, MICS_RS_STORE, op.data());
+  });
+  for (int j = 0; j < p; ++j) s.d2h(ranks[j], out[j], op[size_t(j)], cb);
+  s.finish();
 }
 
 void host_all_reduce(mics_ctx* ctx, const int* ranks, int p, const void* const* bufs, uint64_t bytes, mics_dtype dt,
                      void* const* out) {
-  Scratch s(ctx);
   check_group(ctx, ranks, p);
+  Staging s(ctx);
   if (dt == MICS_BF16) raise(MICS_TYPE_MISMATCH, "all_reduce: bf16 is not a reduction type");
   if (p == 0) return;
   const uint64_t sz = dtype_size(dt);
@@ -643,76 +684,71 @@ void host_all_reduce(mics_ctx* ctx, const int* ranks, int p, const void* const* 
     raise(MICS_TYPE_MISMATCH, "all_reduce: buffer of " + std::to_string(bytes) + " bytes is not divisible into " +
                                   std::to_string(p) + " chunks of whole " + std::to_string(sz) + "-byte elements");
   const uint64_t bs = round_up(bytes, kStage);
-  char* b = s.alloc(bs * uint64_t(p));
+  const uint64_t b = s.block(bs * uint64_t(p));
   std::vector<void*> bp(static_cast<size_t>(p));
   for (int i = 0; i < p; ++i) {
-    bp[size_t(i)] = b + uint64_t(i) * bs;
-    if (bytes) MICS_CUDA(cudaMemcpyAsync(bp[size_t(i)], bufs[i], bytes, cudaMemcpyHostToDevice, ctx->stream));
+    bp[size_t(i)] = s.at(b, ranks[i], uint64_t(i) * bs);
+    s.h2d(ranks[i], bp[size_t(i)], bufs[i], bytes);
   }
-  all_reduce(ctx, ranks, p, bp.data(), bytes / sz, dt);
-  for (int j = 0; j < p; ++j)
-    if (bytes) MICS_CUDA(cudaMemcpyAsync(out[j], bp[size_t(j)], bytes, cudaMemcpyDeviceToHost, ctx->stream));
-  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+  s.each([&](mics_ctx* m) { all_reduce(m, ranks, p, bp.data(), bytes / sz, dt); });
+  for (int j = 0; j < p; ++j) s.d2h(ranks[j], out[j], bp[size_t(j)], bytes);
+  s.finish();
 }
 
 void host_hier_all_gather(mics_ctx* ctx, int n, int p, int k, const void* const* shards, uint64_t chunk,
                           void* const* out, int corrupt) {
-  Scratch s(ctx);
   if (n < 1 || n > ctx->n)
     raise(MICS_SHAPE_ERROR, "cluster has " + std::to_string(n) + " ranks but the context has " +
                                 std::to_string(ctx->n));  // collectives.cpp:200-202
+  Staging s(ctx);
   const uint64_t cs = round_up(chunk, kStage), os = round_up(uint64_t(p) * chunk, kStage);
-  char* in = s.alloc(cs * uint64_t(n));
-  char* ob = s.alloc(os * uint64_t(n));
+  const uint64_t in = s.block(cs * uint64_t(n)), ob = s.block(os * uint64_t(n));
   std::vector<const void*> ip(static_cast<size_t>(n));
   std::vector<void*> op(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) {
-    ip[size_t(i)] = in + uint64_t(i) * cs;
-    op[size_t(i)] = ob + uint64_t(i) * os;
-    if (chunk) MICS_CUDA(cudaMemcpyAsync(in + uint64_t(i) * cs, shards[i], chunk, cudaMemcpyHostToDevice, ctx->stream));
+    ip[size_t(i)] = s.at(in, i, uint64_t(i) * cs);
+    op[size_t(i)] = s.at(ob, i, uint64_t(i) * os);
+    s.h2d(i, const_cast<void*>(ip[size_t(i)]), shards[i], chunk);
   }
-  hier_all_gather(ctx, n, p, k, ip.data(), chunk, op.data(), corrupt);
-  for (int j = 0; j < n; ++j)
-    if (chunk) MICS_CUDA(cudaMemcpyAsync(out[j], op[size_t(j)], uint64_t(p) * chunk, cudaMemcpyDeviceToHost, ctx->stream));
-  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+  s.each([&](mics_ctx* m) { hier_all_gather(m, n, p, k, ip.data(), chunk, op.data(), corrupt); });
+  for (int j = 0; j < n; ++j) s.d2h(j, out[j], op[size_t(j)], uint64_t(p) * chunk);
+  s.finish();
 }
 
 void host_batched_all_gather(mics_ctx* ctx, int count, const int* sizes, const int* ranks, const uint64_t* chunks,
                              const void* const* shards, void* const* out) {
-  Scratch s(ctx);
+  Staging s(ctx);
   std::vector<mics_ag_desc> d(static_cast<size_t>(std::max(count, 0)));
   std::vector<std::vector<const void*>> ip(d.size());
   std::vector<std::vector<void*>> op(d.size());
   uint64_t ro = 0;
   for (int b = 0; b < count; ++b) {
     const int p = sizes[b];
+    check_group(ctx, ranks + ro, p);
     const uint64_t c = chunks[b], cs = round_up(c, kStage), os = round_up(uint64_t(p) * c, kStage);
-    char* in = s.alloc(cs * uint64_t(p));
-    char* ob = s.alloc(os * uint64_t(p));
+    const uint64_t in = s.block(cs * uint64_t(p)), ob = s.block(os * uint64_t(p));
     for (int i = 0; i < p; ++i) {
-      ip[size_t(b)].push_back(in + uint64_t(i) * cs);
-      op[size_t(b)].push_back(ob + uint64_t(i) * os);
-      if (c) MICS_CUDA(cudaMemcpyAsync(in + uint64_t(i) * cs, shards[ro + uint64_t(i)], c, cudaMemcpyHostToDevice,
-                                       ctx->stream));
+      const int r = ranks[ro + uint64_t(i)];
+      ip[size_t(b)].push_back(s.at(in, r, uint64_t(i) * cs));
+      op[size_t(b)].push_back(s.at(ob, r, uint64_t(i) * os));
+      s.h2d(r, const_cast<void*>(ip[size_t(b)].back()), shards[ro + uint64_t(i)], c);
     }
     d[size_t(b)] = mics_ag_desc{ranks + ro, p, ip[size_t(b)].data(), c, op[size_t(b)].data()};
     ro += uint64_t(p);
   }
-  batched_all_gather(ctx, d.data(), count);
+  s.each([&](mics_ctx* m) { batched_all_gather(m, d.data(), count); });
   ro = 0;
   for (int b = 0; b < count; ++b) {
     for (int j = 0; j < sizes[b]; ++j)
-      if (chunks[b])
-        MICS_CUDA(cudaMemcpyAsync(out[ro + uint64_t(j)], op[size_t(b)][size_t(j)], uint64_t(sizes[b]) * chunks[b],
-                                  cudaMemcpyDeviceToHost, ctx->stream));
+      s.d2h(ranks[ro + uint64_t(j)], out[ro + uint64_t(j)], op[size_t(b)][size_t(j)], uint64_t(sizes[b]) * chunks[b]);
     ro += uint64_t(sizes[b]);
   }
-  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+  s.finish();
 }
 
 void host_batched_reduce_scatter(mics_ctx* ctx, int count, const int* sizes, const int* ranks, const uint64_t* bytes,
                                  const void* const* bufs, mics_dtype dt, void* const* out) {
-  Scratch s(ctx);
+  Staging s(ctx);
   if (dt == MICS_BF16) raise(MICS_TYPE_MISMATCH, "reduce_scatter: bf16 is not a reduction type");
   const uint64_t sz = dtype_size(dt);
   std::vector<mics_rs_desc> d(static_cast<size_t>(std::max(count, 0)));
@@ -721,31 +757,30 @@ void host_batched_reduce_scatter(mics_ctx* ctx, int count, const int* sizes, con
   uint64_t ro = 0;
   for (int b = 0; b < count; ++b) {
     const int p = sizes[b];
+    check_group(ctx, ranks + ro, p);
     if (p > 0 && bytes[b] % (uint64_t(p) * sz))
       raise(MICS_TYPE_MISMATCH, "batched_reduce_scatter: buffer set " + std::to_string(b) +
                                     " is not divisible into whole chunks");
     const uint64_t bs = round_up(bytes[b], kStage), cb = p ? bytes[b] / uint64_t(p) : 0, cs = round_up(cb, kStage);
-    char* in = s.alloc(bs * uint64_t(p));
-    char* ob = s.alloc(cs * uint64_t(p));
+    const uint64_t in = s.block(bs * uint64_t(p)), ob = s.block(cs * uint64_t(p));
     for (int i = 0; i < p; ++i) {
-      ip[size_t(b)].push_back(in + uint64_t(i) * bs);
-      op[size_t(b)].push_back(ob + uint64_t(i) * cs);
-      if (bytes[b]) MICS_CUDA(cudaMemcpyAsync(in + uint64_t(i) * bs, bufs[ro + uint64_t(i)], bytes[b],
-                                              cudaMemcpyHostToDevice, ctx->stream));
+      const int r = ranks[ro + uint64_t(i)];
+      ip[size_t(b)].push_back(s.at(in, r, uint64_t(i) * bs));
+      op[size_t(b)].push_back(s.at(ob, r, uint64_t(i) * cs));
+      s.h2d(r, const_cast<void*>(ip[size_t(b)].back()), bufs[ro + uint64_t(i)], bytes[b]);
     }
     d[size_t(b)] = mics_rs_desc{ranks + ro, p, ip[size_t(b)].data(), bytes[b] / sz, bytes[b] / sz, op[size_t(b)].data()};
     ro += uint64_t(p);
   }
-  batched_reduce_scatter(ctx, d.data(), count, dt, dt, 1.0, MICS_RS_STORE);
+  s.each([&](mics_ctx* m) { batched_reduce_scatter(m, d.data(), count, dt, dt, 1.0, MICS_RS_STORE); });
   ro = 0;
   for (int b = 0; b < count; ++b) {
     const uint64_t cb = sizes[b] ? bytes[b] / uint64_t(sizes[b]) : 0;
     for (int j = 0; j < sizes[b]; ++j)
-      if (cb) MICS_CUDA(cudaMemcpyAsync(out[ro + uint64_t(j)], op[size_t(b)][size_t(j)], cb, cudaMemcpyDeviceToHost,
-                                        ctx->stream));
+      s.d2h(ranks[ro + uint64_t(j)], out[ro + uint64_t(j)], op[size_t(b)][size_t(j)], cb);
     ro += uint64_t(sizes[b]);
   }
-  MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+  s.finish();
 }
 
 }  // namespace mics

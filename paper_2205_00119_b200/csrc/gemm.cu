@@ -501,13 +501,18 @@ bool make_c_map(CUtensorMap* m, void* c, uint64_t ldc, int M, int N, bool bf16) 
 }
 
 int gemm_grid(int ntiles, int max_sms, int ctas) {
-  static int nsm = [] {
-    int dev = 0, n = 0;
-    MICS_CUDA(cudaGetDevice(&dev));
-    MICS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  // the shared-memory opt-in is per device (a multi-device context plans on several)
+  static uint64_t ready = 0;
+  static int nsm_of[64] = {};
+  int dev = 0;
+  MICS_CUDA(cudaGetDevice(&dev));
+  if (dev >= 64) raise(MICS_CONFIG_ERROR, "device ordinal beyond 63");
+  if (!(ready >> dev & 1)) {
+    MICS_CUDA(cudaDeviceGetAttribute(&nsm_of[dev], cudaDevAttrMultiProcessorCount, dev));
     MICS_CUDA(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
-    return n;
-  }();
+    ready |= 1ull << dev;
+  }
+  const int nsm = nsm_of[dev];
   const int sms = max_sms > 0 && max_sms < nsm ? max_sms : nsm;
   const int clusters = sms / ctas > 0 ? sms / ctas : 1;
   return ctas * (ntiles < clusters ? ntiles : clusters);

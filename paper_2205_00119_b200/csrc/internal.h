@@ -92,6 +92,7 @@ struct HierPipe {
   uint32_t first;             // x == 0: waits for its predecessor before anything
   uint32_t dist;              // gather slots - 1: launch x writes after launch x - dist completed everywhere
   uint64_t done_mask;         // processes whose done counters gate this launch's writes (self included)
+  unsigned* ticket;           // this launch's own CTA ticket (consecutive launches run concurrently)
 };
 
 struct RedJob {               // one output chunk (one destination rank, one segment)
@@ -240,6 +241,14 @@ AdamScalars make_adam_scalars(double lr, double b1, double b2, double eps, doubl
 // the context (VirtualRankEngine's B200 counterpart)
 struct mics_ctx {
   int n = 0, world = 1, wrank = 0, per = 0, device = 0, nsm = 148;
+  // Single-process multi-GPU context (mics_init_devices): `subs` holds one member
+  // context per GPU — member d behaves as process d of a `world`-GPU job, with its own
+  // arena, streams and barrier slots, peers mapped by peer access instead of CUDA IPC.
+  // Every C-ABI call on the group is run member by member (capi.cpp): each plans and
+  // enqueues the work of its own ranks, and the device flag barriers synchronise them,
+  // exactly as the separate processes of a torchrun job are synchronised.
+  std::vector<mics_ctx*> subs;
+  bool member = false;  // a member of a group (host-buffer staging allowed although world > 1)
   int blocks_per_sm = 4;
   // resident CTAs/SM per kernel: copy, adam, reduce by [input dtype][source class 2/4/8/9]
   int occ_copy = 2, occ_adam = 4, occ_reduce[4][4] = {};
@@ -319,10 +328,16 @@ struct mics_ctx {
     const char* c = static_cast<const char*>(p);
     return !ipc_ready || (c >= base && c < base + cap);
   }
-  uint64_t local_alloc(uint64_t bytes);  // world == 1 scratch
+  uint64_t local_alloc(uint64_t bytes);  // world == 1 (or group member) scratch
 };
 
 namespace mics {
+// the contexts that run a call: the members of a multi-device group, or the context itself
+inline std::vector<mics_ctx*> members(mics_ctx* c) { return c->subs.empty() ? std::vector<mics_ctx*>{c} : c->subs; }
+// the member hosting `rank` (the context itself when it is not a group)
+inline mics_ctx* owner(mics_ctx* c, int rank) {
+  return c->subs.empty() ? c : c->subs[size_t(c->process_of(rank))];
+}
 // collectives planners (collectives.cpp), shared with the sync/step drivers
 struct CopyPlan {
   std::vector<CopySeg> segs;

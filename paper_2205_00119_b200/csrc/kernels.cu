@@ -428,8 +428,8 @@ __global__ void __launch_bounds__(kThreads) k_hier_pipe(const HierSeg* __restric
   __syncthreads();
   if (threadIdx.x == 0) {
     fence_gpu();  // this CTA's stores before its ticket
-    if (atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1) {  // last CTA: launch x (and every earlier one) done
-      ctl->ticket = 0;
+    if (atomicAdd(hp.ticket, 1u) == gridDim.x - 1) {  // last CTA: launch x (and every earlier one) done
+      *hp.ticket = 0;
       if (hp.last) ctl->base = epoch;
       publish_flag(my_done, epoch, sys_scope);
     }

@@ -76,7 +76,7 @@ uint64_t mics_ctx::peer_mask(const int* ranks, int count) const {
 }
 
 uint64_t mics_ctx::local_alloc(uint64_t bytes) {
-  if (world != 1) raise(MICS_CONFIG_ERROR, "host-buffer API needs a single-process context");
+  if (world != 1 && !member) raise(MICS_CONFIG_ERROR, "host-buffer API needs a single-process context");
   const uint64_t off = used;
   const uint64_t sz = mics::round_up(bytes ? bytes : 1, mics::kAlign);
   if (off + sz > top)
@@ -186,11 +186,16 @@ mics_ctx* create_ctx(const mics_init_args* a) {
 
 void destroy_ctx(mics_ctx* c) {
   if (!c) return;
+  if (!c->subs.empty()) {  // a multi-device group: its members own everything
+    for (mics_ctx* m : c->subs) destroy_ctx(m);
+    delete c;
+    return;
+  }
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->side_stream) cudaStreamSynchronize(c->side_stream);
   for (int w = 0; w < c->world; ++w)
-    if (w != c->wrank && c->peer_base[w]) cudaIpcCloseMemHandle(c->peer_base[w]);
+    if (w != c->wrank && c->peer_base[w] && !c->member) cudaIpcCloseMemHandle(c->peer_base[w]);
   cudaFree(c->ring);
   cudaFree(c->d_tickets);
   cudaFree(c->d_hctl);
@@ -209,17 +214,9 @@ void ipc_export(mics_ctx* c, void* handle) {
   std::memcpy(handle, &h, sizeof(h));
 }
 
-void ipc_import(mics_ctx* c, const void* handles) {
-  if (c->ipc_ready) raise(MICS_CONFIG_ERROR, "IPC handles already imported");
-  MICS_CUDA(cudaSetDevice(c->device));
-  for (int w = 0; w < c->world; ++w) {
-    if (w == c->wrank) continue;
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, static_cast<const char*>(handles) + size_t(w) * MICS_IPC_HANDLE_BYTES, sizeof(h));
-    void* p = nullptr;
-    MICS_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-    c->peer_base[w] = static_cast<char*>(p);
-  }
+namespace {
+// flag tables once every peer_base[] is known (IPC-mapped or peer-accessible UVA)
+void connect_peers(mics_ctx* c) {
   PeerTab tab[mics_ctx::kChannels];
   std::memset(tab, 0, sizeof(tab));
   for (int ch = 0; ch < mics_ctx::kChannels; ++ch)
@@ -231,6 +228,75 @@ void ipc_import(mics_ctx* c, const void* handles) {
     }
   MICS_CUDA(cudaMemcpy(c->d_tab, tab, sizeof(tab), cudaMemcpyHostToDevice));
   c->ipc_ready = c->world > 1;
+}
+}  // namespace
+
+void ipc_import(mics_ctx* c, const void* handles) {
+  if (c->ipc_ready) raise(MICS_CONFIG_ERROR, "IPC handles already imported");
+  if (c->member) raise(MICS_CONFIG_ERROR, "a multi-device context connects its GPUs itself");
+  MICS_CUDA(cudaSetDevice(c->device));
+  for (int w = 0; w < c->world; ++w) {
+    if (w == c->wrank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + size_t(w) * MICS_IPC_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    MICS_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->peer_base[w] = static_cast<char*>(p);
+  }
+  connect_peers(c);
+}
+
+// One process, several GPUs: one member context per device (member d = "process" d of
+// a world of ndev), peer access between every pair, arenas mapped by UVA pointers.
+mics_ctx* create_group(const mics_init_args* a, const int* devices, int ndev) {
+  if (!a) raise(MICS_OUT_OF_RANGE, "null init args");
+  if (ndev < 1 || ndev > MICS_MAX_WORLD || !devices) raise(MICS_OUT_OF_RANGE, "need 1..64 devices");
+  if (a->world != 1 || a->world_rank != 0)
+    raise(MICS_CONFIG_ERROR, "a multi-device context is one process (world 1, world_rank 0)");
+  if (a->n_ranks < 1 || a->n_ranks % ndev)
+    raise(MICS_NON_DIVISIBLE, "the device count must divide n_ranks (node-major rank placement)");
+  auto* g = new mics_ctx();
+  try {
+    g->n = a->n_ranks;
+    g->world = ndev;
+    g->wrank = 0;
+    g->per = a->n_ranks / ndev;
+    g->device = devices[0];
+    for (int d = 0; d < ndev; ++d) {
+      mics_init_args s = *a;
+      s.world = ndev;
+      s.world_rank = d;
+      s.device = devices[d];
+      mics_ctx* m = create_ctx(&s);
+      m->member = true;
+      g->subs.push_back(m);
+    }
+    for (int x = 0; x < ndev; ++x)
+      for (int y = 0; y < ndev; ++y) {
+        if (devices[x] == devices[y]) continue;
+        int ok = 0;
+        MICS_CUDA(cudaDeviceCanAccessPeer(&ok, devices[x], devices[y]));
+        if (!ok) raise(MICS_CONFIG_ERROR, "no peer access between GPUs " + std::to_string(devices[x]) + " and " +
+                                              std::to_string(devices[y]));
+        MICS_CUDA(cudaSetDevice(devices[x]));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(devices[y], 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+        else MICS_CUDA(e);
+      }
+    for (mics_ctx* m : g->subs) {
+      for (int w = 0; w < ndev; ++w) m->peer_base[w] = g->subs[size_t(w)]->base;
+      MICS_CUDA(cudaSetDevice(m->device));
+      connect_peers(m);
+    }
+    g->nsm = g->subs[0]->nsm;
+    g->stream = g->subs[0]->stream;
+    g->ipc_ready = ndev > 1;
+  } catch (...) {
+    for (mics_ctx* m : g->subs) destroy_ctx(m);
+    delete g;
+    throw;
+  }
+  return g;
 }
 
 mics_buf alloc_sym(mics_ctx* c, uint64_t bytes_per_rank) {

@@ -37,6 +37,7 @@ void release(mics_step* st) {
   for (auto& v : st->ag)
     for (auto& l : v) l.release();
   for (auto& l : st->agp) l.release();
+  if (st->d_hp_tickets) cudaFree(st->d_hp_tickets);
   for (auto& v : st->micro)
     for (auto& l : v) l.release();
   st->bnd.rs.release();
@@ -142,6 +143,8 @@ void build_hier_pipe(mics_step* st) {
     for (int j2 = 0; j2 < k; ++j2) done_mask |= 1ull << ctx->process_of(base + m * k + j2);
   }
   const int V = int(visits.size());
+  MICS_CUDA(cudaMalloc(&st->d_hp_tickets, sizeof(unsigned) * size_t(V + 1)));
+  MICS_CUDA(cudaMemset(st->d_hp_tickets, 0, sizeof(unsigned) * size_t(V + 1)));
   for (int x = 0; x <= V; ++x) {
     HierPlan plan;
     if (x < V) plan = stage(x, 1);
@@ -153,6 +156,7 @@ void build_hier_pipe(mics_step* st) {
     l.hpipe.first = x == 0;
     l.hpipe.dist = uint32_t(st->gather_slots - 1);
     l.hpipe.done_mask = ctx->ipc_ready ? done_mask : (1ull << ctx->wrank);
+    l.hpipe.ticket = st->d_hp_tickets + x;
     // consecutive launches overlap (PDL): each gets a share of the SMs, like the flat chain
     l.grid = ctx->grid_for(plan.tiles, std::max(1, ctx->occ_hier / 2));
     st->agp.push_back(l);
@@ -771,7 +775,7 @@ void enqueue_compute_step(mics_step* st, PhaseClock* clk) {
 
 }  // namespace
 
-mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
+mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
   if (!cfg || cfg->nlayers < 1 || !cfg->layer_params) raise(MICS_OUT_OF_RANGE, "step config needs >= 1 layer");
   // every layer gathers something: the fence positions of the gather chain
   // (enqueue_gathers) and the first gather's wait for the boundary count on it
@@ -933,10 +937,13 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg) {
     st->stats.shard_elems = S;
     st->stats.gathered_max_bytes = maxl;
     st->stats.grad_elems = sy->grad_elems;
-    // everybody's initial parameters are written before anyone gathers them
-    MICS_CUDA(cudaStreamSynchronize(ctx->stream));
-    barrier_all(ctx);
-    MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+    // everybody's initial parameters are written before anyone gathers them (the members
+    // of a multi-device context settle together, capi.cpp)
+    if (settle) {
+      MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+      barrier_all(ctx);
+      MICS_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     // kernels and algorithmic bytes of one step on this process (enqueue() skips empty launches)
     auto runs = [](const Launch& x) -> uint64_t { return (x.ndesc || x.bar.mask) ? 1 : 0; };
     mics_step_stats& S2 = st->stats;
@@ -1129,28 +1136,22 @@ void step_run(mics_step* st, int iters) {
   st->stats.adam_step = st->adam_step;
 }
 
-// One step with CUDA events around each phase; returns milliseconds per phase
-// (ms[0] all-gather, [1] reduce-scatter, [2] boundary, [3] generation, [4] GEMMs).
-void step_profile(mics_step* st, double* ms) {
+ProfileRec* step_profile_begin(mics_step* st) {
   mics_ctx* ctx = st->ctx;
   const int s = st->cfg.s;
-  for (int i = 0; i < 5; ++i) ms[i] = 0;
+  auto* rec = new ProfileRec();
   if (st->compute) {  // serialised on the main stream, events around every gather / GEMM group
     PhaseClock clk;
     clk.s = ctx->stream;
     enqueue_compute_step(st, &clk);
     st->step_idx++;
-    MICS_CUDA(cudaEventSynchronize(clk.ev.back()));
-    for (size_t i = 1; i < clk.ev.size(); ++i) {
-      float x = 0;
-      MICS_CUDA(cudaEventElapsedTime(&x, clk.ev[i - 1], clk.ev[i]));
-      if (clk.kind[i] >= 0) ms[clk.kind[i]] += x;
-    }
-    for (auto e : clk.ev) cudaEventDestroy(e);
-    st->stats.adam_step = st->adam_step;
-    return;
+    rec->compute = true;
+    rec->ev = std::move(clk.ev);
+    rec->kind = std::move(clk.kind);
+    return rec;
   }
-  std::vector<cudaEvent_t> ev(size_t(4 * s + 2));
+  std::vector<cudaEvent_t>& ev = rec->ev;
+  ev.resize(size_t(4 * s + 2));
   for (auto& e : ev) MICS_CUDA(cudaEventCreate(&e));
   int k = 0;
   for (int t = 0; t < s; ++t) {
@@ -1163,42 +1164,61 @@ void step_profile(mics_step* st, double* ms) {
     MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
   }
   MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
-  std::vector<cudaEvent_t> tclk;  // overlapped tail, serialised: RS / boundary per layer group
-  if (st->tail)
-    enqueue_tail(st, &tclk);
+  if (st->tail)  // overlapped tail, serialised: RS / boundary per layer group
+    enqueue_tail(st, &rec->tclk);
   else if (st->fused_tail)
     enqueue_fused_tail(st);  // timed as the boundary phase (it carries the last reduce-scatter)
   else
     enqueue_boundary(st);
   st->step_idx++;
   MICS_CUDA(cudaEventRecord(ev[size_t(k++)], ctx->stream));
-  MICS_CUDA(cudaEventSynchronize(ev[size_t(k - 1)]));
-  float a = 0, r = 0, g = 0, b = 0, x;
-  for (int t = 0; t < s; ++t) {
-    MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * t)], ev[size_t(4 * t + 1)]));
-    g += x;
-    MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * t + 1)], ev[size_t(4 * t + 2)]));
-    a += x;
-    MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * t + 2)], ev[size_t(4 * t + 3)]));
-    r += x;
-  }
-  MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * s)], ev[size_t(4 * s + 1)]));
-  b = x;
-  if (st->tail) {
-    b = 0;
-    for (size_t i = 1; i < tclk.size(); ++i) {
-      MICS_CUDA(cudaEventElapsedTime(&x, tclk[i - 1], tclk[i]));
-      (i % 2 ? r : b) += x;
+  return rec;
+}
+
+void step_profile_end(mics_step* st, ProfileRec* rec, double* ms) {
+  const int s = st->cfg.s;
+  for (int i = 0; i < 5; ++i) ms[i] = 0;
+  std::vector<cudaEvent_t>& ev = rec->ev;
+  MICS_CUDA(cudaEventSynchronize(ev.back()));
+  if (rec->compute) {
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float x = 0;
+      MICS_CUDA(cudaEventElapsedTime(&x, ev[i - 1], ev[i]));
+      if (rec->kind[i] >= 0) ms[rec->kind[i]] += x;
     }
-    for (auto e : tclk) cudaEventDestroy(e);
+  } else {
+    float a = 0, r = 0, g = 0, b = 0, x;
+    for (int t = 0; t < s; ++t) {
+      MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * t)], ev[size_t(4 * t + 1)]));
+      g += x;
+      MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * t + 1)], ev[size_t(4 * t + 2)]));
+      a += x;
+      MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * t + 2)], ev[size_t(4 * t + 3)]));
+      r += x;
+    }
+    MICS_CUDA(cudaEventElapsedTime(&x, ev[size_t(4 * s)], ev[size_t(4 * s + 1)]));
+    b = x;
+    if (st->tail) {
+      b = 0;
+      for (size_t i = 1; i < rec->tclk.size(); ++i) {
+        MICS_CUDA(cudaEventElapsedTime(&x, rec->tclk[i - 1], rec->tclk[i]));
+        (i % 2 ? r : b) += x;
+      }
+    }
+    ms[0] = a;
+    ms[1] = r;
+    ms[2] = b;
+    ms[3] = g;
   }
-  for (auto& e : ev) cudaEventDestroy(e);
-  ms[0] = a;
-  ms[1] = r;
-  ms[2] = b;
-  ms[3] = g;
+  for (auto e : rec->tclk) cudaEventDestroy(e);
+  for (auto e : ev) cudaEventDestroy(e);
+  delete rec;
   st->stats.adam_step = st->adam_step;
 }
+
+// One step with CUDA events around each phase; milliseconds per phase (ms[0] all-gather,
+// [1] reduce-scatter, [2] boundary, [3] generation, [4] GEMMs).
+void step_profile(mics_step* st, double* ms) { step_profile_end(st, step_profile_begin(st), ms); }
 
 // End-to-end variant through host memory: every micro-step each local rank's
 // gradients are copied from (pinned) host memory — host_grads holds one gradient

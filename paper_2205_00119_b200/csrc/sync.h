@@ -7,6 +7,9 @@
 #include "internal.h"
 
 struct mics_sync {
+  // a multi-device context's sync state: one member state per GPU (capi.cpp runs every
+  // call on each; queries read member 0 — the members evolve identically)
+  std::vector<mics_sync*> subs;
   mics_ctx* ctx = nullptr;
   int n = 0, p = 0, s = 1, nseg = 0;
   mics_dtype acc_t = MICS_F32;
@@ -52,7 +55,19 @@ void alt_boundary(mics_sync* st);
 // MiCS step driver state (step.cpp)
 constexpr int kMaxGatherSlots = 8;  // mics_step::gather_slots upper bound (MICS_GATHER_SLOTS)
 
+namespace mics {
+struct ProfileRec {  // one profiled step in flight (step_profile_begin / step_profile_end)
+  bool compute = false;
+  std::vector<cudaEvent_t> ev, tclk;
+  std::vector<int> kind;  // step with compute: the phase of the interval ending at ev[i]
+};
+}  // namespace mics
+
 struct mics_step {
+  // a multi-device context's step: one member step per GPU, and the group view of their
+  // sync states (owned here; the member states belong to the member steps)
+  std::vector<mics_step*> subs;
+  mics_sync* gsync = nullptr;
   mics_ctx* ctx = nullptr;
   mics_step_cfg cfg{};
   std::vector<uint64_t> layers;
@@ -63,6 +78,7 @@ struct mics_step {
   std::vector<std::vector<mics::Launch>> ag;  // per layer: 1 launch (k_copy flat or k_hier)
   // pipelined hierarchical gathers of one micro-step (k_hier_pipe, comm-only step): 2L+1 launches
   std::vector<mics::Launch> agp;
+  unsigned* d_hp_tickets = nullptr;  // [2L+1] CTA tickets, one per pipelined launch
   // hierarchical gathers: per rank [slots][q][hflag_tiles] (pipelined) or [q][hflag_tiles] u64 flags
   mics_buf hflags{};
   uint64_t hflag_tiles = 0;

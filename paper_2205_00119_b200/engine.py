@@ -31,15 +31,23 @@ def dtype_code(dtype) -> int:
 
 class Engine:
     def __init__(self, num_threads: int | None = None, *, n_ranks: int = 64, world: int = 1, world_rank: int = 0,
-                 device: int = 0, arena_bytes: int = 1 << 30):
+                 device: int = 0, arena_bytes: int = 1 << 30, devices=None):
+        """One GPU (`device`), one GPU of a `world`-process job, or — `devices` — one
+        process driving several GPUs (mics_init_devices): ranks node-major over them,
+        `arena_bytes` per GPU."""
         self.num_threads = None if num_threads is None else max(1, int(num_threads))
         self.n = n_ranks
         self.world = world
         self.world_rank = world_rank
-        self.device = device
-        args = InitArgs(n_ranks, world, world_rank, device, arena_bytes)
+        self.devices = list(devices) if devices else [device]
+        self.device = self.devices[0]
+        args = InitArgs(n_ranks, world, world_rank, self.device, arena_bytes)
         ctx = C.c_void_p()
-        check(lib.mics_init(C.byref(args), C.byref(ctx)))
+        if devices:
+            arr = (C.c_int * len(self.devices))(*self.devices)
+            check(lib.mics_init_devices(C.byref(args), arr, len(self.devices), C.byref(ctx)))
+        else:
+            check(lib.mics_init(C.byref(args), C.byref(ctx)))
         self.ctx = ctx
         first, count = C.c_int(0), C.c_int(0)
         check(lib.mics_local_ranks(self.ctx, C.byref(first), C.byref(count)))
@@ -81,6 +89,10 @@ class Engine:
         assert len(blob) == IPC_HANDLE_BYTES * self.world
         cbuf = C.create_string_buffer(blob, len(blob))
         check(lib.mics_ipc_import(self.ctx, cbuf))
+
+    def gpu_of(self, rank: int) -> int:
+        """The CUDA device hosting `rank` (multi-device contexts: node-major placement)."""
+        return self.devices[rank // (self.n // len(self.devices))] if len(self.devices) > 1 else self.device
 
     def process_of(self, rank: int) -> int:
         out = C.c_int(0)

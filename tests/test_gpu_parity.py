@@ -23,13 +23,21 @@ def m():
     return m
 
 
-@pytest.fixture(scope="module")
-def engines(m):
+@pytest.fixture(scope="module", params=["1gpu", "2gpus_one_process"])
+def engines(m, request):
+    """Engines of n virtual ranks on GPU 0, or spread node-major over GPUs 0 and 1 of
+    this one process (mics_init_devices): every test below runs on both."""
+    devices = None
+    if request.param == "2gpus_one_process":
+        import torch
+        if torch.cuda.device_count() < 2:
+            pytest.skip("needs 2 GPUs")
+        devices = [0, 1]
     cache = {}
 
     def get(n):
         if n not in cache:
-            cache[n] = m.Engine(n_ranks=n, device=0, arena_bytes=512 << 20)
+            cache[n] = m.Engine(n_ranks=n, device=0, arena_bytes=512 << 20, devices=devices)
         cache[n].clear_traffic()
         return cache[n]
     yield get

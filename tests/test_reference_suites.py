@@ -16,11 +16,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "build", "reftests")
 
 
-def _run(name):
+def _run(name, devices=None):
     path = os.path.join(BIN, f"test_{name}")
     if not os.path.exists(path):
         pytest.skip(f"{path} not built (needs /root/reference at build time)")
-    out = subprocess.run([path], capture_output=True, text=True, timeout=600)
+    env = dict(os.environ)
+    if devices:
+        import torch
+        if torch.cuda.device_count() < len(devices):
+            pytest.skip(f"needs {len(devices)} GPUs")
+        env["MICS_DEVICES"] = ",".join(map(str, devices))  # ranks spread over these GPUs, one process
+    out = subprocess.run([path], capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-2000:]
     assert "0 failed" in out.stdout.splitlines()[-1]
     return out.stdout
@@ -32,12 +38,14 @@ def test_reference_topology_suite():
 
 
 @pytest.mark.gpu
-def test_reference_collectives_suite():
-    out = _run("collectives")
+@pytest.mark.parametrize("devices", [None, [0, 1]], ids=["1gpu", "2gpus_one_process"])
+def test_reference_collectives_suite(devices):
+    out = _run("collectives", devices)
     assert out.count("[PASS]") == 12
 
 
 @pytest.mark.gpu
-def test_reference_sync_schedule_suite():
-    out = _run("sync_schedule")
+@pytest.mark.parametrize("devices", [None, [0, 1]], ids=["1gpu", "2gpus_one_process"])
+def test_reference_sync_schedule_suite(devices):
+    out = _run("sync_schedule", devices)
     assert out.count("[PASS]") == 5
