@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define MICS_ABI_VERSION 2
+#define MICS_ABI_VERSION 3
 #define MICS_IPC_HANDLE_BYTES 64
 #define MICS_MAX_WORLD 64
 #define MICS_MAX_GROUP 1024
@@ -355,6 +355,8 @@ typedef struct {
   /* step with compute: tensor-core FLOPs and GEMM launches per step (this process) */
   double compute_flops;
   uint64_t gemm_launches;
+  uint64_t gather_slots;       /* layer l's gathered parameters live in slot l % gather_slots */
+  uint64_t gather_slot_bytes;  /* bytes of one slot of the `gathered` buffer (per rank) */
 } mics_step_stats;
 
 mics_status mics_step_create(mics_ctx* ctx, const mics_step_cfg* cfg, mics_step** out);

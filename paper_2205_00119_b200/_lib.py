@@ -78,7 +78,7 @@ class StepStats(C.Structure):
                 ("ag_remote_bytes", U64), ("ag_hbm_bytes", U64), ("ag_launches", U64),
                 ("rs_remote_bytes", U64), ("rs_hbm_bytes", U64), ("rs_launches", U64),
                 ("bnd_remote_bytes", U64), ("bnd_hbm_bytes", U64), ("bnd_launches", U64),
-                ("compute_flops", D), ("gemm_launches", U64)]
+                ("compute_flops", D), ("gemm_launches", U64), ("gather_slots", U64), ("gather_slot_bytes", U64)]
 
 
 # (name, restype, argtypes); restype I is a mics_status

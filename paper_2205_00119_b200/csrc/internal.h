@@ -93,6 +93,8 @@ struct HierPipe {
   uint32_t dist;              // gather slots - 1: launch x writes after launch x - dist completed everywhere
   uint64_t done_mask;         // processes whose done counters gate this launch's writes (self included)
   unsigned* ticket;           // this launch's own CTA ticket (consecutive launches run concurrently)
+  uint32_t diag;              // MICS_HP_DIAG bits (debugging): 1 wait at start, 2 trigger at end, 4 no done gate
+  uint32_t pad_;
 };
 
 struct RedJob {               // one output chunk (one destination rank, one segment)

@@ -390,11 +390,11 @@ __global__ void __launch_bounds__(kThreads) k_hier_pipe(const HierSeg* __restric
   }
   __syncthreads();
   const HierSeg* segs = staged ? reinterpret_cast<const HierSeg*>(smem) : gsegs;
-  if (hp.first) asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (hp.first || (hp.diag & 1)) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!(hp.diag & 2)) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint64_t base = *reinterpret_cast<volatile uint64_t*>(&ctl->base);
   const uint64_t epoch = base + hp.x + 1;
-  if (threadIdx.x == 0 && hp.x >= hp.dist) {  // write-after-read / -write gate
+  if (threadIdx.x == 0 && hp.x >= hp.dist && !(hp.diag & 4)) {  // write-after-read / -write gate
     const uint64_t target = epoch - hp.dist;
     for (uint64_t m = hp.done_mask; m; m &= m - 1) {
       const int w = __ffsll(static_cast<long long>(m)) - 1;
@@ -434,6 +434,7 @@ __global__ void __launch_bounds__(kThreads) k_hier_pipe(const HierSeg* __restric
       publish_flag(my_done, epoch, sys_scope);
     }
   }
+  if (hp.diag & 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- K2: reduce engine

@@ -157,6 +157,8 @@ void build_hier_pipe(mics_step* st) {
     l.hpipe.dist = uint32_t(st->gather_slots - 1);
     l.hpipe.done_mask = ctx->ipc_ready ? done_mask : (1ull << ctx->wrank);
     l.hpipe.ticket = st->d_hp_tickets + x;
+    if (const char* e = std::getenv("MICS_HP_DIAG")) l.hpipe.diag = uint32_t(std::atoi(e));
+    if (const char* e = std::getenv("MICS_HP_DIST")) l.hpipe.dist = uint32_t(std::atoi(e));
     // consecutive launches overlap (PDL): each gets a share of the SMs, like the flat chain
     l.grid = ctx->grid_for(plan.tiles, std::max(1, ctx->occ_hier / 2));
     st->agp.push_back(l);
@@ -805,7 +807,14 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
     st->v = alloc_sym(ctx, S * 4);
     // Without compute nothing consumes a gather, so up to three run concurrently
     // (enqueue_gathers): three slots.  With compute a layer's GEMMs release its slot.
-    st->gather_slots = cfg->compute ? 2 : 3;
+    // Pipelined hierarchical gathers (k_hier_pipe; MICS_HIER_PIPE=0: one k_hier launch per
+    // visit, as with compute) keep four: launch x may then write once launch x-3 is done
+    // everywhere (the done gate), so three consecutive launches overlap (with a gate at
+    // x-2, i.e. three slots, the pipeline measured to stall, tools/gpu_runs/R2_h.sh).
+    const bool hier = cfg->hier_k > 0 && cfg->p > cfg->hier_k;
+    const char* hpe = std::getenv("MICS_HIER_PIPE");
+    const bool hpipe = hier && !cfg->compute && !(hpe && hpe[0] == '0');
+    st->gather_slots = cfg->compute ? 2 : hpipe ? 4 : 3;
     if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)
       st->gather_slots = std::max(2, std::min(kMaxGatherSlots, std::atoi(e)));
     st->gathered = alloc_sym(ctx, uint64_t(st->gather_slots) * st->gathered_half);
@@ -835,11 +844,6 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
       for (int t = 0; t < cfg->s; ++t) enqueue_generate(st, t);
     }
     // plans
-    const bool hier = cfg->hier_k > 0 && cfg->p > cfg->hier_k;
-    // pipelined hierarchical gathers in the comm-only step (MICS_HIER_PIPE=0: one k_hier
-    // launch per layer visit, as in the step with compute)
-    const char* hpe = std::getenv("MICS_HIER_PIPE");
-    const bool hpipe = hier && !cfg->compute && !(hpe && hpe[0] == '0');
     if (hier) {  // stage-1 tile flags of the hierarchical gathers (per gather slot when pipelined)
       uint64_t cmax = 0;
       for (uint64_t c : sy->chunk) cmax = std::max(cmax, c * 2);
@@ -936,6 +940,8 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
     st->stats.gen_bytes = generated(st) ? uint64_t(cfg->s) * sy->grad_elems * szg : 0;
     st->stats.shard_elems = S;
     st->stats.gathered_max_bytes = maxl;
+    st->stats.gather_slots = uint64_t(st->gather_slots);
+    st->stats.gather_slot_bytes = st->gathered_half;
     st->stats.grad_elems = sy->grad_elems;
     // everybody's initial parameters are written before anyone gathers them (the members
     // of a multi-device context settle together, capi.cpp)

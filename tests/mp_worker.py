@@ -180,9 +180,11 @@ def main():
             e7.synchronize()
             S = step.sync_info()[0].shard_elems
             b = step.buffers()
-            half = (step.stats().gathered_max_bytes + 255) // 256 * 256
+            half, slots = step.stats().gather_slot_bytes, step.stats().gather_slots
+            segs = step.sync_info()[1]
             res[pipe] = [e7.d2h(b["master"], r, S) for r in e7.local_ranks] + \
-                        [e7.d2h(b["gathered"], r, 3 * half // 2, "bf16") for r in e7.local_ranks]
+                        [e7.d2h(b["gathered"], r, p * segs[l][1], "bf16", off=(l % slots) * half)
+                         for r in e7.local_ranks for l in range(3)]
             step.close()
             e7.close()
         os.environ.pop("MICS_HIER_PIPE")

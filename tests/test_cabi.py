@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
     assert set(syms) == set(EXPORTS), set(syms) ^ set(EXPORTS)
-    assert lib.mics_abi_version() == 2
+    assert lib.mics_abi_version() == 3
 
 
 def test_status_names_follow_errc_order():

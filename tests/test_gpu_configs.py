@@ -100,7 +100,7 @@ def check_step_sampled(oracle, eng, step, wl, opts, nsamples=300, seed=7):
     f32 or bf16), checked BIT-EXACTLY at sampled shard elements of every rank (both
     ends and every layer boundary included) by replaying the folds and Adam on the
     CPU, and every gathered slot (the last backward gathers left layer l in slot
-    l mod 3) at sampled positions against the group's pre-update bf16 shards."""
+    l mod gather_slots) at sampled positions against the group's pre-update bf16 shards."""
     n, p, s = wl.n, wl.p, wl.s
     info, segs = step.sync_info()
     S = info.shard_elems
@@ -143,21 +143,21 @@ def check_step_sampled(oracle, eng, step, wl, opts, nsamples=300, seed=7):
                 assert eng.d2h(b["master"], r, 1, off=int(x) * 4).view(np.uint32)[0] == u32(wp)[0], (int(x), r)
                 assert eng.d2h(b["exp_avg_sq"], r, 1, off=int(x) * 4).view(np.uint32)[0] == u32(wv)[0], (int(x), r)
                 assert eng.d2h(b["param_bf16"], r, 1, "bf16", off=int(x) * 2)[0] == wb[0], (int(x), r)
-    half = (step.stats().gathered_max_bytes + 255) // 256 * 256
+    half, slots = step.stats().gather_slot_bytes, step.stats().gather_slots
     for l in range(min(3, len(segs))):
         _, cl, sol, _ = segs[l]
         for pos_e in rng.choice(p * cl, 64, replace=False):
             pos, e = divmod(int(pos_e), cl)
             want = oracle.f32_to_bf16(oracle.gen_f32(seed_m, pos, 0, 255, sol + e, 1))[0]
             for r in range(n):
-                got = eng.d2h(b["gathered"], r, 1, "bf16", off=(l % 3) * half + int(pos_e) * 2)[0]
+                got = eng.d2h(b["gathered"], r, 1, "bf16", off=(l % slots) * half + int(pos_e) * 2)[0]
                 assert got == want, (l, r, pos, e)
         # both ends of every slot, every position
         for pos in range(p):
             for e in (0, cl - 1):
                 want = oracle.f32_to_bf16(oracle.gen_f32(seed_m, pos, 0, 255, sol + e, 1))[0]
                 for r in range(n):
-                    got = eng.d2h(b["gathered"], r, 1, "bf16", off=(l % 3) * half + (pos * cl + e) * 2)[0]
+                    got = eng.d2h(b["gathered"], r, 1, "bf16", off=(l % slots) * half + (pos * cl + e) * 2)[0]
                     assert got == want, (l, r, pos, e)
 
 

@@ -132,9 +132,9 @@ def test_step_identical_for_any_gather_grid(monkeypatch, graph):
         step.run(2)
         eng.synchronize()
         b, S = step.buffers(), step.sync_info()[0].shard_elems
-        half = (step.stats().gathered_max_bytes + 255) // 256 * 256
+        half, slots = step.stats().gather_slot_bytes, step.stats().gather_slots
         res.append([(u8(eng.d2h(b["master"], r, S)), u8(eng.d2h(b["exp_avg_sq"], r, S)),
-                     u8(eng.d2h(b["gathered"], r, 3 * half // 2, "bf16"))) for r in range(8)])
+                     u8(eng.d2h(b["gathered"], r, slots * half // 2, "bf16"))) for r in range(8)])
         step.close()
         eng.close()
     for other in res[1:]:

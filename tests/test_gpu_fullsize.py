@@ -52,17 +52,17 @@ def check_sampled(oracle, eng, step, wl, opts, ranks, nsamples=400, seed=7):
             assert got.view(np.uint32)[0] == wp.view(np.uint32)[0], (int(x), r)
             assert eng.d2h(b["param_bf16"], r, 1, "bf16", off=int(x) * 2)[0] == wb[0], (int(x), r)
     # all-gather: the last gathers of the backward pass (layers 2, 1, 0) left layer l in
-    # slot l mod 3 (csrc/step.cpp gather_slots) = the group's pre-update bf16 shards;
+    # slot l mod gather_slots (csrc/step.cpp) = the group's pre-update bf16 shards;
     # they ran as one PDL chain, so this also checks that no earlier gather of a slot
     # landed after the last one
-    half = (step.stats().gathered_max_bytes + 255) // 256 * 256
+    half, slots = step.stats().gather_slot_bytes, step.stats().gather_slots
     for l in range(min(3, len(segs))):
         _, cl, sol, _ = segs[l]
         for pos_e in rng.choice(p * cl, 100, replace=False):
             pos, e = divmod(int(pos_e), cl)
             want = oracle.f32_to_bf16(oracle.gen_f32(seed_m, pos, 0, 255, sol + e, 1))[0]
             for r in ranks[:2]:
-                got = eng.d2h(b["gathered"], r, 1, "bf16", off=(l % 3) * half + int(pos_e) * 2)[0]
+                got = eng.d2h(b["gathered"], r, 1, "bf16", off=(l % slots) * half + int(pos_e) * 2)[0]
                 assert got == want, (l, r, pos, e)
 
 

@@ -91,9 +91,9 @@ def test_step_on_two_gpus_equals_one_gpu(m, p, k, alt, gdt):
         step.run_host(hptr, 1)
         eng.synchronize()
         b, S = step.buffers(), info.shard_elems
-        half = (step.stats().gathered_max_bytes + 255) // 256 * 256
+        half, slots = step.stats().gather_slot_bytes, step.stats().gather_slots
         res.append([(u8(eng.d2h(b["master"], r, S)), u8(eng.d2h(b["exp_avg_sq"], r, S)),
-                     u8(eng.d2h(b["gathered"], r, 3 * half // 2, "bf16"))) for r in range(8)])
+                     u8(eng.d2h(b["gathered"], r, slots * half // 2, "bf16"))) for r in range(8)])
         host_free(hptr)
         step.close()
         eng.close()

@@ -92,12 +92,12 @@ def test_step_matches_cpu_restatement(oracle, alternative, grad_dtype, hier_k, p
     # the last gathers (backward pass, layers 2, 1, 0) left layer l in slot l mod 3
     # (csrc/step.cpp gather_slots): the pre-update bf16 params of the group
     stats = step.stats()
-    half = (stats.gathered_max_bytes + 255) // 256 * 256
+    half, slots = stats.gather_slot_bytes, stats.gather_slots
     for l in range(min(3, len(segs))):
         _, cl, sol, _ = segs[l]
         for r in range(n):
             g = r // p
-            got = eng.d2h(bufs["gathered"], r, p * cl, "bf16", off=(l % 3) * half)
+            got = eng.d2h(bufs["gathered"], r, p * cl, "bf16", off=(l % slots) * half)
             for i in range(p):
                 want_bf = oracle.f32_to_bf16(init[g * p + i][sol:sol + cl])
                 assert np.array_equal(got[i * cl:(i + 1) * cl], want_bf), (l, r, i)
@@ -129,9 +129,12 @@ def test_hier_pipe_matches_per_visit(monkeypatch, graph):
             step.run(3)
             eng.synchronize()
             b, S = step.buffers(), step.sync_info()[0].shard_elems
-            half = (step.stats().gathered_max_bytes + 255) // 256 * 256
-            res.append([(u32(eng.d2h(b["master"], r, S)), eng.d2h(b["gathered"], r, 3 * half // 2, "bf16"))
-                        for r in range(8)])
+            # the last backward gathers (layers 2, 1, 0) are in slot l % gather_slots (4 pipelined, 3 not)
+            half, slots = step.stats().gather_slot_bytes, step.stats().gather_slots
+            segs = step.sync_info()[1]
+            res.append([(u32(eng.d2h(b["master"], r, S)),) +
+                        tuple(eng.d2h(b["gathered"], r, p * segs[l][1], "bf16", off=(l % slots) * half)
+                              for l in range(3)) for r in range(8)])
             step.close()
             eng.close()
         for other in res[1:]:
