@@ -51,7 +51,8 @@ def test_step_cfg_layout_matches_header():
     body = text[text.index("typedef struct {\n  int p, s, nlayers;"):text.index("} mics_step_cfg;")]
     names = re.findall(r"\b(\w+)\s*(?:,|;)", re.sub(r"/\*.*?\*/", "", body, flags=re.S))
     assert [f[0] for f in StepCfg._fields_] == names
-    assert StepStats._fields_[-2:] == [("compute_flops", C.c_double), ("gemm_launches", C.c_uint64)]
+    assert StepStats._fields_[-4:] == [("compute_flops", C.c_double), ("gemm_launches", C.c_uint64),
+                                      ("gather_slots", C.c_uint64), ("gather_slot_bytes", C.c_uint64)]
 
 
 def test_trace_report_parses(tmp_path):
