@@ -76,7 +76,7 @@ void HierPlan::add_group(int stage, const std::vector<std::tuple<const void*, vo
 // peer's stage-1 chunk t, guarded by that chunk's tile flags.
 HierPlan plan_hier(mics_ctx* ctx, int n, int p, int k, uint64_t chunk, int corrupt,
                    const std::function<const void*(int)>& src, const std::function<char*(int, uint64_t)>& dst,
-                   const std::function<uint64_t*(int)>& flags, uint64_t ftiles, int stages) {
+                   const std::function<uint64_t*(int)>& flags, uint64_t ftiles) {
   HierPlan plan;
   const int q = p / k;
   using Item = std::tuple<const void*, void*, uint64_t*>;
@@ -90,44 +90,29 @@ HierPlan plan_hier(mics_ctx* ctx, int n, int p, int k, uint64_t chunk, int corru
         std::vector<Item> s1, s3;
         for (int j2 = 0; j2 < k; ++j2)  // a node peer elsewhere reads / publishes flags across GPUs
           if (j2 != j) plan.sys |= !ctx->local(base + m * k + j2);
-        if (stages & 1)
-          for (int m2 = 0; m2 < q; ++m2) {
-            const uint64_t pos = corrupt ? uint64_t(j) * q + m2 : uint64_t(m2) * k + j;
-            const int from = base + m2 * k + j;
-            s1.emplace_back(src(from), dst(r, pos), flags(r) + uint64_t(m2) * ftiles);
+        for (int m2 = 0; m2 < q; ++m2) {
+          const uint64_t pos = corrupt ? uint64_t(j) * q + m2 : uint64_t(m2) * k + j;
+          const int from = base + m2 * k + j;
+          s1.emplace_back(src(from), dst(r, pos), flags(r) + uint64_t(m2) * ftiles);
+          (ctx->local(from) ? plan.hbm_bytes : plan.remote_bytes) += chunk;
+          plan.hbm_bytes += chunk;
+        }
+        for (int j2 = 0; j2 < k; ++j2) {
+          if (j2 == j) continue;
+          const int from = base + m * k + j2;
+          for (int t = 0; t < q; ++t) {
+            const uint64_t pos = corrupt ? uint64_t(j2) * q + t : uint64_t(t) * k + j2;
+            s3.emplace_back(dst(from, pos), dst(r, pos), flags(from) + uint64_t(t) * ftiles);
             (ctx->local(from) ? plan.hbm_bytes : plan.remote_bytes) += chunk;
             plan.hbm_bytes += chunk;
           }
-        if (stages & 2)
-          for (int j2 = 0; j2 < k; ++j2) {
-            if (j2 == j) continue;
-            const int from = base + m * k + j2;
-            for (int t = 0; t < q; ++t) {
-              const uint64_t pos = corrupt ? uint64_t(j2) * q + t : uint64_t(t) * k + j2;
-              s3.emplace_back(dst(from, pos), dst(r, pos), flags(from) + uint64_t(t) * ftiles);
-              (ctx->local(from) ? plan.hbm_bytes : plan.remote_bytes) += chunk;
-              plan.hbm_bytes += chunk;
-            }
-          }
+        }
         plan.add_group(1, s1, chunk);
         st3.push_back(std::move(s3));
       }
   }
   for (const auto& s3 : st3) plan.add_group(3, s3, chunk);  // every stage-1 tile precedes every stage-3 tile
   return plan;
-}
-
-HierPlan concat_hier(const HierPlan& a, const HierPlan& b) {
-  HierPlan c = a;
-  for (HierSeg g : b.segs) {
-    g.tile0 += a.tiles;
-    c.segs.push_back(g);
-  }
-  c.tiles = a.tiles + b.tiles;
-  c.sys = a.sys || b.sys;
-  c.remote_bytes += b.remote_bytes;
-  c.hbm_bytes += b.hbm_bytes;
-  return c;
 }
 
 void RedPlan::add(const std::vector<const void*>& src, void* dst, uint64_t elems, uint64_t valid) {
@@ -306,8 +291,7 @@ void enqueue(mics_ctx* ctx, const Launch& l, int dep_first, cudaStream_t stream)
   cudaStream_t st = stream ? stream : ctx->stream;
   // A launch without local work still runs (one CTA) when it carries a barrier:
   // the peers count on this process's signals.
-  // (a pipelined hierarchical launch without local work still advances its epochs)
-  if (l.ndesc == 0 && l.bar.mask == 0 && l.kind != Launch::HIER_PIPE) return;
+  if (l.ndesc == 0 && l.bar.mask == 0) return;
   BarrierArg bar = l.bar;
   if (dep_first >= 0) bar.dep_first = dep_first;
   if (bar.mask) bar.dep_first = 1;  // barrier tickets: never overlap the predecessor
@@ -328,11 +312,6 @@ void enqueue(mics_ctx* ctx, const Launch& l, int dep_first, cudaStream_t stream)
     case Launch::HIER:
       launch_hier(st, static_cast<const HierSeg*>(l.d_desc), l.ndesc, l.ntiles, l.grid, ctx->d_hctl + l.hier_chan,
                   l.hier_sys, bar);
-      break;
-    case Launch::HIER_PIPE:
-      launch_hier_pipe(st, static_cast<const HierSeg*>(l.d_desc), l.ndesc, l.ntiles, l.grid,
-                       ctx->d_hctl + l.hier_chan, ctx->d_tab + l.hier_chan,
-                       reinterpret_cast<uint64_t*>(ctx->base + kDoneOffset) + l.hier_chan, l.hpipe, l.hier_sys);
       break;
     case Launch::TAIL:
       launch_tail(st, l.in_t, l.tail_r, l.tail_p, static_cast<const TailJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid,

@@ -79,22 +79,9 @@ struct HierSeg {              // 64 B
 };
 static_assert(sizeof(HierSeg) == 64, "HierSeg layout");
 struct HierCtl {              // per barrier channel, device memory
-  uint64_t epoch;             // k_hier: epoch of the last completed launch
-  uint64_t base;              // k_hier_pipe: epoch of the last launch of the previous micro-step
+  uint64_t epoch;             // epoch of the last completed k_hier launch
   unsigned ticket;            // CTA arrivals of the running launch
   unsigned pad_;
-};
-// Pipelined hierarchical gathers of the step (k_hier_pipe): launch x of a micro-step's
-// V+1 launches runs stage 1 of visit x and stage 3 of visit x-1.
-struct HierPipe {
-  uint32_t x;                 // launch index in the micro-step (epoch = base + x + 1)
-  uint32_t last;              // x == V: advances HierCtl::base at its end
-  uint32_t first;             // x == 0: waits for its predecessor before anything
-  uint32_t dist;              // gather slots - 1: launch x writes after launch x - dist completed everywhere
-  uint64_t done_mask;         // processes whose done counters gate this launch's writes (self included)
-  unsigned* ticket;           // this launch's own CTA ticket (consecutive launches run concurrently)
-  uint32_t diag;              // MICS_HP_DIAG bits (debugging): 1 wait at start, 2 trigger at end, 4 no done gate
-  uint32_t pad_;
 };
 
 struct RedJob {               // one output chunk (one destination rank, one segment)
@@ -162,11 +149,7 @@ struct TailJob {
 struct PeerTab {
   uint64_t* remote_flag[MICS_MAX_WORLD];
   uint64_t* local_flag[MICS_MAX_WORLD];
-  // process w's "last completed pipelined hierarchical launch" epoch on this channel
-  // (arena head, kDoneOffset + 8 * channel), self included
-  uint64_t* done[MICS_MAX_WORLD];
 };
-constexpr uint64_t kDoneOffset = 2048;  // arena head: done counters (after the barrier flag slots)
 
 struct BarrierArg {
   const PeerTab* tab;
@@ -201,8 +184,6 @@ void launch_copy(cudaStream_t s, const CopySeg* segs, int nseg, uint32_t ntiles,
 // sys_scope: some stage-3 reader of a flag is on another GPU (system-scope publication)
 void launch_hier(cudaStream_t s, const HierSeg* segs, int nseg, uint32_t ntiles, int grid, HierCtl* ctl,
                  int sys_scope, const BarrierArg& bar);
-void launch_hier_pipe(cudaStream_t s, const HierSeg* segs, int nseg, uint32_t ntiles, int grid, HierCtl* ctl,
-                      const PeerTab* tab, uint64_t* my_done, const HierPipe& hp, int sys_scope);
 // `table_bytes`: size of the uploaded job table + source-pointer arrays (staged in smem when small)
 void launch_reduce(cudaStream_t s, mics_dtype in_t, mics_dtype acc_t, const RedJob* jobs, int njobs,
                    uint64_t table_bytes, uint32_t max_p, uint32_t ntiles, int grid, double scale, int mode,
@@ -376,12 +357,9 @@ mics_buf hier_flags(mics_ctx* ctx, uint64_t bytes_per_rank);
 inline uint64_t hier_flag_tiles(uint64_t chunk_bytes) { return ceil_div(chunk_bytes, kCopyTile); }
 // src(r): rank r's input chunk; dst(r, pos): position `pos` of rank r's output; flags(r):
 // rank r's flag array ([q][ftiles] u64, peer-mapped for remote ranks).
-// stages: bit 0 = stage 1, bit 1 = stage 3.
 HierPlan plan_hier(mics_ctx* ctx, int n, int p, int k, uint64_t chunk, int corrupt,
                    const std::function<const void*(int)>& src, const std::function<char*(int, uint64_t)>& dst,
-                   const std::function<uint64_t*(int)>& flags, uint64_t ftiles, int stages = 3);
-// the segments of `b` after those of `a`, in one launch
-HierPlan concat_hier(const HierPlan& a, const HierPlan& b);
+                   const std::function<uint64_t*(int)>& flags, uint64_t ftiles);
 struct AdamPlan {
   std::vector<AdamJob> jobs;
   std::vector<std::vector<const void*>> srcs;
@@ -394,10 +372,9 @@ struct AdamPlan {
 
 // A device-resident, replayable launch (built once, launched many times).
 struct Launch {
-  enum Kind { COPY, REDUCE, ADAM, BARRIER, TAIL, HIER, HIER_PIPE } kind = COPY;
+  enum Kind { COPY, REDUCE, ADAM, BARRIER, TAIL, HIER } kind = COPY;
   int tail_r = 0, tail_p = 0;  // TAIL: replicas and group size (mode = 1 zero-accumulate)
-  int hier_sys = 0, hier_chan = 0;  // HIER*: system-scope flags; channel of its epoch counter
-  HierPipe hpipe{};                  // HIER_PIPE
+  int hier_sys = 0, hier_chan = 0;  // HIER: system-scope flags; channel of its epoch counter
   void* d_desc = nullptr;  // owned device table (cudaMalloc)
   uint64_t table_bytes = 0;
   uint32_t max_p = 1;

@@ -361,82 +361,6 @@ __global__ void __launch_bounds__(kThreads) k_hier(const HierSeg* __restrict__ g
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Pipelined hierarchical gathers of the step (no barrier anywhere): launch x of a
-// micro-step's V+1 launches (V = 2L layer visits) runs stage 1 of visit x and stage 3
-// of visit x-1 (HierPipe), so each visit's NVLink-bound stage 1 overlaps the previous
-// visit's stage 3, and consecutive launches overlap through PDL:
-//  - it triggers its successor at once and waits for its predecessor only at its end
-//    (completion order), except launch 0, which waits first (it follows the
-//    reduce-scatter / boundary that wrote the shards and HierCtl::base);
-//  - read-after-write: a stage-3 tile waits for the node peer's flag of the stage-1
-//    tile it reads (published by launch x-1, epoch base + x);
-//  - write-after-read / write-after-write on the gather slots: before writing, every
-//    CTA waits until each process hosting a node peer, and this one, completed launch
-//    x - dist (done counters): with dist = slots - 1 every earlier reader and writer of
-//    the slot launch x writes (visit x - slots, read by stage 3 in launch x - dist) is done.
-// No tile ever waits on a tile of the same or a later launch, so no CTA can block one
-// that would unblock it; a launch's successor becomes resident only once all its CTAs
-// have started.
-__global__ void __launch_bounds__(kThreads) k_hier_pipe(const HierSeg* __restrict__ gsegs, int nseg,
-                                                        uint32_t table_bytes, uint32_t ntiles, HierCtl* ctl,
-                                                        const PeerTab* __restrict__ tab, uint64_t* my_done,
-                                                        HierPipe hp, int sys_scope) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const bool staged = table_bytes != 0;
-  if (staged) {
-    const uint4* s = reinterpret_cast<const uint4*>(gsegs);
-    uint4* d = reinterpret_cast<uint4*>(smem);
-    for (uint32_t i = threadIdx.x; i < table_bytes / 16; i += kThreads) d[i] = s[i];
-  }
-  __syncthreads();
-  const HierSeg* segs = staged ? reinterpret_cast<const HierSeg*>(smem) : gsegs;
-  if (hp.first || (hp.diag & 1)) asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (!(hp.diag & 2)) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const uint64_t base = *reinterpret_cast<volatile uint64_t*>(&ctl->base);
-  const uint64_t epoch = base + hp.x + 1;
-  if (threadIdx.x == 0 && hp.x >= hp.dist && !(hp.diag & 4)) {  // write-after-read / -write gate
-    const uint64_t target = epoch - hp.dist;
-    for (uint64_t m = hp.done_mask; m; m &= m - 1) {
-      const int w = __ffsll(static_cast<long long>(m)) - 1;
-      wait_flag(tab->done[w], target, sys_scope);
-    }
-  }
-  __syncthreads();
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    int idx = find_desc(segs, nseg, tile);
-    uint32_t rel = tile - segs[idx].tile0;
-    const uint32_t k = segs[idx].gsize;
-    if (k > 1) {
-      idx = idx - int(k) + 1 + int(rel % k);
-      rel /= k;
-    }
-    const HierSeg& s = segs[idx];
-    const uint64_t off = uint64_t(rel) * kCopyTile;
-    const uint64_t rem = s.bytes - off;
-    const uint32_t nb = rem < kCopyTile ? uint32_t(rem) : kCopyTile;
-    if (s.stage == 3) {  // the previous visit's stage-1 tile of the node peer
-      if (threadIdx.x == 0) wait_flag(s.flags + rel, epoch - 1, sys_scope);
-      __syncthreads();
-      copy_tile<true>(s.src + off, s.dst + off, nb);
-    } else {
-      copy_tile<false>(s.src + off, s.dst + off, nb);
-      __syncthreads();
-      if (threadIdx.x == 0) publish_flag(s.flags + rel, epoch, sys_scope);
-    }
-  }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // completion order: the predecessor is done
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_gpu();  // this CTA's stores before its ticket
-    if (atomicAdd(hp.ticket, 1u) == gridDim.x - 1) {  // last CTA: launch x (and every earlier one) done
-      *hp.ticket = 0;
-      if (hp.last) ctl->base = epoch;
-      publish_flag(my_done, epoch, sys_scope);
-    }
-  }
-  if (hp.diag & 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
 // ---------------------------------------------------------------- K2: reduce engine
 template <typename T> struct Arith;
 template <> struct Arith<float> {
@@ -1040,12 +964,6 @@ void launch_hier(cudaStream_t s, const HierSeg* segs, int nseg, uint32_t ntiles,
                  int sys_scope, const BarrierArg& bar) {
   const uint32_t tb = uint64_t(nseg) * sizeof(HierSeg) <= uint64_t(kSmemTable) ? uint32_t(nseg * sizeof(HierSeg)) : 0u;
   launch_ex(k_hier, grid, kThreads, tb, s, segs, nseg, tb, ntiles, ctl, sys_scope, bar);
-}
-
-void launch_hier_pipe(cudaStream_t s, const HierSeg* segs, int nseg, uint32_t ntiles, int grid, HierCtl* ctl,
-                      const PeerTab* tab, uint64_t* my_done, const HierPipe& hp, int sys_scope) {
-  const uint32_t tb = uint64_t(nseg) * sizeof(HierSeg) <= uint64_t(kSmemTable) ? uint32_t(nseg * sizeof(HierSeg)) : 0u;
-  launch_ex(k_hier_pipe, grid, kThreads, tb, s, segs, nseg, tb, ntiles, ctl, tab, my_done, hp, sys_scope);
 }
 
 uint32_t reduce_tile_elems(mics_dtype in_t) {

@@ -36,8 +36,6 @@ constexpr uint32_t kAlignElems = 8;
 void release(mics_step* st) {
   for (auto& v : st->ag)
     for (auto& l : v) l.release();
-  for (auto& l : st->agp) l.release();
-  if (st->d_hp_tickets) cudaFree(st->d_hp_tickets);
   for (auto& v : st->micro)
     for (auto& l : v) l.release();
   st->bnd.rs.release();
@@ -110,59 +108,6 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan) {
       [&](int r) { return reinterpret_cast<uint64_t*>(ctx->rank_ptr(st->hflags, r)); }, st->hflag_tiles);
   out.push_back(make_hier_launch(ctx, plan, ctx->barrier(0, 0, 0), chan, true));
   return out;
-}
-
-// The pipelined hierarchical gathers of one micro-step (comm-only step, k_hier_pipe):
-// V+1 launches for the V = 2L layer visits (forward 0..L-1, backward L-1..0); launch x
-// runs stage 1 of visit x and stage 3 of visit x-1.  Stage-1 flags are kept per gather
-// slot, so a visit's flags are only rewritten by a later visit of the same slot, which
-// the done gate orders after every reader of the earlier one (kernels.cu k_hier_pipe).
-void build_hier_pipe(mics_step* st) {
-  mics_ctx* ctx = st->ctx;
-  mics_sync* sy = st->sync;
-  const int L = st->cfg.nlayers, p = sy->p, n = sy->n, k = st->cfg.hier_k, q = p / k;
-  std::vector<int> visits;
-  for (int l = 0; l < L; ++l) visits.push_back(l);
-  for (int l = L; l-- > 0;) visits.push_back(l);
-  auto stage = [&](int v, int which) {
-    const int l = visits[size_t(v)];
-    const uint64_t cb = sy->chunk[size_t(l)] * 2, soff = sy->shard_off[size_t(l)] * 2;
-    const uint64_t goff = uint64_t(l % st->gather_slots) * st->gathered_half;
-    const uint64_t foff = uint64_t(l % st->gather_slots) * uint64_t(q) * st->hflag_tiles;
-    return plan_hier(
-        ctx, n, p, k, cb, 0, [&](int r) { return static_cast<const void*>(ctx->rank_ptr(st->pbf16, r) + soff); },
-        [&](int r, uint64_t pos) { return ctx->rank_ptr(st->gathered, r) + goff + pos * cb; },
-        [&](int r) { return reinterpret_cast<uint64_t*>(ctx->rank_ptr(st->hflags, r)) + foff; }, st->hflag_tiles,
-        which);
-  };
-  // processes hosting a node peer of a local rank, and this one (the done gate)
-  uint64_t done_mask = 1ull << ctx->wrank;
-  for (int r = 0; r < n; ++r) {
-    if (!ctx->local(r)) continue;
-    const int base = r / p * p, m = (r - base) / k;
-    for (int j2 = 0; j2 < k; ++j2) done_mask |= 1ull << ctx->process_of(base + m * k + j2);
-  }
-  const int V = int(visits.size());
-  MICS_CUDA(cudaMalloc(&st->d_hp_tickets, sizeof(unsigned) * size_t(V + 1)));
-  MICS_CUDA(cudaMemset(st->d_hp_tickets, 0, sizeof(unsigned) * size_t(V + 1)));
-  for (int x = 0; x <= V; ++x) {
-    HierPlan plan;
-    if (x < V) plan = stage(x, 1);
-    if (x > 0) plan = concat_hier(plan, stage(x - 1, 2));
-    Launch l = make_hier_launch(ctx, plan, ctx->barrier(0, 0, 0), 0, true);
-    l.kind = Launch::HIER_PIPE;
-    l.hpipe.x = uint32_t(x);
-    l.hpipe.last = x == V;
-    l.hpipe.first = x == 0;
-    l.hpipe.dist = uint32_t(st->gather_slots - 1);
-    l.hpipe.done_mask = ctx->ipc_ready ? done_mask : (1ull << ctx->wrank);
-    l.hpipe.ticket = st->d_hp_tickets + x;
-    if (const char* e = std::getenv("MICS_HP_DIAG")) l.hpipe.diag = uint32_t(std::atoi(e));
-    if (const char* e = std::getenv("MICS_HP_DIST")) l.hpipe.dist = uint32_t(std::atoi(e));
-    // consecutive launches overlap (PDL): each gets a share of the SMs, like the flat chain
-    l.grid = ctx->grid_for(plan.tiles, std::max(1, ctx->occ_hier / 2));
-    st->agp.push_back(l);
-  }
 }
 
 void enqueue_generate(mics_step* st, int t) {
@@ -350,10 +295,6 @@ void enqueue_fused_tail(mics_step* st) {
 // the fence positions are the ones counted here.
 void enqueue_gathers(mics_step* st, int t) {
   mics_ctx* ctx = st->ctx;
-  if (!st->agp.empty()) {  // pipelined hierarchical gathers (they order themselves)
-    for (const Launch& x : st->agp) enqueue(ctx, x);
-    return;
-  }
   bool first = true;
   const int m = st->gather_slots - 1;
   int pos = 0;
@@ -807,14 +748,8 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
     st->v = alloc_sym(ctx, S * 4);
     // Without compute nothing consumes a gather, so up to three run concurrently
     // (enqueue_gathers): three slots.  With compute a layer's GEMMs release its slot.
-    // Pipelined hierarchical gathers (k_hier_pipe; MICS_HIER_PIPE=0: one k_hier launch per
-    // visit, as with compute) keep four: launch x may then write once launch x-3 is done
-    // everywhere (the done gate), so three consecutive launches overlap (with a gate at
-    // x-2, i.e. three slots, the pipeline measured to stall, tools/gpu_runs/R2_h.sh).
     const bool hier = cfg->hier_k > 0 && cfg->p > cfg->hier_k;
-    const char* hpe = std::getenv("MICS_HIER_PIPE");
-    const bool hpipe = hier && !cfg->compute && !(hpe && hpe[0] == '0');
-    st->gather_slots = cfg->compute ? 2 : hpipe ? 4 : 3;
+    st->gather_slots = cfg->compute ? 2 : 3;
     if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)
       st->gather_slots = std::max(2, std::min(kMaxGatherSlots, std::atoi(e)));
     st->gathered = alloc_sym(ctx, uint64_t(st->gather_slots) * st->gathered_half);
@@ -844,16 +779,14 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
       for (int t = 0; t < cfg->s; ++t) enqueue_generate(st, t);
     }
     // plans
-    if (hier) {  // stage-1 tile flags of the hierarchical gathers (per gather slot when pipelined)
+    if (hier) {  // stage-1 tile flags of the hierarchical gathers
       uint64_t cmax = 0;
       for (uint64_t c : sy->chunk) cmax = std::max(cmax, c * 2);
       st->hflag_tiles = hier_flag_tiles(cmax);
-      st->hflags = alloc_sym(ctx, uint64_t(hpipe ? st->gather_slots : 1) * uint64_t(cfg->p / cfg->hier_k) *
-                                      st->hflag_tiles * 8);
+      st->hflags = alloc_sym(ctx, uint64_t(cfg->p / cfg->hier_k) * st->hflag_tiles * 8);
       MICS_CUDA(cudaMemsetAsync(ctx->base + st->hflags.offset, 0, st->hflags.stride * uint64_t(ctx->per), ctx->stream));
     }
     for (int l = 0; l < cfg->nlayers; ++l) st->ag.push_back(build_layer_ag(st, l, cfg->compute ? 1 : 0));
-    if (hpipe) build_hier_pipe(st);
     for (int t = 0; t < cfg->s; ++t) {
       const uint64_t goff = uint64_t(t % st->gslots) * sy->grad_elems * szg;
       const int mode = t == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE;
@@ -953,20 +886,12 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
     // kernels and algorithmic bytes of one step on this process (enqueue() skips empty launches)
     auto runs = [](const Launch& x) -> uint64_t { return (x.ndesc || x.bar.mask) ? 1 : 0; };
     mics_step_stats& S2 = st->stats;
-    if (!st->agp.empty()) {
-      for (auto& x : st->agp) {  // one micro-step's pipelined launches
-        S2.ag_launches += uint64_t(cfg->s);
-        S2.ag_remote_bytes += uint64_t(cfg->s) * x.remote_bytes;
-        S2.ag_hbm_bytes += uint64_t(cfg->s) * x.hbm_bytes;
+    for (auto& v : st->ag)
+      for (auto& x : v) {  // forward + backward pass, every micro-step
+        S2.ag_launches += 2 * uint64_t(cfg->s) * runs(x);
+        S2.ag_remote_bytes += 2 * uint64_t(cfg->s) * x.remote_bytes;
+        S2.ag_hbm_bytes += 2 * uint64_t(cfg->s) * x.hbm_bytes;
       }
-    } else {
-      for (auto& v : st->ag)
-        for (auto& x : v) {  // forward + backward pass, every micro-step
-          S2.ag_launches += 2 * uint64_t(cfg->s) * runs(x);
-          S2.ag_remote_bytes += 2 * uint64_t(cfg->s) * x.remote_bytes;
-          S2.ag_hbm_bytes += 2 * uint64_t(cfg->s) * x.hbm_bytes;
-        }
-    }
     for (size_t t = 0; t < st->micro.size(); ++t) {
       if ((st->tail || st->fused_tail) && t + 1 == st->micro.size()) continue;  // replaced by the tail launches
       for (auto& x : st->micro[t]) {

@@ -76,10 +76,7 @@ struct mics_step {
   uint64_t gathered_half = 0;                 // bytes of one gathered buffer (slot)
   int gather_slots = 2;                       // layer l gathers into slot l % gather_slots
   std::vector<std::vector<mics::Launch>> ag;  // per layer: 1 launch (k_copy flat or k_hier)
-  // pipelined hierarchical gathers of one micro-step (k_hier_pipe, comm-only step): 2L+1 launches
-  std::vector<mics::Launch> agp;
-  unsigned* d_hp_tickets = nullptr;  // [2L+1] CTA tickets, one per pipelined launch
-  // hierarchical gathers: per rank [slots][q][hflag_tiles] (pipelined) or [q][hflag_tiles] u64 flags
+  // hierarchical gathers (k_hier): per rank [q][hflag_tiles] u64 stage-1 tile flags
   mics_buf hflags{};
   uint64_t hflag_tiles = 0;
   // per micro-step: the 2-hop reduce-scatter, or the alternative schedule's
