@@ -734,6 +734,9 @@ def run_mics(args, wl, rank, world, local):
         ems = max_over_ranks(max(h0.elapsed_time(h1) / args.e2e_steps, wall * 1e3), world)
         e2e = {"value": samples / (ems / 1e3), "unit": "samples/s", "ms_per_step": ems,
                "h2d_bytes_per_step": per * s * gbytes, "d2h_bytes_per_step": per * min(4096, S) * 4,
+               "h2d_GBps_per_gpu": per * s * gbytes / (ems / 1e3) / 1e9,
+               "bound": "host link: every rank's fp32 gradients of every micro-step cross PCIe (the reference API "
+                        "takes host gradients); h2d_GBps_per_gpu is the achieved host->GPU rate",
                "path": "mics_step_run_host (C-ABI): pinned host gradients -> H2D every micro-step, "
                        "result slice D2H after the boundary",
                "host_cpus": numa}
