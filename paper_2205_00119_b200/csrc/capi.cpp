@@ -102,8 +102,18 @@ mics_plan* make_plan(mics_ctx* ctx, F&& build) {
   return p;
 }
 
+// Every entry point: exceptions become a status, and the caller's current CUDA device
+// is restored (a multi-device context switches devices member by member).
 template <typename F>
 mics_status guard(F&& f) {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+  struct Restore {
+    int d;
+    ~Restore() {
+      if (d >= 0) cudaSetDevice(d);
+    }
+  } restore{dev};
   try {
     f();
     g_last_error.clear();

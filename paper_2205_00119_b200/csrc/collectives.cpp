@@ -51,7 +51,7 @@ void CopyPlan::add_group(const std::vector<std::pair<const void*, std::vector<vo
 }
 
 void HierPlan::add_group(int stage, const std::vector<std::tuple<const void*, void*, uint64_t*>>& items,
-                         uint64_t bytes) {
+                         uint64_t bytes, int lag) {
   if (bytes == 0 || items.empty()) return;
   const uint32_t t0 = tiles, per = uint32_t(ceil_div(bytes, kCopyTile)), k = uint32_t(items.size());
   for (const auto& [s, d, f] : items) {
@@ -64,6 +64,7 @@ void HierPlan::add_group(int stage, const std::vector<std::tuple<const void*, vo
     g.tile0 = t0;
     g.gsize = k;
     g.stage = uint32_t(stage);
+    g.lag = uint32_t(lag);
     segs.push_back(g);
   }
   tiles = t0 + k * per;
@@ -76,7 +77,7 @@ void HierPlan::add_group(int stage, const std::vector<std::tuple<const void*, vo
 // peer's stage-1 chunk t, guarded by that chunk's tile flags.
 HierPlan plan_hier(mics_ctx* ctx, int n, int p, int k, uint64_t chunk, int corrupt,
                    const std::function<const void*(int)>& src, const std::function<char*(int, uint64_t)>& dst,
-                   const std::function<uint64_t*(int)>& flags, uint64_t ftiles) {
+                   const std::function<uint64_t*(int)>& flags, uint64_t ftiles, int stages, int lag) {
   HierPlan plan;
   const int q = p / k;
   using Item = std::tuple<const void*, void*, uint64_t*>;
@@ -90,14 +91,14 @@ HierPlan plan_hier(mics_ctx* ctx, int n, int p, int k, uint64_t chunk, int corru
         std::vector<Item> s1, s3;
         for (int j2 = 0; j2 < k; ++j2)  // a node peer elsewhere reads / publishes flags across GPUs
           if (j2 != j) plan.sys |= !ctx->local(base + m * k + j2);
-        for (int m2 = 0; m2 < q; ++m2) {
+        for (int m2 = 0; m2 < q && (stages & 1); ++m2) {
           const uint64_t pos = corrupt ? uint64_t(j) * q + m2 : uint64_t(m2) * k + j;
           const int from = base + m2 * k + j;
           s1.emplace_back(src(from), dst(r, pos), flags(r) + uint64_t(m2) * ftiles);
           (ctx->local(from) ? plan.hbm_bytes : plan.remote_bytes) += chunk;
           plan.hbm_bytes += chunk;
         }
-        for (int j2 = 0; j2 < k; ++j2) {
+        for (int j2 = 0; j2 < k && (stages & 2); ++j2) {
           if (j2 == j) continue;
           const int from = base + m * k + j2;
           for (int t = 0; t < q; ++t) {
@@ -111,8 +112,21 @@ HierPlan plan_hier(mics_ctx* ctx, int n, int p, int k, uint64_t chunk, int corru
         st3.push_back(std::move(s3));
       }
   }
-  for (const auto& s3 : st3) plan.add_group(3, s3, chunk);  // every stage-1 tile precedes every stage-3 tile
+  for (const auto& s3 : st3) plan.add_group(3, s3, chunk, lag);  // every stage-1 tile precedes every stage-3 tile
   return plan;
+}
+
+HierPlan concat_hier(const HierPlan& a, const HierPlan& b) {
+  HierPlan c = a;
+  for (HierSeg g : b.segs) {
+    g.tile0 += a.tiles;
+    c.segs.push_back(g);
+  }
+  c.tiles = a.tiles + b.tiles;
+  c.sys = a.sys || b.sys;
+  c.remote_bytes += b.remote_bytes;
+  c.hbm_bytes += b.hbm_bytes;
+  return c;
 }
 
 void RedPlan::add(const std::vector<const void*>& src, void* dst, uint64_t elems, uint64_t valid) {

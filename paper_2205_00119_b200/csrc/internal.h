@@ -75,7 +75,8 @@ struct HierSeg {              // 64 B
   uint32_t tile0;             // first tile of this segment's stripe group
   uint32_t gsize;             // segments in the stripe group (equal sizes, tiles interleaved)
   uint32_t stage;             // 1 or 3
-  uint32_t pad_[5];
+  uint32_t lag;               // stage 3: its source tiles were published `lag` launches back (0 or 1)
+  uint32_t pad_[4];
 };
 static_assert(sizeof(HierSeg) == 64, "HierSeg layout");
 struct HierCtl {              // per barrier channel, device memory
@@ -348,7 +349,8 @@ struct HierPlan {
   bool sys = false;  // a node peer of a local rank lives in another process
   uint64_t remote_bytes = 0, hbm_bytes = 0;
   // items: (src, dst, flags); equal sizes, tiles interleaved (stripe group)
-  void add_group(int stage, const std::vector<std::tuple<const void*, void*, uint64_t*>>& items, uint64_t bytes);
+  void add_group(int stage, const std::vector<std::tuple<const void*, void*, uint64_t*>>& items, uint64_t bytes,
+                 int lag = 0);
 };
 // The ad-hoc hierarchical all-gathers' flag array (>= bytes per rank, zeroed), carved
 // from the top of the arena so mark/release of the bump allocator never frees it.
@@ -357,9 +359,12 @@ mics_buf hier_flags(mics_ctx* ctx, uint64_t bytes_per_rank);
 inline uint64_t hier_flag_tiles(uint64_t chunk_bytes) { return ceil_div(chunk_bytes, kCopyTile); }
 // src(r): rank r's input chunk; dst(r, pos): position `pos` of rank r's output; flags(r):
 // rank r's flag array ([q][ftiles] u64, peer-mapped for remote ranks).
+// stages: bit 0 = stage 1, bit 1 = stage 3; lag: see HierSeg::lag
 HierPlan plan_hier(mics_ctx* ctx, int n, int p, int k, uint64_t chunk, int corrupt,
                    const std::function<const void*(int)>& src, const std::function<char*(int, uint64_t)>& dst,
-                   const std::function<uint64_t*(int)>& flags, uint64_t ftiles);
+                   const std::function<uint64_t*(int)>& flags, uint64_t ftiles, int stages = 3, int lag = 0);
+// the segments of `b` after those of `a`, in one launch
+HierPlan concat_hier(const HierPlan& a, const HierPlan& b);
 struct AdamPlan {
   std::vector<AdamJob> jobs;
   std::vector<std::vector<const void*>> srcs;

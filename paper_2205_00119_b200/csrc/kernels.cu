@@ -308,13 +308,16 @@ __device__ __forceinline__ void wait_flag(const uint64_t* f, uint64_t v, int sys
   }
 }
 
-// Stage 1 and stage 3 of every local rank's hierarchical all-gather in one grid (see
-// HierSeg).  PDL: the launch waits for its predecessor before anything (the epoch and,
-// in the step, the write-after-read order of the gather slots: a rank's visit i+1
-// completes only after every node peer started visit i+1, i.e. finished reading
-// visit i), and lets its successor launch only at its very end — an early successor's
-// CTAs would hold SM slots a not-yet-resident CTA of this grid needs to publish the
-// flags resident CTAs are waiting for.  The grid is one resident wave.
+// Stage 1 and stage 3 of hierarchical all-gathers in one grid (see HierSeg): one layer
+// visit (lag-0 stage-3 segments wait for this launch's stage-1 tiles), or, in the
+// comm-only step, stage 1 of visit x with stage 3 of visit x-1 (lag 1: their flags were
+// published by the previous launch).  PDL: the launch waits for its predecessor before
+// anything (the epoch, and in the step the write-after-read order of the gather slots:
+// a rank's launch x completes only after each node peer started launch x, i.e.
+// finished launch x-1) and lets its successor launch only at its very end — an early
+// successor's CTAs could hold SM slots a not-yet-resident CTA of this grid needs to
+// publish the flags resident CTAs are waiting for (profiles/r2/hier_pipe_README.md).
+// The grid is one resident wave.
 __global__ void __launch_bounds__(kThreads) k_hier(const HierSeg* __restrict__ gsegs, int nseg, uint32_t table_bytes,
                                                    uint32_t ntiles, HierCtl* ctl, int sys_scope, BarrierArg bar) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(kThreads) k_hier(const HierSeg* __restrict__ g
     const uint64_t rem = s.bytes - off;
     const uint32_t nb = rem < kCopyTile ? uint32_t(rem) : kCopyTile;
     if (s.stage == 3) {  // the node peer's stage-1 tile must be published first
-      if (threadIdx.x == 0) wait_flag(s.flags + rel, epoch, sys_scope);
+      if (threadIdx.x == 0) wait_flag(s.flags + rel, epoch - s.lag, sys_scope);
       __syncthreads();
       copy_tile<true>(s.src + off, s.dst + off, nb);
     } else {

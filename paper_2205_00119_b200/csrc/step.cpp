@@ -36,6 +36,7 @@ constexpr uint32_t kAlignElems = 8;
 void release(mics_step* st) {
   for (auto& v : st->ag)
     for (auto& l : v) l.release();
+  for (auto& l : st->agm) l.release();
   for (auto& v : st->micro)
     for (auto& l : v) l.release();
   st->bnd.rs.release();
@@ -108,6 +109,41 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan) {
       [&](int r) { return reinterpret_cast<uint64_t*>(ctx->rank_ptr(st->hflags, r)); }, st->hflag_tiles);
   out.push_back(make_hier_launch(ctx, plan, ctx->barrier(0, 0, 0), chan, true));
   return out;
+}
+
+// Hierarchical gathers of one micro-step in the comm-only step: 2L+1 k_hier launches for
+// the V = 2L layer visits (forward 0..L-1, backward L-1..0); launch x runs stage 1 of
+// visit x and stage 3 of visit x-1, so each visit's NVLink-bound stage 1 overlaps the
+// previous visit's stage 3, with no barrier: stage 3 waits for the node peers' flags of
+// the previous launch.  Launches are serial on a GPU, and a rank's launch x completes
+// only after every node peer's launch x started (its lag-1 flags), i.e. after the
+// peer's launch x-1 — which read the slot launch x-3 wrote; with four gather slots two
+// visits of one slot are at least four launches apart, so no slot is rewritten while a
+// peer may read it (and the turn's repeated layer rewrites identical bytes).
+void build_hier_merged(mics_step* st) {
+  mics_ctx* ctx = st->ctx;
+  mics_sync* sy = st->sync;
+  const int L = st->cfg.nlayers, p = sy->p, n = sy->n, k = st->cfg.hier_k;
+  std::vector<int> visits;
+  for (int l = 0; l < L; ++l) visits.push_back(l);
+  for (int l = L; l-- > 0;) visits.push_back(l);
+  auto stage = [&](int v, int which) {
+    const int l = visits[size_t(v)];
+    const uint64_t cb = sy->chunk[size_t(l)] * 2, soff = sy->shard_off[size_t(l)] * 2;
+    const uint64_t goff = uint64_t(l % st->gather_slots) * st->gathered_half;
+    return plan_hier(
+        ctx, n, p, k, cb, 0, [&](int r) { return static_cast<const void*>(ctx->rank_ptr(st->pbf16, r) + soff); },
+        [&](int r, uint64_t pos) { return ctx->rank_ptr(st->gathered, r) + goff + pos * cb; },
+        [&](int r) { return reinterpret_cast<uint64_t*>(ctx->rank_ptr(st->hflags, r)); }, st->hflag_tiles, which,
+        which == 2 ? 1 : 0);
+  };
+  const int V = int(visits.size());
+  for (int x = 0; x <= V; ++x) {
+    HierPlan plan;
+    if (x < V) plan = stage(x, 1);
+    if (x > 0) plan = concat_hier(plan, stage(x - 1, 2));
+    st->agm.push_back(make_hier_launch(ctx, plan, ctx->barrier(0, 0, 0), 0, true));
+  }
 }
 
 void enqueue_generate(mics_step* st, int t) {
@@ -295,6 +331,10 @@ void enqueue_fused_tail(mics_step* st) {
 // the fence positions are the ones counted here.
 void enqueue_gathers(mics_step* st, int t) {
   mics_ctx* ctx = st->ctx;
+  if (!st->agm.empty()) {  // merged hierarchical sequence (k_hier orders itself: flags, serial launches)
+    for (const Launch& x : st->agm) enqueue(ctx, x);
+    return;
+  }
   bool first = true;
   const int m = st->gather_slots - 1;
   int pos = 0;
@@ -748,8 +788,11 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
     st->v = alloc_sym(ctx, S * 4);
     // Without compute nothing consumes a gather, so up to three run concurrently
     // (enqueue_gathers): three slots.  With compute a layer's GEMMs release its slot.
+    // The merged hierarchical sequence of the comm-only step keeps four (build_hier_merged).
     const bool hier = cfg->hier_k > 0 && cfg->p > cfg->hier_k;
-    st->gather_slots = cfg->compute ? 2 : 3;
+    const char* hme = std::getenv("MICS_HIER_MERGE");  // 0: one k_hier launch per visit (A/B runs)
+    const bool hmerge = hier && !cfg->compute && !(hme && hme[0] == '0');
+    st->gather_slots = cfg->compute ? 2 : hmerge ? 4 : 3;
     if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)
       st->gather_slots = std::max(2, std::min(kMaxGatherSlots, std::atoi(e)));
     st->gathered = alloc_sym(ctx, uint64_t(st->gather_slots) * st->gathered_half);
@@ -787,6 +830,7 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
       MICS_CUDA(cudaMemsetAsync(ctx->base + st->hflags.offset, 0, st->hflags.stride * uint64_t(ctx->per), ctx->stream));
     }
     for (int l = 0; l < cfg->nlayers; ++l) st->ag.push_back(build_layer_ag(st, l, cfg->compute ? 1 : 0));
+    if (hmerge) build_hier_merged(st);
     for (int t = 0; t < cfg->s; ++t) {
       const uint64_t goff = uint64_t(t % st->gslots) * sy->grad_elems * szg;
       const int mode = t == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE;
@@ -886,12 +930,20 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
     // kernels and algorithmic bytes of one step on this process (enqueue() skips empty launches)
     auto runs = [](const Launch& x) -> uint64_t { return (x.ndesc || x.bar.mask) ? 1 : 0; };
     mics_step_stats& S2 = st->stats;
-    for (auto& v : st->ag)
-      for (auto& x : v) {  // forward + backward pass, every micro-step
-        S2.ag_launches += 2 * uint64_t(cfg->s) * runs(x);
-        S2.ag_remote_bytes += 2 * uint64_t(cfg->s) * x.remote_bytes;
-        S2.ag_hbm_bytes += 2 * uint64_t(cfg->s) * x.hbm_bytes;
+    if (!st->agm.empty()) {
+      for (auto& x : st->agm) {  // one micro-step's merged launches
+        S2.ag_launches += uint64_t(cfg->s) * runs(x);
+        S2.ag_remote_bytes += uint64_t(cfg->s) * x.remote_bytes;
+        S2.ag_hbm_bytes += uint64_t(cfg->s) * x.hbm_bytes;
       }
+    } else {
+      for (auto& v : st->ag)
+        for (auto& x : v) {  // forward + backward pass, every micro-step
+          S2.ag_launches += 2 * uint64_t(cfg->s) * runs(x);
+          S2.ag_remote_bytes += 2 * uint64_t(cfg->s) * x.remote_bytes;
+          S2.ag_hbm_bytes += 2 * uint64_t(cfg->s) * x.hbm_bytes;
+        }
+    }
     for (size_t t = 0; t < st->micro.size(); ++t) {
       if ((st->tail || st->fused_tail) && t + 1 == st->micro.size()) continue;  // replaced by the tail launches
       for (auto& x : st->micro[t]) {

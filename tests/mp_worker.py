@@ -166,6 +166,31 @@ def main():
         step.close()
         e2.close()
 
+    # ---- merged hierarchical launches (flags across processes; node peers on other GPUs
+    # for p=8, k=4) vs one k_hier launch per visit, over 3 steps: same bits
+    for p, k in ((4, 2), (8, 4)):
+        res = {}
+        for merge in ("1", "0"):
+            os.environ["MICS_HIER_MERGE"] = merge
+            e7 = Engine(n_ranks=n, world=world, world_rank=rank, device=local, arena_bytes=256 << 20)
+            mdist.connect(e7)
+            step = MicsStep(e7, Workload("hm", [70_000, 12_345, 40_000, 9_999, 33_333], p=p, s=2, hier_k=k),
+                            StepOptions(seed=5))
+            step.run(3)
+            e7.synchronize()
+            S = step.sync_info()[0].shard_elems
+            b = step.buffers()
+            half, slots = step.stats().gather_slot_bytes, step.stats().gather_slots
+            segs = step.sync_info()[1]
+            res[merge] = [e7.d2h(b["master"], r, S) for r in e7.local_ranks] + \
+                         [e7.d2h(b["gathered"], r, p * segs[l][1], "bf16", off=(l % slots) * half)
+                          for r in e7.local_ranks for l in range(3)]
+            step.close()
+            e7.close()
+        os.environ.pop("MICS_HIER_MERGE")
+        for x, y in zip(res["0"], res["1"]):
+            expect(np.array_equal(x.view(np.uint16), y.view(np.uint16)), f"hier merged != per-visit (p={p}, k={k})")
+
     # ---- full-size C3 step across processes: sampled elements bit-exact (test_gpu_fullsize)
     from test_gpu_fullsize import check_sampled
     import bench

@@ -101,11 +101,44 @@ def test_step_matches_cpu_restatement(oracle, alternative, grad_dtype, hier_k, p
             for i in range(p):
                 want_bf = oracle.f32_to_bf16(init[g * p + i][sol:sol + cl])
                 assert np.array_equal(got[i * cl:(i + 1) * cl], want_bf), (l, r, i)
-    # one launch per layer visit, flat (k_copy) or hierarchical (k_hier)
-    want_ag = 2 * s * len(layers)
+    # flat: one k_copy launch per layer visit; hierarchical: 2L+1 merged k_hier launches per
+    # micro-step (launch x = stage 1 of visit x + stage 3 of visit x-1)
+    want_ag = s * (2 * len(layers) + 1) if hier_k and p > hier_k else 2 * s * len(layers)
     assert stats.launches > 0 and stats.ag_launches == want_ag
     step.close()
     eng.close()
+
+
+@pytest.mark.parametrize("graph", ["1", "0"])
+def test_hier_merged_matches_per_visit(monkeypatch, graph):
+    """The comm-only step's merged hierarchical launches (launch x = stage 1 of visit x +
+    stage 3 of visit x-1, flags instead of barriers, four gather slots) vs one k_hier
+    launch per visit (MICS_HIER_MERGE=0): same parameters and gathered layers over three
+    steps, at p=4/k=2 and p=8/k=4, with the default grid and a 5-CTA cap."""
+    from paper_2205_00119_b200.engine import Engine
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
+    monkeypatch.setenv("MICS_GRAPH", graph)
+    for p, k in ((4, 2), (8, 4)):
+        res = []
+        for merge, cap in (("0", 0), ("1", 0), ("1", 5)):
+            monkeypatch.setenv("MICS_HIER_MERGE", merge)
+            eng = Engine(n_ranks=8, device=0, arena_bytes=256 << 20)
+            eng.set_parallelism(0, cap)
+            wl = Workload("hm", [70_000, 12_345, 40_000, 9_999, 33_333, 4_096], p=p, s=2, grad_dtype="bf16", hier_k=k)
+            step = MicsStep(eng, wl, StepOptions(seed=29))
+            step.run(3)
+            eng.synchronize()
+            b, (info, segs) = step.buffers(), step.sync_info()
+            half, slots = step.stats().gather_slot_bytes, step.stats().gather_slots
+            res.append([(u32(eng.d2h(b["master"], r, info.shard_elems)),) +
+                        tuple(eng.d2h(b["gathered"], r, p * segs[l][1], "bf16", off=(l % slots) * half)
+                              for l in range(3)) for r in range(8)])
+            step.close()
+            eng.close()
+        for other in res[1:]:
+            for r in range(8):
+                for a, c in zip(res[0][r], other[r]):
+                    assert np.array_equal(a, c), (p, k, r)
 
 
 def test_step_two_steps_deterministic(oracle):
