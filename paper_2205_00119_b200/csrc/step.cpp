@@ -793,8 +793,8 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
     const char* hme = std::getenv("MICS_HIER_MERGE");  // 0: one k_hier launch per visit (A/B runs)
     const bool hmerge = hier && !cfg->compute && !(hme && hme[0] == '0');
     st->gather_slots = cfg->compute ? 2 : hmerge ? 4 : 3;
-    if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)
-      st->gather_slots = std::max(2, std::min(kMaxGatherSlots, std::atoi(e)));
+    if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)  // flat chain only
+      st->gather_slots = std::max(hmerge ? 4 : 2, std::min(kMaxGatherSlots, std::atoi(e)));
     st->gathered = alloc_sym(ctx, uint64_t(st->gather_slots) * st->gathered_half);
     // gradient slots: s resident sets, 1 regenerated per micro-step, or with compute 2
     // (the GEMMs of micro-step t+1 write one while the reduce-scatter of t reads the other)
