@@ -323,10 +323,17 @@ void enqueue(mics_ctx* ctx, const Launch& l, int dep_first, cudaStream_t stream)
     case Launch::BARRIER:
       launch_barrier(st, bar);
       break;
-    case Launch::HIER:
-      launch_hier(st, static_cast<const HierSeg*>(l.d_desc), l.ndesc, l.ntiles, l.grid, ctx->d_hctl + l.hier_chan,
-                  l.hier_sys, bar);
+    case Launch::HIER: {
+      HierArg ha;
+      ha.ctl = ctx->d_hctl + l.hier_chan;
+      ha.tab = ctx->d_tab + l.hier_chan;
+      ha.my_done = l.hier_merged ? reinterpret_cast<uint64_t*>(ctx->base + kDoneOffset) + l.hier_chan : nullptr;
+      ha.peer_mask = l.hier_peers;
+      ha.sys_scope = l.hier_sys;
+      ha.tile_flags = l.hier_merged ? 0 : 1;
+      launch_hier(st, static_cast<const HierSeg*>(l.d_desc), l.ndesc, l.ntiles, l.grid, ha, bar);
       break;
+    }
     case Launch::TAIL:
       launch_tail(st, l.in_t, l.tail_r, l.tail_p, static_cast<const TailJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid,
                   l.adam, l.dyn, l.mode, bar);

@@ -84,6 +84,15 @@ struct HierCtl {              // per barrier channel, device memory
   unsigned ticket;            // CTA arrivals of the running launch
   unsigned pad_;
 };
+struct PeerTab;
+struct HierArg {
+  HierCtl* ctl;
+  const PeerTab* tab;         // done counters of the peers (channel's table)
+  uint64_t* my_done;          // this process's done counter (merged launches), or null
+  uint64_t peer_mask;         // lag-1 stage-3 tiles wait until these processes' done >= epoch - 1
+  int sys_scope;              // flags / counters read across GPUs
+  int tile_flags;             // stage-1 tiles publish per-tile flags (lag-0 stage-3 readers)
+};
 
 struct RedJob {               // one output chunk (one destination rank, one segment)
   const uint8_t* const* srcs; // p source pointers, already offset to this chunk
@@ -150,7 +159,11 @@ struct TailJob {
 struct PeerTab {
   uint64_t* remote_flag[MICS_MAX_WORLD];
   uint64_t* local_flag[MICS_MAX_WORLD];
+  // process w's epoch of its last completed merged k_hier launch on this channel
+  // (arena head, kDoneOffset + 8 * channel); self included
+  uint64_t* done[MICS_MAX_WORLD];
 };
+constexpr uint64_t kDoneOffset = 2048;  // arena head: done counters, after the barrier flag slots
 
 struct BarrierArg {
   const PeerTab* tab;
@@ -182,9 +195,8 @@ struct BarrierArg {
 // --------------------------------------------------------------------------
 // kernel launchers (kernels.cu)
 void launch_copy(cudaStream_t s, const CopySeg* segs, int nseg, uint32_t ntiles, int grid, const BarrierArg& bar);
-// sys_scope: some stage-3 reader of a flag is on another GPU (system-scope publication)
-void launch_hier(cudaStream_t s, const HierSeg* segs, int nseg, uint32_t ntiles, int grid, HierCtl* ctl,
-                 int sys_scope, const BarrierArg& bar);
+void launch_hier(cudaStream_t s, const HierSeg* segs, int nseg, uint32_t ntiles, int grid, const HierArg& ha,
+                 const BarrierArg& bar);
 // `table_bytes`: size of the uploaded job table + source-pointer arrays (staged in smem when small)
 void launch_reduce(cudaStream_t s, mics_dtype in_t, mics_dtype acc_t, const RedJob* jobs, int njobs,
                    uint64_t table_bytes, uint32_t max_p, uint32_t ntiles, int grid, double scale, int mode,
@@ -380,6 +392,8 @@ struct Launch {
   enum Kind { COPY, REDUCE, ADAM, BARRIER, TAIL, HIER } kind = COPY;
   int tail_r = 0, tail_p = 0;  // TAIL: replicas and group size (mode = 1 zero-accumulate)
   int hier_sys = 0, hier_chan = 0;  // HIER: system-scope flags; channel of its epoch counter
+  uint64_t hier_peers = 0;          // HIER (merged): processes whose previous launch lag-1 tiles read
+  int hier_merged = 0;              // HIER: merged launch (done counter instead of per-tile flags)
   void* d_desc = nullptr;  // owned device table (cudaMalloc)
   uint64_t table_bytes = 0;
   uint32_t max_p = 1;

@@ -319,7 +319,7 @@ __device__ __forceinline__ void wait_flag(const uint64_t* f, uint64_t v, int sys
 // publish the flags resident CTAs are waiting for (profiles/r2/hier_pipe_README.md).
 // The grid is one resident wave.
 __global__ void __launch_bounds__(kThreads) k_hier(const HierSeg* __restrict__ gsegs, int nseg, uint32_t table_bytes,
-                                                   uint32_t ntiles, HierCtl* ctl, int sys_scope, BarrierArg bar) {
+                                                   uint32_t ntiles, HierArg ha, BarrierArg bar) {
   extern __shared__ __align__(16) unsigned char smem[];
   const bool staged = table_bytes != 0;
   if (staged) {
@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(kThreads) k_hier(const HierSeg* __restrict__ g
   const HierSeg* segs = staged ? reinterpret_cast<const HierSeg*>(smem) : gsegs;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   bar_entry(bar);
-  const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(&ctl->epoch) + 1;
+  const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(&ha.ctl->epoch) + 1;
+  bool peers_done = ha.peer_mask == 0;  // lag-1 sources: the node peers' previous launch completed
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     int idx = find_desc(segs, nseg, tile);
     uint32_t rel = tile - segs[idx].tile0;
@@ -344,21 +345,35 @@ __global__ void __launch_bounds__(kThreads) k_hier(const HierSeg* __restrict__ g
     const uint64_t off = uint64_t(rel) * kCopyTile;
     const uint64_t rem = s.bytes - off;
     const uint32_t nb = rem < kCopyTile ? uint32_t(rem) : kCopyTile;
-    if (s.stage == 3) {  // the node peer's stage-1 tile must be published first
-      if (threadIdx.x == 0) wait_flag(s.flags + rel, epoch - s.lag, sys_scope);
-      __syncthreads();
+    if (s.stage == 3) {
+      if (s.lag == 0) {  // the node peer's stage-1 tile of this launch must be published first
+        if (threadIdx.x == 0) wait_flag(s.flags + rel, epoch, ha.sys_scope);
+        __syncthreads();
+      } else if (!peers_done) {  // once per CTA: every node peer finished its previous launch
+        if (threadIdx.x == 0)
+          for (uint64_t m = ha.peer_mask; m; m &= m - 1)
+            wait_flag(ha.tab->done[__ffsll(static_cast<long long>(m)) - 1], epoch - 1, ha.sys_scope);
+        __syncthreads();
+        peers_done = true;
+      }
       copy_tile<true>(s.src + off, s.dst + off, nb);
     } else {
       copy_tile<false>(s.src + off, s.dst + off, nb);
-      __syncthreads();  // every thread's stores of the tile before the publication
-      if (threadIdx.x == 0) publish_flag(s.flags + rel, epoch, sys_scope);
+      if (ha.tile_flags) {
+        __syncthreads();  // every thread's stores of the tile before the publication
+        if (threadIdx.x == 0) publish_flag(s.flags + rel, epoch, ha.sys_scope);
+      }
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0 && atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1) {  // last CTA: the launch is done
-    ctl->ticket = 0;
-    ctl->epoch = epoch;
-    fence_gpu();
+  if (threadIdx.x == 0) {
+    fence_gpu();  // this CTA's stores before its ticket
+    if (atomicAdd(&ha.ctl->ticket, 1u) == gridDim.x - 1) {  // last CTA: the launch is done
+      ha.ctl->ticket = 0;
+      ha.ctl->epoch = epoch;
+      if (ha.my_done) publish_flag(ha.my_done, epoch, ha.sys_scope);  // every CTA's stores, via the tickets
+      else fence_gpu();
+    }
   }
   bar_exit(bar);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -963,10 +978,10 @@ void launch_copy(cudaStream_t s, const CopySeg* segs, int nseg, uint32_t ntiles,
   launch_ex(k_copy, grid, kThreads, tb, s, segs, nseg, tb, ntiles, bar);
 }
 
-void launch_hier(cudaStream_t s, const HierSeg* segs, int nseg, uint32_t ntiles, int grid, HierCtl* ctl,
-                 int sys_scope, const BarrierArg& bar) {
+void launch_hier(cudaStream_t s, const HierSeg* segs, int nseg, uint32_t ntiles, int grid, const HierArg& ha,
+                 const BarrierArg& bar) {
   const uint32_t tb = uint64_t(nseg) * sizeof(HierSeg) <= uint64_t(kSmemTable) ? uint32_t(nseg * sizeof(HierSeg)) : 0u;
-  launch_ex(k_hier, grid, kThreads, tb, s, segs, nseg, tb, ntiles, ctl, sys_scope, bar);
+  launch_ex(k_hier, grid, kThreads, tb, s, segs, nseg, tb, ntiles, ha, bar);
 }
 
 uint32_t reduce_tile_elems(mics_dtype in_t) {

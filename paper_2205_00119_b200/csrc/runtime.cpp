@@ -158,8 +158,15 @@ mics_ctx* create_ctx(const mics_init_args* a) {
     c->peer_base[c->wrank] = c->base;
     constexpr int K = mics_ctx::kChannels;
     static_assert(K * MICS_MAX_WORLD * sizeof(uint64_t) <= kFlagsBytes, "flag slots of every channel fit");
+    static_assert(kDoneOffset >= K * MICS_MAX_WORLD * sizeof(uint64_t) && kDoneOffset + 8 * K <= kFlagsBytes,
+                  "done counters after the flag slots, inside the arena head");
     MICS_CUDA(cudaMalloc(&c->d_tab, K * sizeof(PeerTab)));
-    MICS_CUDA(cudaMemset(c->d_tab, 0, K * sizeof(PeerTab)));
+    {
+      PeerTab tab[K];
+      std::memset(tab, 0, sizeof(tab));
+      for (int ch = 0; ch < K; ++ch) tab[ch].done[c->wrank] = reinterpret_cast<uint64_t*>(c->base + kDoneOffset) + ch;
+      MICS_CUDA(cudaMemcpy(c->d_tab, tab, sizeof(tab), cudaMemcpyHostToDevice));
+    }
     MICS_CUDA(cudaMalloc(&c->d_nbar, K * sizeof(uint64_t) * MICS_MAX_WORLD));
     MICS_CUDA(cudaMemset(c->d_nbar, 0, K * sizeof(uint64_t) * MICS_MAX_WORLD));
     MICS_CUDA(cudaMalloc(&c->d_tickets, K * 2 * sizeof(unsigned)));
@@ -216,6 +223,7 @@ void connect_peers(mics_ctx* c) {
       // channel ch, slot w on our arena is written by process w; slot wrank on process w's arena is ours
       tab[ch].local_flag[w] = reinterpret_cast<uint64_t*>(c->base) + ch * MICS_MAX_WORLD + w;
       tab[ch].remote_flag[w] = reinterpret_cast<uint64_t*>(c->peer_base[w]) + ch * MICS_MAX_WORLD + c->wrank;
+      tab[ch].done[w] = reinterpret_cast<uint64_t*>(c->peer_base[w] + kDoneOffset) + ch;
     }
   MICS_CUDA(cudaMemcpy(c->d_tab, tab, sizeof(tab), cudaMemcpyHostToDevice));
   c->ipc_ready = c->world > 1;

@@ -114,12 +114,13 @@ std::vector<Launch> build_layer_ag(mics_step* st, int l, int chan) {
 // Hierarchical gathers of one micro-step in the comm-only step: 2L+1 k_hier launches for
 // the V = 2L layer visits (forward 0..L-1, backward L-1..0); launch x runs stage 1 of
 // visit x and stage 3 of visit x-1, so each visit's NVLink-bound stage 1 overlaps the
-// previous visit's stage 3, with no barrier: stage 3 waits for the node peers' flags of
-// the previous launch.  Launches are serial on a GPU, and a rank's launch x completes
-// only after every node peer's launch x started (its lag-1 flags), i.e. after the
-// peer's launch x-1 — which read the slot launch x-3 wrote; with four gather slots two
-// visits of one slot are at least four launches apart, so no slot is rewritten while a
-// peer may read it (and the turn's repeated layer rewrites identical bytes).
+// previous visit's stage 3, with no barrier.  Launches are serial on each GPU; before
+// its first stage-3 tile a CTA waits until every process hosting a node peer has
+// completed launch x-1 (its done counter, published by that launch's last CTA) — the
+// only cross-GPU wait, one-sided and one launch back.  Write-after-read: a rank's launch
+// x starts after its launch x-1, which waited for the peers' launch x-2, so every
+// peer read of a slot that launch x rewrites (visits x-3 and earlier, read in launches
+// x-2 and earlier) is done; the turn's repeated layer rewrites identical bytes.
 void build_hier_merged(mics_step* st) {
   mics_ctx* ctx = st->ctx;
   mics_sync* sy = st->sync;
@@ -137,12 +138,23 @@ void build_hier_merged(mics_step* st) {
         [&](int r) { return reinterpret_cast<uint64_t*>(ctx->rank_ptr(st->hflags, r)); }, st->hflag_tiles, which,
         which == 2 ? 1 : 0);
   };
+  // processes hosting a node peer of a local rank (self excluded: its launch x-1 is done)
+  uint64_t peers = 0;
+  for (int r = 0; r < n; ++r) {
+    if (!ctx->local(r)) continue;
+    const int base = r / p * p, m = (r - base) / k;
+    for (int j2 = 0; j2 < k; ++j2)
+      if (ctx->process_of(base + m * k + j2) != ctx->wrank) peers |= 1ull << ctx->process_of(base + m * k + j2);
+  }
   const int V = int(visits.size());
   for (int x = 0; x <= V; ++x) {
     HierPlan plan;
     if (x < V) plan = stage(x, 1);
     if (x > 0) plan = concat_hier(plan, stage(x - 1, 2));
-    st->agm.push_back(make_hier_launch(ctx, plan, ctx->barrier(0, 0, 0), 0, true));
+    Launch l = make_hier_launch(ctx, plan, ctx->barrier(0, 0, 0), 0, true);
+    l.hier_merged = 1;
+    l.hier_peers = ctx->ipc_ready ? peers : 0;
+    st->agm.push_back(l);
   }
 }
 
@@ -788,13 +800,12 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
     st->v = alloc_sym(ctx, S * 4);
     // Without compute nothing consumes a gather, so up to three run concurrently
     // (enqueue_gathers): three slots.  With compute a layer's GEMMs release its slot.
-    // The merged hierarchical sequence of the comm-only step keeps four (build_hier_merged).
     const bool hier = cfg->hier_k > 0 && cfg->p > cfg->hier_k;
     const char* hme = std::getenv("MICS_HIER_MERGE");  // 0: one k_hier launch per visit (A/B runs)
     const bool hmerge = hier && !cfg->compute && !(hme && hme[0] == '0');
-    st->gather_slots = cfg->compute ? 2 : hmerge ? 4 : 3;
-    if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)  // flat chain only
-      st->gather_slots = std::max(hmerge ? 4 : 2, std::min(kMaxGatherSlots, std::atoi(e)));
+    st->gather_slots = cfg->compute ? 2 : 3;
+    if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)
+      st->gather_slots = std::max(3, std::min(kMaxGatherSlots, std::atoi(e)));
     st->gathered = alloc_sym(ctx, uint64_t(st->gather_slots) * st->gathered_half);
     // gradient slots: s resident sets, 1 regenerated per micro-step, or with compute 2
     // (the GEMMs of micro-step t+1 write one while the reduce-scatter of t reads the other)

@@ -112,9 +112,9 @@ def test_step_matches_cpu_restatement(oracle, alternative, grad_dtype, hier_k, p
 @pytest.mark.parametrize("graph", ["1", "0"])
 def test_hier_merged_matches_per_visit(monkeypatch, graph):
     """The comm-only step's merged hierarchical launches (launch x = stage 1 of visit x +
-    stage 3 of visit x-1, flags instead of barriers, four gather slots) vs one k_hier
-    launch per visit (MICS_HIER_MERGE=0): same parameters and gathered layers over three
-    steps, at p=4/k=2 and p=8/k=4, with the default grid and a 5-CTA cap."""
+    stage 3 of visit x-1, done counters instead of barriers) vs one k_hier launch per
+    visit (MICS_HIER_MERGE=0): same parameters and gathered layers over three steps, at
+    p=4/k=2 and p=8/k=4, with the default grid and a 5-CTA cap."""
     from paper_2205_00119_b200.engine import Engine
     from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
     monkeypatch.setenv("MICS_GRAPH", graph)
