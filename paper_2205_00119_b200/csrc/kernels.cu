@@ -318,7 +318,7 @@ __device__ __forceinline__ void wait_flag(const uint64_t* f, uint64_t v, int sys
 // successor's CTAs could hold SM slots a not-yet-resident CTA of this grid needs to
 // publish the flags resident CTAs are waiting for (profiles/r2/hier_pipe_README.md).
 // The grid is one resident wave.
-__global__ void __launch_bounds__(kThreads) k_hier(const HierSeg* __restrict__ gsegs, int nseg, uint32_t table_bytes,
+__global__ void __launch_bounds__(kThreads, 3) k_hier(const HierSeg* __restrict__ gsegs, int nseg, uint32_t table_bytes,
                                                    uint32_t ntiles, HierArg ha, BarrierArg bar) {
   extern __shared__ __align__(16) unsigned char smem[];
   const bool staged = table_bytes != 0;
