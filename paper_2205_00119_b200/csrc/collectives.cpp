@@ -331,6 +331,7 @@ void enqueue(mics_ctx* ctx, const Launch& l, int dep_first, cudaStream_t stream)
       ha.peer_mask = l.hier_peers;
       ha.sys_scope = l.hier_sys;
       ha.tile_flags = l.hier_merged ? 0 : 1;
+      ha.interleave_n1 = l.hier_merged ? l.hier_n1 : 0;
       launch_hier(st, static_cast<const HierSeg*>(l.d_desc), l.ndesc, l.ntiles, l.grid, ha, bar);
       break;
     }

@@ -92,6 +92,10 @@ struct HierArg {
   uint64_t peer_mask;         // lag-1 stage-3 tiles wait until these processes' done >= epoch - 1
   int sys_scope;              // flags / counters read across GPUs
   int tile_flags;             // stage-1 tiles publish per-tile flags (lag-0 stage-3 readers)
+  // merged launches: tiles [0, n1) (stage 1) and [n1, ntiles) (stage 3 of the previous
+  // visit) are taken alternately, so NVLink pulls and HBM copies run side by side all
+  // through the launch (0 = in order: lag-0 stage-3 tiles must follow every stage-1 tile)
+  uint32_t interleave_n1;
 };
 
 struct RedJob {               // one output chunk (one destination rank, one segment)
@@ -394,6 +398,7 @@ struct Launch {
   int hier_sys = 0, hier_chan = 0;  // HIER: system-scope flags; channel of its epoch counter
   uint64_t hier_peers = 0;          // HIER (merged): processes whose previous launch lag-1 tiles read
   int hier_merged = 0;              // HIER: merged launch (done counter instead of per-tile flags)
+  uint32_t hier_n1 = 0;             // HIER (merged): stage-1 tiles, interleaved with the stage-3 tiles
   void* d_desc = nullptr;  // owned device table (cudaMalloc)
   uint64_t table_bytes = 0;
   uint32_t max_p = 1;

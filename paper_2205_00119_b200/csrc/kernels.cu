@@ -333,7 +333,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_hier(const HierSeg* __restrict_
   bar_entry(bar);
   const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(&ha.ctl->epoch) + 1;
   bool peers_done = ha.peer_mask == 0;  // lag-1 sources: the node peers' previous launch completed
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const uint32_t n1 = ha.interleave_n1, n3 = ntiles - n1, mix = n1 < n3 ? n1 : n3;
+  for (uint32_t i = blockIdx.x; i < ntiles; i += gridDim.x) {
+    uint32_t tile = i;
+    if (n1) {  // alternate the two ranges, then the rest of the longer one
+      if (i < 2 * mix) tile = (i & 1) ? n1 + (i >> 1) : (i >> 1);
+      else tile = n1 > n3 ? i - mix : n1 + i - 2 * mix + mix;
+    }
     int idx = find_desc(segs, nseg, tile);
     uint32_t rel = tile - segs[idx].tile0;
     const uint32_t k = segs[idx].gsize;

@@ -150,9 +150,11 @@ void build_hier_merged(mics_step* st) {
   for (int x = 0; x <= V; ++x) {
     HierPlan plan;
     if (x < V) plan = stage(x, 1);
+    const uint32_t n1 = plan.tiles;
     if (x > 0) plan = concat_hier(plan, stage(x - 1, 2));
     Launch l = make_hier_launch(ctx, plan, ctx->barrier(0, 0, 0), 0, true);
     l.hier_merged = 1;
+    l.hier_n1 = n1 < plan.tiles ? n1 : 0;  // both ranges present: interleave them
     l.hier_peers = ctx->ipc_ready ? peers : 0;
     st->agm.push_back(l);
   }
