@@ -150,7 +150,9 @@ def arena_bytes(wl, per, resident, n=N_RANKS, alternative=False, compute=None):
     r = n // p
     sub = ((S + r - 1) // r + 3) // 4 * 4
     szg = 2 if wl.grad_dtype == "bf16" else 4
-    slots_ag = 2 if compute else max(3, min(8, int(os.environ.get("MICS_GATHER_SLOTS", "3"))))  # csrc/step.cpp
+    hmerge = wl.hier_k and p > wl.hier_k and os.environ.get("MICS_HIER_MERGE") != "0"  # merged hierarchical launches
+    slots_ag = (2 if compute else 3 * int(os.environ.get("MICS_HIER_VISITS", "2")) if hmerge
+                else max(3, min(8, int(os.environ.get("MICS_GATHER_SLOTS", "3")))))  # csrc/step.cpp
     gathered = slots_ag * (((max(chunks) * p * 2) + 255) // 256 * 256)
     slots = min(2, s) if compute else (s if resident else 1)
     per_rank = r * sub * 4 + S * 2 + 3 * S * 4 + gathered + slots * p * S * szg

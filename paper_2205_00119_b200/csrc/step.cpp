@@ -146,12 +146,20 @@ void build_hier_merged(mics_step* st) {
     for (int j2 = 0; j2 < k; ++j2)
       if (ctx->process_of(base + m * k + j2) != ctx->wrank) peers |= 1ull << ctx->process_of(base + m * k + j2);
   }
-  const int V = int(visits.size());
-  for (int x = 0; x <= V; ++x) {
+  // G visits per launch (st->hier_group): launch y runs stage 1 of visits [yG, yG+G) and
+  // stage 3 of visits [(y-1)G, yG); the slots (3G) keep the write-after-read argument
+  // (a slot is rewritten at least three launches after the launch that wrote it)
+  const int V = int(visits.size()), G = st->hier_group, Y = (V + G - 1) / G;
+  auto group = [&](int y, int which) {
+    HierPlan g;
+    for (int v = y * G; v < std::min(V, (y + 1) * G); ++v) g = concat_hier(g, stage(v, which));
+    return g;
+  };
+  for (int x = 0; x <= Y; ++x) {
     HierPlan plan;
-    if (x < V) plan = stage(x, 1);
+    if (x < Y) plan = group(x, 1);
     const uint32_t n1 = plan.tiles;
-    if (x > 0) plan = concat_hier(plan, stage(x - 1, 2));
+    if (x > 0) plan = concat_hier(plan, group(x - 1, 2));
     Launch l = make_hier_launch(ctx, plan, ctx->barrier(0, 0, 0), 0, true);
     l.hier_merged = 1;
     l.hier_n1 = n1 < plan.tiles ? n1 : 0;  // both ranges present: interleave them
@@ -805,8 +813,11 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
     const bool hier = cfg->hier_k > 0 && cfg->p > cfg->hier_k;
     const char* hme = std::getenv("MICS_HIER_MERGE");  // 0: one k_hier launch per visit (A/B runs)
     const bool hmerge = hier && !cfg->compute && !(hme && hme[0] == '0');
-    st->gather_slots = cfg->compute ? 2 : 3;
-    if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute)
+    // merged hierarchical launches take hier_group layer visits each (MICS_HIER_VISITS)
+    st->hier_group = 2;
+    if (const char* e = std::getenv("MICS_HIER_VISITS")) st->hier_group = std::max(1, std::min(2, std::atoi(e)));
+    st->gather_slots = cfg->compute ? 2 : hmerge ? 3 * st->hier_group : 3;
+    if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute && !hmerge)
       st->gather_slots = std::max(3, std::min(kMaxGatherSlots, std::atoi(e)));
     st->gathered = alloc_sym(ctx, uint64_t(st->gather_slots) * st->gathered_half);
     // gradient slots: s resident sets, 1 regenerated per micro-step, or with compute 2
