@@ -815,7 +815,7 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
     const bool hmerge = hier && !cfg->compute && !(hme && hme[0] == '0');
     // merged hierarchical launches take hier_group layer visits each (MICS_HIER_VISITS)
     st->hier_group = 2;
-    if (const char* e = std::getenv("MICS_HIER_VISITS")) st->hier_group = std::max(1, std::min(2, std::atoi(e)));
+    if (const char* e = std::getenv("MICS_HIER_VISITS")) st->hier_group = std::max(1, std::min(4, std::atoi(e)));
     st->gather_slots = cfg->compute ? 2 : hmerge ? 3 * st->hier_group : 3;
     if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute && !hmerge)
       st->gather_slots = std::max(3, std::min(kMaxGatherSlots, std::atoi(e)));

@@ -53,7 +53,7 @@ void alt_boundary(mics_sync* st);
 }  // namespace mics
 
 // MiCS step driver state (step.cpp)
-constexpr int kMaxGatherSlots = 8;  // mics_step::gather_slots upper bound (MICS_GATHER_SLOTS)
+constexpr int kMaxGatherSlots = 12;  // mics_step::gather_slots upper bound (3 x merged hierarchical visits)
 
 namespace mics {
 struct ProfileRec {  // one profiled step in flight (step_profile_begin / step_profile_end)
