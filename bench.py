@@ -151,7 +151,7 @@ def arena_bytes(wl, per, resident, n=N_RANKS, alternative=False, compute=None):
     sub = ((S + r - 1) // r + 3) // 4 * 4
     szg = 2 if wl.grad_dtype == "bf16" else 4
     hmerge = wl.hier_k and p > wl.hier_k and os.environ.get("MICS_HIER_MERGE") != "0"  # merged hierarchical launches
-    slots_ag = (2 if compute else 3 * int(os.environ.get("MICS_HIER_VISITS", "2")) if hmerge
+    slots_ag = (2 if compute else 3 * int(os.environ.get("MICS_HIER_VISITS", "3")) if hmerge
                 else max(3, min(8, int(os.environ.get("MICS_GATHER_SLOTS", "3")))))  # csrc/step.cpp
     gathered = slots_ag * (((max(chunks) * p * 2) + 255) // 256 * 256)
     slots = min(2, s) if compute else (s if resident else 1)

@@ -813,8 +813,10 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
     const bool hier = cfg->hier_k > 0 && cfg->p > cfg->hier_k;
     const char* hme = std::getenv("MICS_HIER_MERGE");  // 0: one k_hier launch per visit (A/B runs)
     const bool hmerge = hier && !cfg->compute && !(hme && hme[0] == '0');
-    // merged hierarchical launches take hier_group layer visits each (MICS_HIER_VISITS)
-    st->hier_group = 2;
+    // merged hierarchical launches take hier_group layer visits each (MICS_HIER_VISITS);
+    // C4 all-gather phase on 4 B200 (n=8 / n=4 ranks), G = 1..4: 26.7/39.0, 25.9/35.5,
+    // 25.5/34.7, 26.6/33.9 ms (profiles/r2/logs/R2q_*)
+    st->hier_group = 3;
     if (const char* e = std::getenv("MICS_HIER_VISITS")) st->hier_group = std::max(1, std::min(4, std::atoi(e)));
     st->gather_slots = cfg->compute ? 2 : hmerge ? 3 * st->hier_group : 3;
     if (const char* e = std::getenv("MICS_GATHER_SLOTS"); e && !cfg->compute && !hmerge)

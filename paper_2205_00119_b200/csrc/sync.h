@@ -78,7 +78,7 @@ struct mics_step {
   std::vector<std::vector<mics::Launch>> ag;  // per layer: 1 launch (k_copy flat or k_hier)
   // merged hierarchical gathers of one micro-step (comm-only step): 2L/G+1 k_hier launches
   std::vector<mics::Launch> agm;
-  int hier_group = 2;  // G: layer visits per merged launch
+  int hier_group = 3;  // G: layer visits per merged launch
   // hierarchical gathers (k_hier): per rank [q][hflag_tiles] u64 stage-1 tile flags
   mics_buf hflags{};
   uint64_t hflag_tiles = 0;

@@ -101,9 +101,9 @@ def test_step_matches_cpu_restatement(oracle, alternative, grad_dtype, hier_k, p
             for i in range(p):
                 want_bf = oracle.f32_to_bf16(init[g * p + i][sol:sol + cl])
                 assert np.array_equal(got[i * cl:(i + 1) * cl], want_bf), (l, r, i)
-    # flat: one k_copy launch per layer visit; hierarchical: L+1 merged k_hier launches per
-    # micro-step (launch y = stage 1 of visits 2y, 2y+1 + stage 3 of visits 2y-2, 2y-1)
-    want_ag = s * (len(layers) + 1) if hier_k and p > hier_k else 2 * s * len(layers)
+    # flat: one k_copy launch per layer visit; hierarchical: ceil(2L/3)+1 merged k_hier
+    # launches per micro-step (launch y = stage 1 of 3 visits + stage 3 of the 3 before)
+    want_ag = s * (-(-2 * len(layers) // 3) + 1) if hier_k and p > hier_k else 2 * s * len(layers)
     assert stats.launches > 0 and stats.ag_launches == want_ag
     step.close()
     eng.close()
@@ -112,7 +112,7 @@ def test_step_matches_cpu_restatement(oracle, alternative, grad_dtype, hier_k, p
 @pytest.mark.parametrize("graph", ["1", "0"])
 def test_hier_merged_matches_per_visit(monkeypatch, graph):
     """The comm-only step's merged hierarchical launches (launch y = stage 1 of G visits +
-    stage 3 of the previous G, done counters instead of barriers; G = 2 and 1) vs one
+    stage 3 of the previous G, done counters instead of barriers; G = 3, 1, 4) vs one
     k_hier launch per visit (MICS_HIER_MERGE=0): same parameters and gathered layers
     over three steps, at p=4/k=2 and p=8/k=4, with the default grid and a 5-CTA cap."""
     from paper_2205_00119_b200.engine import Engine
@@ -120,7 +120,7 @@ def test_hier_merged_matches_per_visit(monkeypatch, graph):
     monkeypatch.setenv("MICS_GRAPH", graph)
     for p, k in ((4, 2), (8, 4)):
         res = []
-        for merge, visits, cap in (("0", "2", 0), ("1", "2", 0), ("1", "1", 0), ("1", "2", 5)):
+        for merge, visits, cap in (("0", "3", 0), ("1", "3", 0), ("1", "1", 0), ("1", "4", 0), ("1", "3", 5)):
             monkeypatch.setenv("MICS_HIER_MERGE", merge)
             monkeypatch.setenv("MICS_HIER_VISITS", visits)
             eng = Engine(n_ranks=8, device=0, arena_bytes=256 << 20)
