@@ -1,10 +1,15 @@
 """K3 (`k_hier`) NVLink evidence in ONE process (ncu profiles one process): a
-multi-device context (mics_init_devices) over GPUs 0 and 1 with n=4 virtual ranks,
-p=4, k=2 — node peers share a GPU, the stage-1 channel pulls cross NVLink, exactly the
-C4 n=8 / 4-GPU placement.  Chunk = one GPT-2 1.5B block's bf16 chunk at p=4.
-Prints CUDA-event GB/s (stage-1 NVLink bytes and total bytes per launch).
+multi-device context (mics_init_devices) over GPUs 0 and 1.
 
-    python tools/ncu_hier.py [chunk_bytes] [reps]
+  python tools/ncu_hier.py api  [chunk] [reps]   one hierarchical_all_gather per call (per-visit
+                                                 k_hier, entry/exit barrier), n=4, p=4, k=2
+  python tools/ncu_hier.py step [layers] [steps] the comm-only MiCS step on GPT-2 1.5B layers
+                                                 (C4 shapes), n=4 ranks, p=4, k=2: merged k_hier
+                                                 launches (stage 1 of 3 visits + stage 3 of the
+                                                 previous 3, done counters)
+
+Both place node peers on one GPU and the stage-1 channel across NVLink, exactly the C4
+n=8 / 4-GPU placement.  Prints CUDA-event times and the NVLink bytes per launch.
 """
 import json
 import os
@@ -17,10 +22,36 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     import torch
 
-    from paper_2205_00119_b200.collectives import hierarchical_all_gather_device
     from paper_2205_00119_b200.engine import Engine
-    chunk = int(sys.argv[1]) if len(sys.argv) > 1 else 30_740_800 // 4 * 2
-    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+    mode = sys.argv[1] if len(sys.argv) > 1 else "api"
+    torch.cuda.set_device(0)
+    if mode == "step":
+        import bench
+        from paper_2205_00119_b200.step import MicsStep, StepOptions
+        from paper_2205_00119_b200.workloads import Workload, workloads
+        layers = int(sys.argv[2]) if len(sys.argv) > 2 else 13
+        steps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+        c4 = workloads()["C4"]
+        wl = Workload("C4 layers", c4.layer_params[:layers], p=4, s=1, grad_dtype="bf16", hier_k=2, n=4)
+        eng = Engine(n_ranks=4, arena_bytes=bench.arena_bytes(wl, 2, False, 4), devices=[0, 1])
+        step = MicsStep(eng, wl, StepOptions(resident_grads=False))
+        step.run(1)
+        eng.synchronize()
+        prof = step.profile()
+        st = step.stats()
+        t0 = time.perf_counter()
+        step.run(steps)
+        eng.synchronize()
+        print(json.dumps({"op": "step (merged k_hier)", "layers": layers, "ms_per_step": (time.perf_counter() - t0) * 1e3
+                          / steps, "allgather_ms": prof["allgather_ms"], "ag_launches": st.ag_launches,
+                          "ag_nvlink_bytes_per_gpu": st.ag_remote_bytes,
+                          "ag_nvlink_GBps": st.ag_remote_bytes / prof["allgather_ms"] / 1e6}), flush=True)
+        step.close()
+        eng.close()
+        return
+    from paper_2205_00119_b200.collectives import hierarchical_all_gather_device
+    chunk = int(sys.argv[2]) if len(sys.argv) > 2 else 30_740_800 // 4 * 2
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
     n, p, k = 4, 4, 2
     eng = Engine(n_ranks=n, arena_bytes=(p + 1) * chunk + (256 << 20), devices=[0, 1])
     src, out = eng.alloc(chunk), eng.alloc(p * chunk)
@@ -35,21 +66,17 @@ def main():
 
     run()
     eng.synchronize()
-    ext = torch.cuda.ExternalStream(eng.stream())
+    ext = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", 0))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0 = time.perf_counter()
     e0.record(ext)
     for _ in range(reps):
         run()
     e1.record(ext)
     eng.synchronize()
-    wall = (time.perf_counter() - t0) / reps
     ms = e0.elapsed_time(e1) / reps  # GPU 0's stream; the members meet at the launch's barriers
-    # per GPU per launch: 2 local ranks x (q-1) = 1 remote stage-1 chunk each over NVLink
-    nvl = 2 * (p // k - 1) * chunk
-    print(json.dumps({"op": "k_hier p=4 k=2, 2 ranks/GPU on 2 GPUs (one process)", "chunk_bytes": chunk,
-                      "ms": ms, "wall_ms": wall * 1e3, "nvlink_bytes_per_gpu": nvl,
-                      "nvlink_GBps": nvl / ms / 1e6, "gathered_bytes_per_rank": p * chunk}), flush=True)
+    nvl = 2 * (p // k - 1) * chunk   # per GPU per launch: 2 local ranks x (q-1) remote stage-1 chunks
+    print(json.dumps({"op": "k_hier p=4 k=2 (one launch per call), 2 ranks/GPU on 2 GPUs", "chunk_bytes": chunk,
+                      "ms": ms, "nvlink_bytes_per_gpu": nvl, "nvlink_GBps": nvl / ms / 1e6}), flush=True)
     eng.close()
 
 
