@@ -105,6 +105,7 @@ mics_status mics_init(const mics_init_args* args, mics_ctx** out);
  * host-buffer API and the sync / step drivers then span the GPUs. */
 mics_status mics_init_devices(const mics_init_args* args, const int* devices, int ndev, mics_ctx** out);
 mics_status mics_device_count(mics_ctx* ctx, int* ndev); /* GPUs of the context (1 unless mics_init_devices) */
+mics_status mics_device_stream(mics_ctx* ctx, int d, void** cuda_stream); /* member d's stream (timing) */
 mics_status mics_destroy(mics_ctx* ctx);
 /* CUDA IPC handle of this process's arena; gather all `world` handles (in world
  * order) with any out-of-band channel (torch.distributed) and import them. */

@@ -94,6 +94,7 @@ _SIGS = [
     ("mics_init", I, [C.POINTER(InitArgs), C.POINTER(VP)]),
     ("mics_init_devices", I, [C.POINTER(InitArgs), PI, I, C.POINTER(VP)]),
     ("mics_device_count", I, [VP, PI]),
+    ("mics_device_stream", I, [VP, I, C.POINTER(VP)]),
     ("mics_destroy", I, [VP]),
     ("mics_ipc_export", I, [VP, VP]),
     ("mics_ipc_import", I, [VP, VP]),

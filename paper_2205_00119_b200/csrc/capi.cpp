@@ -187,6 +187,15 @@ mics_status mics_init_devices(const mics_init_args* args, const int* devices, in
     *out = mics::create_group(args, devices, ndev);
   });
 }
+mics_status mics_device_stream(mics_ctx* ctx, int d, void** s) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(s, "output");
+    const auto m = mics::members(ctx);
+    if (d < 0 || d >= int(m.size())) mics::raise(MICS_OUT_OF_RANGE, "device index out of range");
+    *s = m[size_t(d)]->stream;
+  });
+}
 mics_status mics_device_count(mics_ctx* ctx, int* ndev) {
   return guard([&] {
     need(ctx, "ctx");

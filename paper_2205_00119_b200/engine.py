@@ -150,6 +150,12 @@ class Engine:
         check(lib.mics_stream(self.ctx, C.byref(s)))
         return s.value or 0
 
+    def device_stream(self, d: int) -> int:
+        """cudaStream_t of member d of a multi-device context (d = 0 otherwise)."""
+        out = C.c_void_p()
+        check(lib.mics_device_stream(self.ctx, d, C.byref(out)))
+        return out.value
+
     def synchronize(self) -> None:
         check(lib.mics_synchronize(self.ctx))
 
