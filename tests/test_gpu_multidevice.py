@@ -100,3 +100,27 @@ def test_step_on_two_gpus_equals_one_gpu(m, p, k, alt, gdt):
     for r in range(8):
         for a, c in zip(res[0][r], res[1][r]):
             assert np.array_equal(a, c), r
+
+
+def test_compute_step_on_two_gpus_equals_one_gpu(m):
+    """The step with its layer GEMMs (K7, three streams, copy-engine gathers) with the 8
+    ranks over two GPUs of one process: the same parameters and gradients as on one GPU
+    (every GEMM tile is computed the same way on either GPU)."""
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
+    h = 64
+    wl = Workload("cmp", [h * 40, h * 37, h * 56], p=2, s=2, hidden=h, micro_batch=8, seq_len=16)
+    res = []
+    for devices in (None, [0, 1]):
+        eng = m.Engine(n_ranks=8, device=0, arena_bytes=256 << 20, devices=devices)
+        step = MicsStep(eng, wl, StepOptions(seed=91, lr=1e-3, compute=True))
+        step.run(2)
+        eng.synchronize()
+        info = step.sync_info()[0]
+        b = step.buffers()
+        res.append([(u8(eng.d2h(b["master"], r, info.shard_elems)), u8(eng.d2h(b["grads"], r, info.grad_elems)))
+                    for r in range(8)])
+        step.close()
+        eng.close()
+    for r in range(8):
+        for a, c in zip(res[0][r], res[1][r]):
+            assert np.array_equal(a, c), r
