@@ -335,6 +335,15 @@ void enqueue(mics_ctx* ctx, const Launch& l, int dep_first, cudaStream_t stream)
       launch_hier(st, static_cast<const HierSeg*>(l.d_desc), l.ndesc, l.ntiles, l.grid, ha, bar);
       break;
     }
+    case Launch::FBND: {
+      const auto* rs = static_cast<const FbRsJob*>(l.d_desc);
+      const auto* ad = reinterpret_cast<const FbAdJob*>(
+          static_cast<const char*>(l.d_desc) + round_up(sizeof(FbRsJob) * uint64_t(l.fb_nrs), 16));
+      launch_fbnd(st, rs, l.fb_nrs, ad, l.ndesc - l.fb_nrs, l.fb_nblk, l.fb_blk, l.fb_lag, l.ntiles, l.grid, l.adam,
+                  l.dyn,
+                  l.fb_epoch, l.hier_sys, l.fb_ticket, l.fb_r, bar);
+      break;
+    }
     case Launch::TAIL:
       launch_tail(st, l.in_t, l.tail_r, l.tail_p, static_cast<const TailJob*>(l.d_desc), l.ndesc, l.ntiles, l.grid,
                   l.adam, l.dyn, l.mode, bar);

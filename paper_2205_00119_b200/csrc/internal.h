@@ -137,6 +137,8 @@ struct AdamScalars {
 // (bias correction changes every step).
 struct DevScalars {
   AdamScalars sc;
+  uint32_t pad_;
+  uint64_t epoch;  // the fused layer-group boundaries' flag value of this step (K9)
 };
 
 // Fused tail (K8, every rank on this GPU): the last micro-step's reduce-scatter, the
@@ -155,6 +157,39 @@ struct TailJob {
   uint16_t* bf[kTailMaxR];                        // nullable
   uint64_t elems, valid;                          // chunk elements (multiple of 8); valid gradient prefix
   uint32_t tile0, pad_;
+};
+
+// K9 (`k_fbnd`): the boundary of one layer group in ONE launch, in the overlapped tail of
+// multi-process jobs.  Reduce-scatter items: block k of a local rank's slice, `blk`
+// elements (fold over the r replicas in ascending order, stored in place), then published
+// by a flag pushed into every replica's flag array.  Adam items: block k of owner q's
+// slice of a local rank's range, after waiting for owner q's flag of block k.  Items run
+// in rounds: round t = the reduce-scatter items of block t, then the Adam items of block
+// t - lag (every owner), so NVLink pulls (the fold) and HBM traffic (Adam's state)
+// overlap all through the launch.  An Adam item waits only on reduce-scatter items of an
+// earlier round, which never wait, and items are taken in order from a ticket counter,
+// so every awaited flag is produced by a running CTA.
+uint32_t fb_block();                  // elements per published block (MICS_FB_BLOCK, default 64 Ki)
+struct FbRsJob {                      // one local rank's slice of the group
+  const float* src[kTailMaxR];        // replica q's shard at this slice
+  float* own;                         // this rank's shard at this slice (reduced in place)
+  uint64_t* flag[kTailMaxR];          // replica q's flag for this slice's block 0
+  uint64_t elems;
+  uint32_t r, pad_;
+};
+struct FbAdJob {                      // one local rank (+ an optional second replica of its position)
+  const float* owner[kTailMaxR];      // replica q's shard at the group start (q reduced slice q)
+  const uint64_t* flags;              // this rank's flags for the group: owner q, block k at q * fstride + k
+  float* prm;
+  float* m;
+  float* v;
+  uint16_t* bf;
+  float* prm2;                        // nullable: the second local replica
+  float* m2;
+  float* v2;
+  uint16_t* bf2;
+  uint64_t elems, sub;                // group elements; slice length (multiple of the block)
+  uint32_t r, nblk, pad_, fstride;    // nblk = sub / block; fstride: flags per owner (the largest group's nblk)
 };
 
 // Flag barrier between processes: remote_flag[w] is the slot on process w's
@@ -207,7 +242,8 @@ void launch_reduce(cudaStream_t s, mics_dtype in_t, mics_dtype acc_t, const RedJ
                    const BarrierArg& bar);
 uint32_t reduce_tile_elems(mics_dtype in_t);
 int reduce_class(uint32_t max_p);  // 2, 4, 8 or 9 (> 8 sources)
-int resident_ctas(int kind /* 0 copy, 1 reduce, 2 adam, 4 hier */, mics_dtype in_t, int pclass = 2);
+int resident_ctas(int kind /* 0 copy, 1 reduce, 2 adam, 4 hier, 5 fused boundary */, mics_dtype in_t,
+                  int pclass = 2);
 void launch_adam(cudaStream_t s, const AdamJob* jobs, int njobs, uint32_t ntiles, int grid, const AdamScalars& sc,
                  const DevScalars* dyn, const BarrierArg& bar);
 void launch_set_scalars(cudaStream_t s, DevScalars* dst, const DevScalars& v);
@@ -220,6 +256,9 @@ void launch_generate(cudaStream_t s, void* out, mics_dtype dtype, uint64_t seed,
                      uint64_t start, uint64_t count, int grid);
 void launch_cast_bf16(cudaStream_t s, const float* in, uint16_t* out, uint64_t count, int grid);
 void launch_barrier(cudaStream_t s, const BarrierArg& bar);
+void launch_fbnd(cudaStream_t s, const FbRsJob* rs, int nrs, const FbAdJob* ad, int nad, uint32_t nblk,
+                 uint32_t blk, uint32_t lag, uint32_t items, int grid, const AdamScalars& sc, const DevScalars* dyn,
+                 uint64_t epoch, int sys_scope, uint32_t* ticket, int r, const BarrierArg& bar);
 
 // K7 tcgen05 GEMM (gemm.cu): C[M,N] (+)= A[M,K]·B[K,N], bf16 operands K- or MN-major,
 // fp32 accumulation; planned once (TMA descriptors encoded), launched many times.
@@ -254,6 +293,7 @@ struct mics_ctx {
   int occ_copy = 2, occ_adam = 4, occ_reduce[4][4] = {};
   int occ_copy_indep = 1;  // CTAs/SM of barrier-free gathers chained with PDL
   int occ_hier = 2;        // CTAs/SM of the one-launch hierarchical all-gather (one resident wave)
+  int occ_fbnd = 2;        // CTAs/SM of the fused layer-group boundary (one resident wave)
   int bar_strict = 0;      // BarrierArg::strict (MICS_BAR_STRICT)
   int par_ctas_per_sm = 0; // mics_set_parallelism: CTAs per SM cap (0 = occupancy)
   int par_max_ctas = 0;    // mics_set_parallelism: CTAs per launch cap (0 = none)
@@ -393,12 +433,18 @@ struct AdamPlan {
 
 // A device-resident, replayable launch (built once, launched many times).
 struct Launch {
-  enum Kind { COPY, REDUCE, ADAM, BARRIER, TAIL, HIER } kind = COPY;
+  enum Kind { COPY, REDUCE, ADAM, BARRIER, TAIL, HIER, FBND } kind = COPY;
   int tail_r = 0, tail_p = 0;  // TAIL: replicas and group size (mode = 1 zero-accumulate)
   int hier_sys = 0, hier_chan = 0;  // HIER: system-scope flags; channel of its epoch counter
   uint64_t hier_peers = 0;          // HIER (merged): processes whose previous launch lag-1 tiles read
   int hier_merged = 0;              // HIER: merged launch (done counter instead of per-tile flags)
   uint32_t hier_n1 = 0;             // HIER (merged): stage-1 tiles, interleaved with the stage-3 tiles
+  int fb_nrs = 0;                   // FBND: reduce-scatter jobs (first in the table), then Adam jobs
+  uint32_t fb_nblk = 0;             // FBND: blocks per slice
+  uint32_t fb_blk = 0, fb_lag = 0;  // FBND: elements per block; rounds between a block's fold and its Adam
+  uint64_t fb_epoch = 0;            // FBND: flag value (eager launches; graph replays read DevScalars)
+  uint32_t* fb_ticket = nullptr;    // FBND: this GPU's item counter (zero between launches)
+  int fb_r = 2;                     // FBND: replicas per position (kernel instantiation)
   void* d_desc = nullptr;  // owned device table (cudaMalloc)
   uint64_t table_bytes = 0;
   uint32_t max_p = 1;

@@ -894,6 +894,181 @@ __global__ void __launch_bounds__(kThreads) k_cast_bf16(const float* in, uint16_
     out[i] = f32_to_bf16(in[i]);
 }
 
+// ---------------------------------------------------------------- K9: fused layer-group boundary
+__device__ __forceinline__ void adam4(const float4& g, float* prm, float* m, float* v, uint16_t* bf, uint64_t e,
+                                      const AdamScalars& sc) {
+  float4 p = *reinterpret_cast<const float4*>(prm + e);
+  float4 mm = *reinterpret_cast<const float4*>(m + e);
+  float4 vv = *reinterpret_cast<const float4*>(v + e);
+  adam_one(g.x, p.x, mm.x, vv.x, sc);
+  adam_one(g.y, p.y, mm.y, vv.y, sc);
+  adam_one(g.z, p.z, mm.z, vv.z, sc);
+  adam_one(g.w, p.w, mm.w, vv.w, sc);
+  *reinterpret_cast<float4*>(prm + e) = p;
+  *reinterpret_cast<float4*>(m + e) = mm;
+  *reinterpret_cast<float4*>(v + e) = vv;
+  if (bf) {
+    uint2 pk;
+    pk.x = uint32_t(f32_to_bf16(p.x)) | (uint32_t(f32_to_bf16(p.y)) << 16);
+    pk.y = uint32_t(f32_to_bf16(p.z)) | (uint32_t(f32_to_bf16(p.w)) << 16);
+    *reinterpret_cast<uint2*>(bf + e) = pk;
+  }
+}
+
+// kAdamUnroll float4 rows of one replica's state (row u at e + u * kThreads * 4), every
+// load issued before the first update, like k_adam's full tile
+__device__ __forceinline__ void adam_rows(const uint4 (&gr)[kAdamUnroll], float* prm, float* m, float* v,
+                                          uint16_t* bf, uint64_t e, const AdamScalars& sc) {
+  constexpr uint32_t stride = kThreads * 4;
+  float4 p[kAdamUnroll], mm[kAdamUnroll], vv[kAdamUnroll];
+#pragma unroll
+  for (int u = 0; u < kAdamUnroll; ++u) {
+    p[u] = *reinterpret_cast<const float4*>(prm + e + u * stride);
+    mm[u] = *reinterpret_cast<const float4*>(m + e + u * stride);
+    vv[u] = *reinterpret_cast<const float4*>(v + e + u * stride);
+  }
+#pragma unroll
+  for (int u = 0; u < kAdamUnroll; ++u) {
+    adam_one(__uint_as_float(gr[u].x), p[u].x, mm[u].x, vv[u].x, sc);
+    adam_one(__uint_as_float(gr[u].y), p[u].y, mm[u].y, vv[u].y, sc);
+    adam_one(__uint_as_float(gr[u].z), p[u].z, mm[u].z, vv[u].z, sc);
+    adam_one(__uint_as_float(gr[u].w), p[u].w, mm[u].w, vv[u].w, sc);
+    *reinterpret_cast<float4*>(prm + e + u * stride) = p[u];
+    *reinterpret_cast<float4*>(m + e + u * stride) = mm[u];
+    *reinterpret_cast<float4*>(v + e + u * stride) = vv[u];
+    if (bf) {
+      uint2 pk;
+      pk.x = uint32_t(f32_to_bf16(p[u].x)) | (uint32_t(f32_to_bf16(p[u].y)) << 16);
+      pk.y = uint32_t(f32_to_bf16(p[u].z)) | (uint32_t(f32_to_bf16(p[u].w)) << 16);
+      *reinterpret_cast<uint2*>(bf + e + u * stride) = pk;
+    }
+  }
+}
+
+// See FbRsJob / FbAdJob (internal.h).  PDL: waits for its predecessor at entry and lets
+// its successor launch only at exit (CTAs spin on flags: nothing may take their slots).
+// Items are handed out in order from a ticket counter, so every reduce-scatter item is
+// taken (by a running CTA, which never waits after the entry barrier) before any Adam
+// item is: an Adam CTA never waits on a block that no running CTA owns.  Each CTA takes
+// exactly one ticket past the end, so the launch consumes items + gridDim.x tickets and
+// the last of them resets the counter for the next launch.  RC = replica-count class
+// (2, 4, 8): the fold keeps 8 vectors per thread in flight (RC x U), like k_reduce.
+template <int RC>
+__global__ void __launch_bounds__(kThreads, 2) k_fbnd(const FbRsJob* __restrict__ rs, int nrs,
+                                                      const FbAdJob* __restrict__ ad, int nad, uint32_t r,
+                                                      uint32_t nblk, uint32_t blk, uint32_t lag, uint32_t items,
+                                                      AdamScalars sc,
+                                                      const DevScalars* __restrict__ dyn, uint64_t epoch,
+                                                      int sys_scope, uint32_t* ticket, BarrierArg bar) {
+  constexpr int U = 8 / RC;
+  constexpr uint32_t kRow = kThreads * 4;  // fp32 elements of one float4 row
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (dyn) {  // a replayed graph: this step's scalars and flag value
+    sc = dyn->sc;
+    epoch = dyn->epoch;
+  }
+  bar_entry(bar);
+  __shared__ uint32_t s_item;
+  // gridDim.x >= items: one item per CTA (CTAs retire, so the hardware can give freed
+  // slots to other streams' kernels); else persistent CTAs
+  const bool once = gridDim.x >= items;
+  const uint32_t last = once ? gridDim.x - 1 : items + gridDim.x - 1;
+  for (bool first = true;; first = false) {
+    if (once && !first) break;
+    __syncthreads();  // every thread read the previous item
+    if (threadIdx.x == 0) {
+      const uint32_t t = atomicAdd(ticket, 1u);
+      if (t == last) atomicExch(ticket, 0u);
+      s_item = t;
+    }
+    __syncthreads();
+    const uint32_t item = s_item;
+    if (item >= items) break;
+    const uint32_t per_round = uint32_t(nrs) + uint32_t(nad) * r;
+    const uint32_t round = item / per_round, w = item - round * per_round;
+    if (w < uint32_t(nrs)) {
+      const FbRsJob& J = rs[w];
+      const uint32_t b = round;
+      const uint64_t e0 = uint64_t(b) * blk;
+      if (e0 >= J.elems) continue;  // this slice has fewer blocks (or the lag rounds)
+      const uint64_t end = e0 + blk < J.elems ? e0 + blk : J.elems;
+      const uint8_t* const* srcs = reinterpret_cast<const uint8_t* const*>(J.src);
+      uint64_t e = e0;
+      // full groups of U rows: all r x U sources in flight, the fold in ascending replica order
+      for (; e + uint64_t(U) * kRow <= end; e += uint64_t(U) * kRow) {
+        float acc[U][4];
+        fold_vecs<float, float, RC, U>(srcs, J.r, e + threadIdx.x * 4, kRow, acc);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          *reinterpret_cast<float4*>(J.own + e + threadIdx.x * 4 + u * kRow) =
+              make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
+      }
+      for (uint64_t x = e + threadIdx.x; x < end; x += kThreads) {  // the group's ragged end
+        float a = J.src[0][x];
+        for (uint32_t q = 1; q < J.r; ++q) a = __fadd_rn(a, J.src[q][x]);
+        J.own[x] = a;
+      }
+      __syncthreads();  // the block's stores, then one flag into every replica's array
+      if (threadIdx.x == 0) {
+        if (sys_scope) fence_sys(); else fence_gpu();
+        for (uint32_t q = 0; q < J.r; ++q) {
+          if (sys_scope) st_relaxed_sys(J.flag[q] + b, epoch);
+          else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(J.flag[q] + b), "l"(epoch) : "memory");
+        }
+      }
+    } else {
+      if (round < lag || round - lag >= nblk) continue;
+      const uint32_t a = w - uint32_t(nrs), q = a % r, k = round - lag;  // owners interleaved
+      const FbAdJob& J = ad[a / r];
+      const uint64_t e0 = uint64_t(q) * J.sub + uint64_t(k) * blk;
+      const uint64_t send = (uint64_t(q) + 1) * J.sub < J.elems ? (uint64_t(q) + 1) * J.sub : J.elems;
+      if (e0 >= send) continue;  // past the end of owner q's slice
+      const uint64_t end = e0 + blk < send ? e0 + blk : send;
+      if (threadIdx.x == 0) wait_flag(J.flags + uint64_t(q) * J.fstride + k, epoch, sys_scope);
+      __syncthreads();
+      const float* g = J.owner[q];
+      uint64_t e = e0;
+      for (; e + uint64_t(kAdamUnroll) * kRow <= end; e += uint64_t(kAdamUnroll) * kRow) {
+        const uint64_t et = e + threadIdx.x * 4;
+        uint4 gr[kAdamUnroll];  // L2-coherent: written by the owner during this launch
+#pragma unroll
+        for (int u = 0; u < kAdamUnroll; ++u) gr[u] = ld_cg(g + et + u * kRow);
+        adam_rows(gr, J.prm, J.m, J.v, J.bf, et, sc);
+        if (J.prm2) adam_rows(gr, J.prm2, J.m2, J.v2, J.bf2, et, sc);
+      }
+      for (e += threadIdx.x * 4; e < end; e += kRow) {  // the slice's ragged end
+        if (e + 4 <= end) {
+          const uint4 r4 = ld_cg(g + e);
+          const float4 gv = make_float4(__uint_as_float(r4.x), __uint_as_float(r4.y), __uint_as_float(r4.z),
+                                        __uint_as_float(r4.w));
+          adam4(gv, J.prm, J.m, J.v, J.bf, e, sc);
+          if (J.prm2) adam4(gv, J.prm2, J.m2, J.v2, J.bf2, e, sc);
+        } else {
+          for (uint64_t x = e; x < end; ++x) {
+            const float gx = *reinterpret_cast<const volatile float*>(g + x);
+            float p = J.prm[x], mm = J.m[x], vv = J.v[x];
+            adam_one(gx, p, mm, vv, sc);
+            J.prm[x] = p;
+            J.m[x] = mm;
+            J.v[x] = vv;
+            if (J.bf) J.bf[x] = f32_to_bf16(p);
+            if (J.prm2) {
+              float p2 = J.prm2[x], m2 = J.m2[x], v2 = J.v2[x];
+              adam_one(gx, p2, m2, v2, sc);
+              J.prm2[x] = p2;
+              J.m2[x] = m2;
+              J.v2[x] = v2;
+              if (J.bf2) J.bf2[x] = f32_to_bf16(p2);
+            }
+          }
+        }
+      }
+    }
+  }
+  bar_exit(bar);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __global__ void k_set_scalars(DevScalars* dst, DevScalars v) { *dst = v; }
 
 __global__ void k_barrier(BarrierArg bar) {
@@ -966,6 +1141,14 @@ int resident_ctas(int kind, mics_dtype in_t, int pc) {
     case 4:
       MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_hier, kThreads, kSmemTable));
       break;
+    case 5: {
+      int n2 = 0, n4 = 0;
+      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fbnd<8>, kThreads, 0));
+      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n4, k_fbnd<4>, kThreads, 0));
+      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n2, k_fbnd<2>, kThreads, 0));
+      n = std::min(n, std::min(n2, n4));
+      break;
+    }
     case 1:
       if (in_t == MICS_BF16) n = reduce_occupancy<uint16_t, float>(pc);
       else if (in_t == MICS_F64) n = reduce_occupancy<double, double>(pc);
@@ -1058,6 +1241,14 @@ void launch_cast_bf16(cudaStream_t s, const float* in, uint16_t* out, uint64_t c
   if (count == 0) return;
   k_cast_bf16<<<grid, kThreads, 0, s>>>(in, out, count);
   MICS_CUDA(cudaGetLastError());
+}
+
+void launch_fbnd(cudaStream_t s, const FbRsJob* rs, int nrs, const FbAdJob* ad, int nad, uint32_t nblk,
+                 uint32_t blk, uint32_t lag, uint32_t items, int grid, const AdamScalars& sc, const DevScalars* dyn,
+                 uint64_t epoch, int sys_scope, uint32_t* ticket, int r, const BarrierArg& bar) {
+  auto kern = r <= 2 ? k_fbnd<2> : r <= 4 ? k_fbnd<4> : k_fbnd<8>;
+  launch_ex(kern, grid, kThreads, 0, s, rs, nrs, ad, nad, uint32_t(r), nblk, blk, lag, items, sc, dyn, epoch,
+            sys_scope, ticket, bar);
 }
 
 void launch_barrier(cudaStream_t s, const BarrierArg& bar) {

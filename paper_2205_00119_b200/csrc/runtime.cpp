@@ -144,6 +144,7 @@ mics_ctx* create_ctx(const mics_init_args* a) {
     // the one-launch hierarchical all-gather must be one resident wave (its stage-3
     // tiles wait for other CTAs' stage-1 tiles): at most its occupancy, 3 like the chain
     c->occ_hier = std::min(resident_ctas(4, MICS_F32), 3);
+    c->occ_fbnd = resident_ctas(5, MICS_F32);
     const int classes[4] = {2, 4, 8, 9};
     for (int t = 0; t < 4; ++t)
       for (int k = 0; k < 4; ++k) c->occ_reduce[t][k] = resident_ctas(1, mics_dtype(t), classes[k]);

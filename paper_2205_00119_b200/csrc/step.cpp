@@ -48,9 +48,11 @@ void release(mics_step* st) {
     b.rs.release();
     b.ag.release();
   }
+  for (auto& l : st->tail_fb) l.release();
   for (auto e : st->ev_tail) cudaEventDestroy(e);
   for (auto e : st->ev_tail_rs) cudaEventDestroy(e);
   if (st->tail_rs_stream) cudaStreamDestroy(st->tail_rs_stream);
+
   if (st->ev_tail_done) cudaEventDestroy(st->ev_tail_done);
   for (auto e : st->ev_h2d) cudaEventDestroy(e);
   for (auto e : st->ev_rs_slot) cudaEventDestroy(e);
@@ -236,9 +238,11 @@ void enqueue_tail(mics_step* st, std::vector<cudaEvent_t>* clk) {
   st->adam_step++;
   const AdamScalars sc = make_adam_scalars(st->cfg.lr, st->cfg.beta1, st->cfg.beta2, st->cfg.eps,
                                            st->cfg.weight_decay, st->adam_step, st->adam.grad_scale);
+  if (!st->tail_fb.empty()) ++st->fb_epoch;  // this step's flag value of the fused boundaries
   if (st->d_scalars && !st->capturing) {
     DevScalars v{};
     v.sc = sc;
+    v.epoch = st->fb_epoch;
     launch_set_scalars(M, st->d_scalars, v);
   }
   auto mark = [&]() {
@@ -253,6 +257,26 @@ void enqueue_tail(mics_step* st, std::vector<cudaEvent_t>* clk) {
   // so group g+1's boundary reduce-scatter runs under group g's Adam
   cudaStream_t R2 = serial ? M : st->tail_rs_stream;
   mark();
+  if (!st->tail_fb.empty()) {  // K9: each group's boundary is one launch on its own stream (channel 2)
+    for (size_t g = 0; g < st->tail_rs.size(); ++g) {
+      enqueue(ctx, st->tail_rs[g], -1, M);
+      mark();
+      if (!serial) {
+        MICS_CUDA(cudaEventRecord(st->ev_tail[g], M));
+        MICS_CUDA(cudaStreamWaitEvent(R2, st->ev_tail[g], 0));
+      }
+      Launch& f = st->tail_fb[g];
+      f.adam = sc;
+      f.fb_epoch = st->fb_epoch;
+      enqueue(ctx, f, -1, R2);
+      mark();
+    }
+    if (!serial) {
+      MICS_CUDA(cudaEventRecord(st->ev_tail_done, R2));
+      MICS_CUDA(cudaStreamWaitEvent(M, st->ev_tail_done, 0));
+    }
+    return;
+  }
   for (size_t g = 0; g < st->tail_rs.size(); ++g) {
     enqueue(ctx, st->tail_rs[g], -1, M);
     mark();
@@ -886,9 +910,17 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
       const bool auto_on = ctx->world > 1 && sy->n / sy->p > 1;
       st->tail = !st->compute && sy->n / sy->p > 1 && (te ? te[0] == '1' : auto_on);
       if (st->tail) {
-        // 8 groups when the last reduce-scatter stays inside a GPU (HBM): N=2 16.36 -> 16.00 ms,
-        // N=4 8.68 -> 8.50; 4 when it crosses GPUs too (one rank per GPU: 9.85 vs 10.39 ms at 8)
-        plan_layer_groups(st, ctx->per >= cfg->p ? 8 : 4);
+        // K9 (default; MICS_TAIL_FUSED=0: the two-kernel boundary): each group's boundary
+        // reduce-scatter and Adam in one launch, Adam blocks pulling a slice block as soon
+        // as its owner published it, on channel 2
+        const char* tfe = std::getenv("MICS_TAIL_FUSED");
+        const bool fused_bnd = !(tfe && tfe[0] == '0') && sy->n / sy->p <= kTailMaxR;
+        // two-kernel boundary: 8 groups when the last reduce-scatter stays inside a GPU
+        // (HBM): N=2 16.36 -> 16.00 ms, N=4 8.68 -> 8.50; 4 when it crosses GPUs too (one
+        // rank per GPU: 9.85 vs 10.39 ms at 8).  K9: 2 groups (fewer launch drains; C3
+        // N=2 15.03 / N=4 8.81 ms at 2 groups vs 15.09 / 8.82 at 8)
+        const char* tg = std::getenv("MICS_TAIL_GROUPS");  // experiments
+        plan_layer_groups(st, tg ? std::max(1, std::atoi(tg)) : fused_bnd ? 2 : ctx->per >= cfg->p ? 8 : 4);
         const int s_last = cfg->s - 1;
         const uint64_t goff = uint64_t(s_last % st->gslots) * sy->grad_elems * szg;
         for (size_t g = 0; g < st->group_range.size(); ++g) {
@@ -898,8 +930,23 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
                                                    s_last == 0 ? MICS_RS_ZERO_ACCUM : MICS_RS_ACCUMULATE, true, false,
                                                    1, 1, nullptr, l0, l1));
           // boundary reduce-scatter on channel 2 (its own stream), Adam on channel 1 (side stream)
-          st->tail_bnd.push_back(build_boundary_range(sy, &st->adam, sy->shard, st->group_range[g].first,
+          if (!fused_bnd)
+            st->tail_bnd.push_back(build_boundary_range(sy, &st->adam, sy->shard, st->group_range[g].first,
                                                       st->group_range[g].second, 1, 2));
+        }
+        if (fused_bnd) {
+          const int r = sy->n / sy->p;
+          uint32_t nblk_max = 1;
+          for (const auto& [lo, hi] : st->group_range)
+            nblk_max = std::max<uint32_t>(nblk_max, uint32_t(ceil_div(ceil_div(hi - lo, uint64_t(r)), fb_block())));
+          const int G = int(st->group_range.size());
+          st->fbflags = alloc_sym(ctx, (uint64_t(G) * uint64_t(r) * nblk_max + uint64_t(G)) * 8);
+          MICS_CUDA(cudaMemsetAsync(ctx->base + st->fbflags.offset, 0, st->fbflags.stride * uint64_t(ctx->per),
+                                    ctx->stream));
+          for (int g = 0; g < G; ++g)
+            st->tail_fb.push_back(build_boundary_fused_range(sy, &st->adam, st->group_range[size_t(g)].first,
+                                                             st->group_range[size_t(g)].second, st->fbflags, g,
+                                                             G, nblk_max, 2));
         }
         st->ev_tail.resize(st->group_range.size());
         for (auto& e : st->ev_tail) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -907,6 +954,7 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
         for (auto& e : st->ev_tail_rs) MICS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         MICS_CUDA(cudaStreamCreateWithFlags(&st->tail_rs_stream, cudaStreamNonBlocking));
         MICS_CUDA(cudaEventCreateWithFlags(&st->ev_tail_done, cudaEventDisableTiming));
+
       }
       const char* fe = std::getenv("MICS_FUSED_TAIL");
       if (!st->tail && !st->compute && ctx->world == 1 && !(fe && fe[0] == '0') &&
@@ -984,7 +1032,13 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
       S2.rs_hbm_bytes += x.hbm_bytes;
     }
     std::vector<const BoundaryLaunches*> bl;
-    if (st->tail)
+    if (st->tail && !st->tail_fb.empty()) {
+      for (const auto& x : st->tail_fb) {
+        S2.bnd_launches += runs(x);
+        S2.bnd_remote_bytes += x.remote_bytes;
+        S2.bnd_hbm_bytes += x.hbm_bytes;
+      }
+    } else if (st->tail)
       for (const auto& x : st->tail_bnd) bl.push_back(&x);
     else if (!st->fused_tail)
       bl.push_back(&st->bnd);
@@ -1047,8 +1101,10 @@ void build_graph(mics_step* st) {
   MICS_CUDA(cudaMalloc(&st->d_scalars, sizeof(DevScalars)));
   st->bnd.rs.dyn = st->bnd.ag.dyn = st->d_scalars;
   for (auto& b : st->tail_bnd) b.ag.dyn = st->d_scalars;
+  for (auto& l : st->tail_fb) l.dyn = st->d_scalars;
   st->ftail.dyn = st->d_scalars;
   const int adam_step0 = st->adam_step;
+  const uint64_t fb_epoch0 = st->fb_epoch;
   const uint64_t launches0 = ctx->launches;
   cudaGraph_t g = nullptr;
   MICS_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
@@ -1096,6 +1152,7 @@ void build_graph(mics_step* st) {
   st->graph_launches = ctx->launches - launches0;
   ctx->launches = launches0;
   st->adam_step = adam_step0;
+  st->fb_epoch = fb_epoch0;
   const cudaError_t e = cudaGraphInstantiate(&st->gexec, g, 0);
   cudaGraphDestroy(g);
   MICS_CUDA(e);
@@ -1107,6 +1164,7 @@ void replay(mics_step* st) {
   DevScalars v{};
   v.sc = make_adam_scalars(st->cfg.lr, st->cfg.beta1, st->cfg.beta2, st->cfg.eps, st->cfg.weight_decay,
                            st->adam_step, st->adam.grad_scale);
+  if (!st->tail_fb.empty()) v.epoch = ++st->fb_epoch;
   launch_set_scalars(ctx->stream, st->d_scalars, v);
   MICS_CUDA(cudaGraphLaunch(st->gexec, ctx->stream));
   ctx->launches += st->graph_launches + 1;

@@ -285,6 +285,146 @@ BoundaryLaunches build_boundary_range(mics_sync* st, const mics_adam* adam, mics
   return out;
 }
 
+// K9: the boundary of shard range [lo, hi) (one layer group of the overlapped tail) as ONE
+// launch: the replication-group reduce-scatter of every local rank's slice, published
+// block by block into every replica's flags, then Adam pulling each block once its
+// owner published it (FbRsJob / FbAdJob).  Same folds and Adam as build_boundary_range;
+// slices are whole blocks (fb_block()).  `flags`: per rank [groups][r][nblk] u64; `g`: this
+// group's index.  Entry barrier with the replication group (every replica's last
+// micro-step reduce-scatter of the group is done), exit barrier with the replication
+// and partition groups (done reading the owners' slices; parameters published).
+uint32_t fb_block() {
+  static const uint32_t b = [] {
+    const char* e = std::getenv("MICS_FB_BLOCK");
+    const long v = e ? std::atol(e) : 16384;
+    return uint32_t(std::max<long>(8192, round_up(uint64_t(std::max<long>(v, 1)), 8192)));
+  }();
+  return b;
+}
+
+Launch build_boundary_fused_range(mics_sync* st, const mics_adam* adam, uint64_t lo, uint64_t hi, mics_buf flags,
+                                  int g, int G, uint32_t nblk_max, int chan) {
+  mics_ctx* ctx = st->ctx;
+  const int n = st->n, p = st->p, r = n / p;
+  if (r > kTailMaxR) raise(MICS_SHAPE_ERROR, "fused boundary: more than 8 replicas");
+  const uint32_t blk = fb_block();
+  const uint64_t len = hi - lo, sub = round_up(ceil_div(len, uint64_t(r)), blk);
+  const uint32_t nblk = uint32_t(sub / blk);
+  if (nblk > nblk_max) raise(MICS_CONFIG_ERROR, "fused boundary: flag array too small");
+  uint64_t rmask = 0, pmask = 0;
+  for (int j = 0; j < p; ++j) {
+    const std::vector<int> ranks = iota_ranks(j, r, p);
+    rmask |= ctx->peer_mask(ranks.data(), r);
+  }
+  for (int gg = 0; gg < n / p; ++gg) {
+    const std::vector<int> ranks = iota_ranks(gg * p, p, 1);
+    pmask |= ctx->peer_mask(ranks.data(), p);
+  }
+  auto shard = [&](int rank) { return reinterpret_cast<float*>(ctx->rank_ptr(st->shard, rank)) + lo; };
+  auto flag_of = [&](int rank, int pos) {  // rank's flags for owner `pos` in group g
+    return reinterpret_cast<uint64_t*>(ctx->rank_ptr(flags, rank)) + (uint64_t(g) * r + pos) * nblk_max;
+  };
+  std::vector<FbRsJob> rs;
+  std::vector<FbAdJob> ad;
+  bool sys = false;
+  Launch l;
+  l.kind = Launch::FBND;
+  for (int rho = 0; rho < n; ++rho) {
+    if (!ctx->local(rho)) continue;
+    if (!l.fb_ticket)  // the first local rank's copy
+      l.fb_ticket = reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(ctx->rank_ptr(flags, rho)) +
+                                                uint64_t(G) * r * nblk_max + g);
+    const int j = rho % p, i = rho / p;
+    for (int q = 0; q < r; ++q) sys |= !ctx->local(j + q * p);
+    const uint64_t start = uint64_t(i) * sub, elems = start < len ? std::min(sub, len - start) : 0;
+    if (elems) {
+      FbRsJob J;
+      std::memset(&J, 0, sizeof(J));
+      for (int q = 0; q < r; ++q) {
+        J.src[q] = shard(j + q * p) + start;
+        J.flag[q] = flag_of(j + q * p, i);
+        (ctx->local(j + q * p) ? l.hbm_bytes : l.remote_bytes) += elems * 4;
+      }
+      J.own = shard(rho) + start;
+      J.elems = elems;
+      J.r = uint32_t(r);
+      l.hbm_bytes += elems * 4;
+      rs.push_back(J);
+    }
+  }
+  // Adam: one job per local rank; a second local replica of the same position shares it
+  std::vector<char> merged(static_cast<size_t>(n), 0);
+  auto bf_of = [&](int rho) -> uint16_t* {
+    return adam->param_bf16.stride ? reinterpret_cast<uint16_t*>(ctx->rank_ptr(adam->param_bf16, rho)) + lo : nullptr;
+  };
+  auto f32 = [&](mics_buf b, int rho) { return reinterpret_cast<float*>(ctx->rank_ptr(b, rho)) + lo; };
+  for (int rho = 0; rho < n; ++rho) {
+    if (!ctx->local(rho) || merged[size_t(rho)] || len == 0) continue;
+    const int j = rho % p;
+    FbAdJob J;
+    std::memset(&J, 0, sizeof(J));
+    for (int q = 0; q < r; ++q) {
+      J.owner[q] = shard(j + q * p);
+      const uint64_t a = std::min<uint64_t>(uint64_t(q) * sub, len), b = std::min<uint64_t>((uint64_t(q) + 1) * sub, len);
+      (ctx->local(j + q * p) ? l.hbm_bytes : l.remote_bytes) += (b - a) * 4;
+    }
+    J.flags = flag_of(rho, 0);
+    J.prm = f32(adam->param, rho);
+    J.m = f32(adam->exp_avg, rho);
+    J.v = f32(adam->exp_avg_sq, rho);
+    J.bf = bf_of(rho);
+    l.hbm_bytes += len * (24 + (J.bf ? 2 : 0));
+    for (int rho2 = rho + p; rho2 < n; rho2 += p)
+      if (ctx->local(rho2) && !merged[size_t(rho2)]) {
+        J.prm2 = f32(adam->param, rho2);
+        J.m2 = f32(adam->exp_avg, rho2);
+        J.v2 = f32(adam->exp_avg_sq, rho2);
+        J.bf2 = bf_of(rho2);
+        l.hbm_bytes += len * (24 + (J.bf2 ? 2 : 0));
+        merged[size_t(rho2)] = 1;
+        break;
+      }
+    J.elems = len;
+    J.sub = sub;
+    J.r = uint32_t(r);
+    J.nblk = nblk;
+    J.fstride = nblk_max;
+    ad.push_back(J);
+  }
+  l.fb_nrs = int(rs.size());
+  l.fb_r = r;
+  l.fb_nblk = nblk;
+  l.ndesc = int(rs.size() + ad.size());
+  l.fb_blk = blk;
+  // grid: one resident wave (MICS_FB_CTAS, experiments: CTAs per SM, at most the
+  // resident count, or 0: one CTA per item)
+  const char* ce = std::getenv("MICS_FB_CTAS");
+  const int per_sm = ce ? std::min(std::atoi(ce), ctx->occ_fbnd) : ctx->occ_fbnd;
+  const uint64_t wave = uint64_t(ctx->nsm) * uint64_t(per_sm > 0 ? per_sm : ctx->occ_fbnd);
+  // lag: Adam items of block t are taken two waves of CTAs after the fold of block t
+  // (MICS_FB_LAG overrides), so they rarely wait (C3, 4 GPUs: 1 wave 3.29 ms, 2 waves
+  // 3.18 ms, 8 rounds 3.64 ms)
+  const uint32_t per_round = uint32_t(rs.size() + ad.size() * size_t(r));
+  const char* le = std::getenv("MICS_FB_LAG");
+  l.fb_lag = le ? uint32_t(std::max(0, std::atoi(le))) : uint32_t(ceil_div(2 * wave, std::max<uint32_t>(per_round, 1))) + 1;
+  // rounds t = 0 .. nblk + lag - 1: the fold of block t, then Adam of block t - lag
+  l.ntiles = l.ndesc ? (nblk + l.fb_lag) * per_round : 0;
+  l.grid = int(std::max<uint64_t>(per_sm <= 0 ? l.ntiles : std::min<uint64_t>(l.ntiles, wave), 1));
+  l.hier_sys = sys ? 1 : 0;
+  l.adam = make_adam_scalars(adam->lr, adam->beta1, adam->beta2, adam->eps, adam->weight_decay, adam->step,
+                             adam->grad_scale);
+  l.bar = ctx->barrier(rmask | pmask, 1, 1, chan);
+  if (l.ndesc) {
+    const uint64_t rb = round_up(sizeof(FbRsJob) * rs.size(), 16), bytes = rb + sizeof(FbAdJob) * ad.size();
+    MICS_CUDA(cudaMalloc(&l.d_desc, bytes));
+    std::vector<char> blob(bytes, 0);
+    if (!rs.empty()) std::memcpy(blob.data(), rs.data(), sizeof(FbRsJob) * rs.size());
+    if (!ad.empty()) std::memcpy(blob.data() + rb, ad.data(), sizeof(FbAdJob) * ad.size());
+    MICS_CUDA(cudaMemcpy(l.d_desc, blob.data(), bytes, cudaMemcpyHostToDevice));
+  }
+  return l;
+}
+
 void boundary(mics_sync* st, const mics_adam* adam) {
   check_window(st, true);
   BoundaryLaunches b = build_boundary(st, adam, false, true);

@@ -43,6 +43,9 @@ Launch build_micro_launch(mics_sync* st, mics_buf grads, uint64_t goff, mics_dty
 BoundaryLaunches build_boundary(mics_sync* st, const mics_adam* adam, bool persistent, bool record);
 BoundaryLaunches build_boundary_range(mics_sync* st, const mics_adam* adam, mics_buf shard, uint64_t lo, uint64_t hi,
                                       int chan, int rs_chan = -1);
+// K9: layer group g of G; flags = per rank [G][r][nblk_max] u64 block flags, then G item tickets
+Launch build_boundary_fused_range(mics_sync* st, const mics_adam* adam, uint64_t lo, uint64_t hi, mics_buf flags,
+                                  int g, int G, uint32_t nblk_max, int chan);
 void micro_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode);
 void boundary(mics_sync* st, const mics_adam* adam);
 void alt_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale);
@@ -104,6 +107,10 @@ struct mics_step {
   mics::Launch ftail{};
   std::vector<mics::Launch> tail_rs;
   std::vector<mics::BoundaryLaunches> tail_bnd;
+  // K9 (default): each layer group's boundary as one fused launch (tail_bnd kept for A/B)
+  std::vector<mics::Launch> tail_fb;
+  mics_buf fbflags{};        // per rank [groups][r][nblk] u64 block flags
+  uint64_t fb_epoch = 0;     // flag value of the current step
   std::vector<cudaEvent_t> ev_tail, ev_tail_rs;   // [group]: last RS done / boundary RS done
   cudaEvent_t ev_tail_done = nullptr;
   cudaStream_t tail_rs_stream = nullptr;          // boundary reduce-scatters (channel 2), ahead of Adam

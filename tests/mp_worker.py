@@ -213,11 +213,12 @@ def main():
     # ---- overlapped tail (auto-on for multi-process jobs) vs in order; p=4 spans GPUs at world 4
     for pt in (2, 4):
         res = {}
-        for tail in ("0", "1"):
-            os.environ["MICS_TAIL_OVERLAP"] = tail
+        for tail in ("0", "1", "1f"):
+            os.environ["MICS_TAIL_OVERLAP"] = tail[0]
+            os.environ["MICS_TAIL_FUSED"] = "1" if tail == "1f" else "0"
             e5 = Engine(n_ranks=n, world=world, world_rank=rank, device=local, arena_bytes=256 << 20)
             mdist.connect(e5)
-            step = MicsStep(e5, Workload("tail", [70_000, 12_345, 40_000, 9_999, 33_333], p=pt, s=3),
+            step = MicsStep(e5, Workload("tail", [1_500_000, 70_000, 12_345, 700_000, 40_000, 9_999, 33_333], p=pt, s=3),
                             StepOptions(seed=5))
             step.run(2)
             step.profile()
@@ -228,8 +229,11 @@ def main():
             step.close()
             e5.close()
         os.environ.pop("MICS_TAIL_OVERLAP")
-        for x, y in zip(res["0"], res["1"]):
-            expect(np.array_equal(x.view(np.uint32), y.view(np.uint32)), f"overlapped tail != in-order (p={pt})")
+        os.environ.pop("MICS_TAIL_FUSED")
+        for t in ("1", "1f"):
+            for x, y in zip(res["0"], res[t]):
+                expect(np.array_equal(x.view(np.uint32), y.view(np.uint32)),
+                       f"overlapped tail ({t}) != in-order (p={pt})")
 
     # ---- the step with compute across processes (gathers / GEMMs / sync on three
     # streams, hierarchical gathers on barrier channel 1): GEMM gradients within

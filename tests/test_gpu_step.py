@@ -230,18 +230,20 @@ def test_run_host_matches_device_resident(resident):
 @pytest.mark.parametrize("graph", ["1", "0"])
 def test_overlapped_tail_matches_in_order(monkeypatch, graph):
     """Overlapped tail (last reduce-scatter per layer group on the main stream, each
-    group's boundary all-reduce + Adam on the side stream): same bits as the in-order
-    step over several steps, with a profiled (serialised) step and a host-input step
-    in between."""
+    group's boundary all-reduce + Adam on side streams, as two kernels or as the fused
+    K9 launch): same bits as the in-order step over several steps, with a profiled
+    (serialised) step and a host-input step in between."""
     from paper_2205_00119_b200.engine import Engine, host_alloc, host_free
     from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
     monkeypatch.setenv("MICS_GRAPH", graph)
     monkeypatch.setenv("MICS_FUSED_TAIL", "0")  # the in-order reference path, not K8 (one GPU)
-    wl = Workload("tail", [70_000, 12_345, 40_000, 9_999, 33_333, 4_096], p=2, s=3)
+    # the 1.5M / 700k layers give layer groups of several K9 blocks (65,536 elements) per owner
+    wl = Workload("tail", [1_500_000, 70_000, 12_345, 700_000, 40_000, 9_999, 33_333, 4_096], p=2, s=3)
     res = {}
-    for tail in ("0", "1"):
-        monkeypatch.setenv("MICS_TAIL_OVERLAP", tail)
-        eng = Engine(n_ranks=8, device=0, arena_bytes=256 << 20)
+    for tail in ("0", "1", "1f"):
+        monkeypatch.setenv("MICS_TAIL_OVERLAP", tail[0])
+        monkeypatch.setenv("MICS_TAIL_FUSED", "1" if tail == "1f" else "0")
+        eng = Engine(n_ranks=8, device=0, arena_bytes=1 << 30)
         step = MicsStep(eng, wl, StepOptions(seed=13, lr=1e-3, weight_decay=0.01))
         G = step.stats().grad_elems
         host, hptr = host_alloc(G * 4)
@@ -261,11 +263,16 @@ def test_overlapped_tail_matches_in_order(monkeypatch, graph):
         step.close()
         host_free(hptr)
         eng.close()
-    for x, y in zip(res["0"], res["1"]):
-        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
-    # same reduce-scatter bytes; the tail splits the last reduce-scatter and the boundary per layer group
-    assert res["1launch"][2] == res["0launch"][2]
-    assert res["1launch"][0] > res["0launch"][0] and res["1launch"][1] > res["0launch"][1]
+    for t in ("1", "1f"):
+        for x, y in zip(res["0"], res[t]):
+            assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), t
+        # same reduce-scatter bytes; the tail splits the last reduce-scatter and the boundary per layer group
+        assert res[t + "launch"][2] == res["0launch"][2]
+        assert res[t + "launch"][0] > res["0launch"][0] and res[t + "launch"][1] > res["0launch"][1]
+    # K9: one boundary launch per layer group (2 groups) instead of two (8 groups); the
+    # same boundary bytes
+    assert res["1flaunch"][1] < res["1launch"][1]
+    assert res["1flaunch"][3] == res["1launch"][3]
 
 
 @pytest.mark.parametrize("p,s,grad_dtype", [(2, 3, "f32"), (4, 2, "bf16"), (8, 2, "f32"), (2, 1, "bf16")])
