@@ -336,12 +336,10 @@ void enqueue(mics_ctx* ctx, const Launch& l, int dep_first, cudaStream_t stream)
       break;
     }
     case Launch::FBND: {
-      const auto* rs = static_cast<const FbRsJob*>(l.d_desc);
-      const auto* ad = reinterpret_cast<const FbAdJob*>(
-          static_cast<const char*>(l.d_desc) + round_up(sizeof(FbRsJob) * uint64_t(l.fb_nrs), 16));
-      launch_fbnd(st, rs, l.fb_nrs, ad, l.ndesc - l.fb_nrs, l.fb_nblk, l.fb_blk, l.fb_lag, l.ntiles, l.grid, l.adam,
-                  l.dyn,
-                  l.fb_epoch, l.hier_sys, l.fb_ticket, l.fb_r, bar);
+      FbArg a = l.fb;
+      a.items = l.ntiles;
+      a.sys_scope = l.hier_sys;
+      launch_fbnd(st, a, l.grid, l.adam, l.dyn, l.fb_epoch, bar);
       break;
     }
     case Launch::TAIL:
