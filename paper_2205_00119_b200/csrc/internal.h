@@ -169,32 +169,13 @@ struct TailJob {
 // overlap all through the launch.  An Adam item waits only on reduce-scatter items of an
 // earlier round, which never wait, and items are taken in order from a ticket counter,
 // so every awaited flag is produced by a running CTA.
-//
-// K10 (the same kernel with stage-A items, `build_fused_tail_multi`): the last
-// micro-step's partition-group reduce-scatter joins the launch.  Stage-A items compute a
-// local rank's final accumulator block (acc (+)= fold over the p members' gradients, the
-// k_reduce / K8 folds) and push a flag to the block's owner; fold items wait for the
-// flags of all r replicas first.  Rounds: stage A of block t, the fold of block t - lag,
-// Adam of block t - 2 lag.  Every wait targets items of earlier rounds, and stage-A
-// items never wait.
 uint32_t fb_block();                  // elements per published block (MICS_FB_BLOCK, default 16 Ki)
 struct FbRsJob {                      // one local rank's slice of the group
   const float* src[kTailMaxR];        // replica q's shard at this slice
   float* own;                         // this rank's shard at this slice (reduced in place)
   uint64_t* flag[kTailMaxR];          // replica q's flag for this slice's block 0
-  const uint64_t* aflags;             // K10: this rank's stage-A flags, replica q's block k at q * fstride + k
   uint64_t elems;
-  uint32_t r, fstride;
-};
-struct FtSeg {                        // K10: one layer's piece of the shard (identical on every rank)
-  uint64_t so, c;                     // shard offset and length (elements)
-  uint64_t goff, len;                 // gradient offset of the layer and its length (elements)
-};
-struct FtAJob {                       // K10 stage A: one local rank's accumulator
-  const uint8_t* grads[kTailMaxP];    // partition member i's gradient slot (element 0)
-  float* acc;                         // this rank's shard (element 0)
-  uint64_t* aflag[kTailMaxR];         // owner q's stage-A flags, this rank's row (block 0)
-  uint32_t j, p, pad_[2];             // partition position; partition size
+  uint32_t r, pad_;
 };
 struct FbAdJob {                      // one local rank (+ an optional second replica of its position)
   const float* owner[kTailMaxR];      // replica q's shard at the group start (q reduced slice q)
@@ -213,15 +194,11 @@ struct FbAdJob {                      // one local rank (+ an optional second re
 struct FbArg {                        // one k_fbnd launch (device pointers into its descriptor blob)
   const FbRsJob* rs = nullptr;
   const FbAdJob* ad = nullptr;
-  const FtAJob* aj = nullptr;         // K10 stage A (nA == 0: K9)
-  const FtSeg* segs = nullptr;
-  int nrs = 0, nad = 0, nA = 0, nseg = 0;
-  uint32_t r = 2, nblk = 0, blk = 0, lag = 0;
-  uint32_t items = 0, zero_accum = 0;
-  uint64_t lo = 0, sub = 0, hi = 0;   // stage A: the range (shard elements) and slice length
+  int nrs = 0, nad = 0;
+  uint32_t r = 2, nblk = 0, blk = 0, lag = 0;  // replicas; blocks per slice, elements per block; rounds
+  uint32_t items = 0;
   uint32_t* ticket = nullptr;         // this GPU's item counter (zero between launches)
   int sys_scope = 0;
-  mics_dtype in_t = MICS_F32;         // stage A: gradient type
 };
 
 // Flag barrier between processes: remote_flag[w] is the slot on process w's

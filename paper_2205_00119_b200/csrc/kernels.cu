@@ -946,127 +946,28 @@ __device__ __forceinline__ void adam_rows(const uint4 (&gr)[UA], float* prm, flo
   }
 }
 
-// K10 stage A on one 4-element vector at shard index x (inside one layer's piece):
-// acc[x..x+3] (+)= fold over the p members' gradients, as k_reduce / k_tail fold them
-template <typename In>
-__device__ __forceinline__ void stage_a_vec(const FtAJob& J, const FtSeg* segs, int nseg, uint64_t x,
-                                            uint32_t zero_accum) {
-  int lo = 0, hi = nseg - 1;  // the layer piece holding x (pieces are contiguous, 8-element aligned)
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (segs[mid].so <= x) lo = mid; else hi = mid - 1;
-  }
-  const FtSeg& S = segs[lo];
-  const uint64_t pos = uint64_t(J.j) * S.c + (x - S.so);  // position in the layer's padded gradient
-  float a[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-  if (!zero_accum) {
-    const float4 t = *reinterpret_cast<const float4*>(J.acc + x);
-    a[0] = t.x; a[1] = t.y; a[2] = t.z; a[3] = t.w;
-  }
-  float f[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // padding: every member contributes zeros, the fold is +0
-  if (pos < S.len) {  // a wholly padded vector reads no gradient
-    // members in batches of 4 (all loads of a batch in flight), folded in ascending order
-    for (uint32_t b = 0; b < J.p; b += 4) {
-      float g[4][4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (b + i < J.p) load4<In>(J.grads[b + i], S.goff + pos, g[i]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (b + i < J.p)
-#pragma unroll
-          for (int k = 0; k < 4; ++k) f[k] = (b + i == 0) ? g[0][k] : __fadd_rn(f[k], g[i][k]);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (pos + uint64_t(k) >= S.len) f[k] = 0.0f;
-  }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) a[k] = zero_accum ? __fadd_rn(0.0f, f[k]) : __fadd_rn(a[k], f[k]);
-  *reinterpret_cast<float4*>(J.acc + x) = make_float4(a[0], a[1], a[2], a[3]);
-}
-
-// kStageRows vectors x + u * kThreads * 4 of stage A: one piece lookup and every load in
-// flight when they share a layer piece (the common case), else one vector at a time
-constexpr int kStageRows = 2;
-template <typename In>
-__device__ __forceinline__ void stage_a_rows(const FtAJob& J, const FtSeg* segs, int nseg, uint64_t x,
-                                             uint32_t zero_accum) {
-  constexpr uint32_t kRow = kThreads * 4;
-  int lo = 0, hi = nseg - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (segs[mid].so <= x) lo = mid; else hi = mid - 1;
-  }
-  const FtSeg& S = segs[lo];
-  const uint64_t pos = uint64_t(J.j) * S.c + (x - S.so);
-  if (x + (kStageRows - 1) * kRow >= S.so + S.c || pos + (kStageRows - 1) * kRow + 4 > S.len || J.p > 4) {
-#pragma unroll 1
-    for (int u = 0; u < kStageRows; ++u) stage_a_vec<In>(J, segs, nseg, x + u * kRow, zero_accum);
-    return;
-  }
-  float a[kStageRows][4] = {};
-  if (!zero_accum) {
-#pragma unroll
-    for (int u = 0; u < kStageRows; ++u) {
-      const float4 t = *reinterpret_cast<const float4*>(J.acc + x + u * kRow);
-      a[u][0] = t.x; a[u][1] = t.y; a[u][2] = t.z; a[u][3] = t.w;
-    }
-  }
-  float g[4][kStageRows][4] = {};  // [member][row][lane]: every gradient of the rows valid
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (i < int(J.p))
-#pragma unroll
-      for (int u = 0; u < kStageRows; ++u) load4<In>(J.grads[i], S.goff + pos + u * kRow, g[i][u]);
-#pragma unroll
-  for (int u = 0; u < kStageRows; ++u) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      float f = g[0][u][k];
-#pragma unroll
-      for (int i = 1; i < 4; ++i)
-        if (i < int(J.p)) f = __fadd_rn(f, g[i][u][k]);
-      a[u][k] = zero_accum ? __fadd_rn(0.0f, f) : __fadd_rn(a[u][k], f);
-    }
-    *reinterpret_cast<float4*>(J.acc + x + u * kRow) = make_float4(a[u][0], a[u][1], a[u][2], a[u][3]);
-  }
-}
-
-// See FbRsJob / FbAdJob / FtAJob (internal.h).  PDL: waits for its predecessor at entry
-// and lets its successor launch only at exit (CTAs spin on flags: nothing may take their
-// slots).  Items are handed out in order from a ticket counter, so every item of an
-// earlier round is taken by a running CTA before any item of a later round: a CTA only
-// waits on items of earlier rounds, and stage-A items (K10) and fold items without
-// stage A (K9) never wait.  Each CTA takes exactly one ticket past the end, so the launch
-// consumes items + gridDim.x tickets and the last of them resets the counter for the next
-// launch.  RC = replica-count class (2, 4, 8): the fold keeps 8 vectors per thread in
-// flight (RC x U), like k_reduce.  In = stage A's gradient type.
-// SA: with K10's stage A.  Adam rows per thread in flight (x 4 streams of 16 B loads):
-// 4 without stage A, 2 with it (4 would spill at 128 registers)
-template <int RC, typename In, bool SA>
+// See FbRsJob / FbAdJob (internal.h).  PDL: waits for its predecessor at entry and lets
+// its successor launch only at exit (CTAs spin on flags: nothing may take their slots).
+// Items are handed out in order from a ticket counter, so every item of an earlier round
+// is taken by a running CTA before any item of a later round: an Adam item waits only on
+// fold items of earlier rounds, which never wait.  Each CTA takes exactly one ticket past
+// the end, so the launch consumes items + gridDim.x tickets and the last of them resets
+// the counter for the next launch.  RC = replica-count class (2, 4, 8): the fold keeps 8
+// vectors per thread in flight (RC x U), like k_reduce; Adam 4 rows x 4 streams of 16 B.
+template <int RC>
 __global__ void __launch_bounds__(kThreads, 2) k_fbnd(FbArg fa, AdamScalars sc, const DevScalars* __restrict__ dyn,
                                                       uint64_t epoch, BarrierArg bar) {
   constexpr int U = 8 / RC;
-  constexpr int kFbAdamRows = SA ? 2 : 4;
+  constexpr int kFbAdamRows = 4;
   constexpr uint32_t kRow = kThreads * 4;  // fp32 elements of one float4 row
-  extern __shared__ __align__(16) unsigned char smem[];
-  // stage A's layer pieces, staged in shared memory when they fit (launch_fbnd sizes it)
-  const FtSeg* segs = fa.segs;
-  if (SA) {
-    FtSeg* s = reinterpret_cast<FtSeg*>(smem);
-    for (int i = threadIdx.x; i < fa.nseg; i += kThreads) s[i] = fa.segs[i];
-    segs = s;
-  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (dyn) {  // a replayed graph: this step's scalars and flag value
     sc = dyn->sc;
     epoch = dyn->epoch;
   }
-  bar_entry(bar);  // (its __syncthreads also publishes the staged pieces)
-  const uint32_t r = fa.r, nA = SA ? uint32_t(fa.nA) : 0u, nrs = uint32_t(fa.nrs);
-  const uint32_t lag_b = SA ? fa.lag : 0, lag_c = lag_b + fa.lag;
-  const uint32_t per_round = nA * r + nrs + uint32_t(fa.nad) * r;
+  bar_entry(bar);
+  const uint32_t r = fa.r, nrs = uint32_t(fa.nrs);
+  const uint32_t per_round = nrs + uint32_t(fa.nad) * r;
   __shared__ uint32_t s_item;
   // gridDim.x >= items: one item per CTA (CTAs retire, so the hardware can give freed
   // slots to other streams' kernels); else persistent CTAs
@@ -1085,69 +986,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_fbnd(FbArg fa, AdamScalars sc, 
     const uint32_t item = s_item;
     if (item >= items) break;
     const uint32_t round = item / per_round, w = item - round * per_round;
-    if (SA && w < nA * r) {  // K10 stage A: local rank w / r, owner slice i, block `round`
-      const FtAJob& J = fa.aj[w / r];
-      const uint32_t i = w % r, b = round;
-      const uint64_t s0 = fa.lo + uint64_t(i) * fa.sub, s1 = s0 + fa.sub < fa.hi ? s0 + fa.sub : fa.hi;
-      const uint64_t e0 = s0 + uint64_t(b) * fa.blk;
-      if (b >= fa.nblk || e0 >= s1) continue;
-      const uint64_t end = e0 + fa.blk < s1 ? e0 + fa.blk : s1;  // a multiple of 8 (pieces are)
-      uint64_t x = e0 + threadIdx.x * 4;
-      for (; x + (kStageRows - 1) * kRow < end; x += kStageRows * kRow) stage_a_rows<In>(J, segs, fa.nseg, x, fa.zero_accum);
-      for (; x < end; x += kRow) stage_a_vec<In>(J, segs, fa.nseg, x, fa.zero_accum);
-      __syncthreads();  // the block's stores, then its flag on the owner
-      if (threadIdx.x == 0) {
-        if (fa.sys_scope) fence_sys(); else fence_gpu();
-        if (fa.sys_scope) st_relaxed_sys(J.aflag[i] + b, epoch);
-        else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(J.aflag[i] + b), "l"(epoch) : "memory");
-      }
-    } else if (w - nA * r < nrs) {  // fold of block `round - lag_b` of a local slice
-      if (round < lag_b) continue;
-      const FbRsJob& J = fa.rs[w - nA * r];
-      const uint32_t b = round - lag_b;
+    if (w < nrs) {  // fold of block `round` of a local slice
+      const FbRsJob& J = fa.rs[w];
+      const uint32_t b = round;
       const uint64_t e0 = uint64_t(b) * fa.blk;
       if (e0 >= J.elems) continue;  // this slice has fewer blocks (or the lag rounds)
       const uint64_t end = e0 + fa.blk < J.elems ? e0 + fa.blk : J.elems;
-      if (SA) {  // K10: every replica's accumulator block is final
-        if (threadIdx.x < r) wait_flag(J.aflags + uint64_t(threadIdx.x) * J.fstride + b, epoch, fa.sys_scope);
-        __syncthreads();
-      }
       const uint8_t* const* srcs = reinterpret_cast<const uint8_t* const*>(J.src);
       uint64_t e = e0;
       // full groups of U rows: all r x U sources in flight, the fold in ascending replica order
-      // (K10: the accumulators were written during this launch, so L2-coherent loads)
       for (; e + uint64_t(U) * kRow <= end; e += uint64_t(U) * kRow) {
         float acc[U][4];
-        if constexpr (SA) {
-          uint4 raw[RC][U] = {};  // (initialised: the predicated-off sources carry nothing across iterations)
-#pragma unroll
-          for (int q = 0; q < RC; ++q)
-            if (q < int(J.r))
-#pragma unroll
-              for (int u = 0; u < U; ++u) raw[q][u] = ld_cg(J.src[q] + e + threadIdx.x * 4 + u * kRow);
-#pragma unroll
-          for (int u = 0; u < U; ++u) Codec<float, float>::unpack(raw[0][u], acc[u]);
-#pragma unroll
-          for (int q = 1; q < RC; ++q)
-            if (q < int(J.r))
-#pragma unroll
-              for (int u = 0; u < U; ++u) {
-                float x[4];
-                Codec<float, float>::unpack(raw[q][u], x);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) acc[u][k] = __fadd_rn(acc[u][k], x[k]);
-              }
-        } else {
-          fold_vecs<float, float, RC, U>(srcs, J.r, e + threadIdx.x * 4, kRow, acc);
-        }
+        fold_vecs<float, float, RC, U>(srcs, J.r, e + threadIdx.x * 4, kRow, acc);
 #pragma unroll
         for (int u = 0; u < U; ++u)
           *reinterpret_cast<float4*>(J.own + e + threadIdx.x * 4 + u * kRow) =
               make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
       }
       for (uint64_t x = e + threadIdx.x; x < end; x += kThreads) {  // the slice's ragged end
-        float a = *reinterpret_cast<const volatile float*>(J.src[0] + x);
-        for (uint32_t q = 1; q < J.r; ++q) a = __fadd_rn(a, *reinterpret_cast<const volatile float*>(J.src[q] + x));
+        float a = J.src[0][x];
+        for (uint32_t q = 1; q < J.r; ++q) a = __fadd_rn(a, J.src[q][x]);
         J.own[x] = a;
       }
       __syncthreads();  // the block's stores, then one flag into every replica's array
@@ -1158,9 +1016,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_fbnd(FbArg fa, AdamScalars sc, 
           else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(J.flag[q] + b), "l"(epoch) : "memory");
         }
       }
-    } else {  // Adam of block `round - lag_c` of owner q's slice
-      if (round < lag_c || round - lag_c >= fa.nblk) continue;
-      const uint32_t a = w - nA * r - nrs, q = a % r, k = round - lag_c;  // owners interleaved
+    } else {  // Adam of block `round - lag` of owner q's slice
+      if (round < fa.lag || round - fa.lag >= fa.nblk) continue;
+      const uint32_t a = w - nrs, q = a % r, k = round - fa.lag;  // owners interleaved
       const FbAdJob& J = fa.ad[a / r];
       const uint64_t e0 = uint64_t(q) * J.sub + uint64_t(k) * fa.blk;
       const uint64_t send = (uint64_t(q) + 1) * J.sub < J.elems ? (uint64_t(q) + 1) * J.sub : J.elems;
@@ -1285,9 +1143,9 @@ int resident_ctas(int kind, mics_dtype in_t, int pc) {
       break;
     case 5: {
       int n2 = 0, n4 = 0;
-      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fbnd<8, float, false>, kThreads, kSmemTable));
-      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n4, k_fbnd<4, float, true>, kThreads, kSmemTable));
-      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n2, k_fbnd<2, uint16_t, true>, kThreads, kSmemTable));
+      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fbnd<8>, kThreads, 0));
+      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n4, k_fbnd<4>, kThreads, 0));
+      MICS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n2, k_fbnd<2>, kThreads, 0));
       n = std::min(n, std::min(n2, n4));
       break;
     }
@@ -1387,16 +1245,8 @@ void launch_cast_bf16(cudaStream_t s, const float* in, uint16_t* out, uint64_t c
 
 void launch_fbnd(cudaStream_t s, const FbArg& fa, int grid, const AdamScalars& sc, const DevScalars* dyn,
                  uint64_t epoch, const BarrierArg& bar) {
-  const size_t smem = fa.nA ? size_t(fa.nseg) * sizeof(FtSeg) : 0;
-  using K = void (*)(FbArg, AdamScalars, const DevScalars*, uint64_t, BarrierArg);
-  K kern;
-  if (!fa.nA) kern = fa.r <= 2 ? k_fbnd<2, float, false> : fa.r <= 4 ? k_fbnd<4, float, false> : k_fbnd<8, float, false>;
-  else if (fa.in_t == MICS_BF16)
-    kern = fa.r <= 2 ? k_fbnd<2, uint16_t, true> : fa.r <= 4 ? k_fbnd<4, uint16_t, true> : k_fbnd<8, uint16_t, true>;
-  else
-    kern = fa.r <= 2 ? k_fbnd<2, float, true> : fa.r <= 4 ? k_fbnd<4, float, true> : k_fbnd<8, float, true>;
-  if (smem > 48 * 1024) MICS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  launch_ex(kern, grid, kThreads, smem, s, fa, sc, dyn, epoch, bar);
+  auto kern = fa.r <= 2 ? k_fbnd<2> : fa.r <= 4 ? k_fbnd<4> : k_fbnd<8>;
+  launch_ex(kern, grid, kThreads, 0, s, fa, sc, dyn, epoch, bar);
 }
 
 void launch_barrier(cudaStream_t s, const BarrierArg& bar) {

@@ -352,40 +352,17 @@ void build_fused_tail(mics_step* st) {
   st->fused_tail = true;
 }
 
-// K10 plan: the last micro-step's reduce-scatter, the boundary fold and Adam over the
-// whole shard in one k_fbnd launch (ranks on several GPUs; K8 when all are local)
-void build_fused_tail_multi(mics_step* st) {
-  mics_ctx* ctx = st->ctx;
-  mics_sync* sy = st->sync;
-  const int r = sy->n / sy->p, s = st->cfg.s;
-  const uint64_t S = sy->shard_elems;
-  const uint32_t nblk = uint32_t(std::max<uint64_t>(1, ceil_div(ceil_div(S, uint64_t(r)), fb_block())));
-  st->fbflags = alloc_sym(ctx, (2 * uint64_t(r) * nblk + 1) * 8);
-  MICS_CUDA(cudaMemsetAsync(ctx->base + st->fbflags.offset, 0, st->fbflags.stride * uint64_t(ctx->per), ctx->stream));
-  FtStage sa;
-  sa.grads = st->grads;
-  sa.goff_bytes = uint64_t((s - 1) % st->gslots) * sy->grad_elems * dtype_size(st->cfg.grad_t);
-  sa.in_t = st->cfg.grad_t;
-  sa.zero_accum = s == 1 ? 1 : 0;
-  st->ftail = build_boundary_fused_range(sy, &st->adam, 0, S, st->fbflags, 0, 1, nblk, 0, &sa);
-  st->fused_tail = true;
-  st->ftail_multi = true;
-}
-
 void enqueue_fused_tail(mics_step* st) {
   mics_ctx* ctx = st->ctx;
   st->adam_step++;
-  if (st->ftail_multi) ++st->fb_epoch;  // K10's flag value of this step
   const AdamScalars sc = make_adam_scalars(st->cfg.lr, st->cfg.beta1, st->cfg.beta2, st->cfg.eps,
                                            st->cfg.weight_decay, st->adam_step, st->adam.grad_scale);
   if (st->d_scalars && !st->capturing) {
     DevScalars v{};
     v.sc = sc;
-    v.epoch = st->fb_epoch;
     launch_set_scalars(ctx->stream, st->d_scalars, v);
   }
   st->ftail.adam = sc;
-  st->ftail.fb_epoch = st->fb_epoch;
   enqueue(ctx, st->ftail);
 }
 
@@ -931,14 +908,7 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
       // auto: any multi-process job with a replication fold (measured: N=2 17.48 -> 16.74 ms,
       // N=4 9.11 -> 8.96, one rank per GPU on 4 GPUs 9.94 -> 9.84)
       const bool auto_on = ctx->world > 1 && sy->n / sy->p > 1;
-      // K10 (default across GPUs; MICS_FTAIL=0 off, 2 also on one GPU; an explicit
-      // MICS_TAIL_OVERLAP selects the in-order or the overlapped tail instead): the last
-      // reduce-scatter, the boundary and Adam in one launch
-      const char* fte = std::getenv("MICS_FTAIL");
-      const bool ftm_ok = !st->compute && sy->n / sy->p > 1 && sy->n / sy->p <= kTailMaxR && sy->p <= kTailMaxP &&
-                          (cfg->grad_t == MICS_F32 || cfg->grad_t == MICS_BF16);
-      const bool ftm = ftm_ok && (fte ? (fte[0] == '2' || (fte[0] == '1' && ctx->world > 1)) : (!te && auto_on));
-      st->tail = !ftm && !st->compute && sy->n / sy->p > 1 && (te ? te[0] == '1' : auto_on);
+      st->tail = !st->compute && sy->n / sy->p > 1 && (te ? te[0] == '1' : auto_on);
       if (st->tail) {
         // K9 (default; MICS_TAIL_FUSED=0: the two-kernel boundary): each group's boundary
         // reduce-scatter and Adam in one launch, Adam blocks pulling a slice block as soon
@@ -987,10 +957,8 @@ mics_step* step_create(mics_ctx* ctx, const mics_step_cfg* cfg, bool settle) {
 
       }
       const char* fe = std::getenv("MICS_FUSED_TAIL");
-      if (ftm)
-        build_fused_tail_multi(st);
-      else if (!st->tail && !st->compute && ctx->world == 1 && !(fe && fe[0] == '0') &&
-               tail_supported(cfg->grad_t, sy->n / sy->p, sy->p))
+      if (!st->tail && !st->compute && ctx->world == 1 && !(fe && fe[0] == '0') &&
+          tail_supported(cfg->grad_t, sy->n / sy->p, sy->p))
         build_fused_tail(st);
     } else {  // shards already hold the global sum: the boundary is Adam on the own shard
       AdamPlan ap;
@@ -1197,7 +1165,7 @@ void replay(mics_step* st) {
   DevScalars v{};
   v.sc = make_adam_scalars(st->cfg.lr, st->cfg.beta1, st->cfg.beta2, st->cfg.eps, st->cfg.weight_decay,
                            st->adam_step, st->adam.grad_scale);
-  if (!st->tail_fb.empty() || st->ftail_multi) v.epoch = ++st->fb_epoch;
+  if (!st->tail_fb.empty()) v.epoch = ++st->fb_epoch;
   launch_set_scalars(ctx->stream, st->d_scalars, v);
   MICS_CUDA(cudaGraphLaunch(st->gexec, ctx->stream));
   ctx->launches += st->graph_launches + 1;

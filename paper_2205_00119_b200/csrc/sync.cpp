@@ -303,7 +303,7 @@ uint32_t fb_block() {
 }
 
 Launch build_boundary_fused_range(mics_sync* st, const mics_adam* adam, uint64_t lo, uint64_t hi, mics_buf flags,
-                                  int g, int G, uint32_t nblk_max, int chan, const FtStage* sa) {
+                                  int g, int G, uint32_t nblk_max, int chan) {
   mics_ctx* ctx = st->ctx;
   const int n = st->n, p = st->p, r = n / p;
   if (r > kTailMaxR) raise(MICS_SHAPE_ERROR, "fused boundary: more than 8 replicas");
@@ -324,12 +324,7 @@ Launch build_boundary_fused_range(mics_sync* st, const mics_adam* adam, uint64_t
   auto flag_of = [&](int rank, int pos) {  // rank's flags for owner `pos` in group g
     return reinterpret_cast<uint64_t*>(ctx->rank_ptr(flags, rank)) + (uint64_t(g) * r + pos) * nblk_max;
   };
-  // K10: stage-A flags after the fold flags (rank's row for replica `q`), then the tickets
-  auto aflag_of = [&](int rank, int q) {
-    return reinterpret_cast<uint64_t*>(ctx->rank_ptr(flags, rank)) + uint64_t(G) * r * nblk_max +
-           (uint64_t(g) * r + q) * nblk_max;
-  };
-  const uint64_t ticket_off = uint64_t(sa ? 2 : 1) * G * r * nblk_max + g;
+  const uint64_t ticket_off = uint64_t(G) * r * nblk_max + g;  // after every group's flags
   std::vector<FbRsJob> rs;
   std::vector<FbAdJob> ad;
   bool sys = false;
@@ -353,8 +348,6 @@ Launch build_boundary_fused_range(mics_sync* st, const mics_adam* adam, uint64_t
       J.own = shard(rho) + start;
       J.elems = elems;
       J.r = uint32_t(r);
-      J.fstride = nblk_max;
-      if (sa) J.aflags = aflag_of(rho, 0);
       l.hbm_bytes += elems * 4;
       rs.push_back(J);
     }
@@ -398,47 +391,12 @@ Launch build_boundary_fused_range(mics_sync* st, const mics_adam* adam, uint64_t
     J.fstride = nblk_max;
     ad.push_back(J);
   }
-  // K10 stage A: every local rank's accumulator over the range, in blocks of the owners' slices
-  std::vector<FtAJob> aj;
-  std::vector<FtSeg> segs;
-  if (sa) {
-    const uint64_t szg = dtype_size(sa->in_t);
-    for (int rho = 0; rho < n; ++rho) {
-      if (!ctx->local(rho)) continue;
-      const int j = rho % p, q0 = rho / p;
-      FtAJob J;
-      std::memset(&J, 0, sizeof(J));
-      for (int i = 0; i < p; ++i) {
-        const int m = q0 * p + i;  // partition member i
-        J.grads[i] = reinterpret_cast<const uint8_t*>(ctx->rank_ptr(sa->grads, m) + sa->goff_bytes);
-        (ctx->local(m) ? l.hbm_bytes : l.remote_bytes) += len * szg;
-      }
-      J.acc = reinterpret_cast<float*>(ctx->rank_ptr(st->shard, rho));
-      for (int q = 0; q < r; ++q) J.aflag[q] = aflag_of(j + q * p, q0);
-      J.j = uint32_t(j);
-      J.p = uint32_t(p);
-      l.hbm_bytes += len * (sa->zero_accum ? 4 : 8);
-      aj.push_back(J);
-    }
-    for (size_t x = 0; x < st->shard_off.size(); ++x) {
-      const uint64_t so = st->shard_off[x], c = st->chunk[x];
-      if (so + c <= lo || so >= hi || c == 0) continue;
-      segs.push_back({so, c, st->grad_off[x], st->len[x]});
-    }
-  }
   l.fb.nrs = int(rs.size());
   l.fb.nad = int(ad.size());
-  l.fb.nA = int(aj.size());
-  l.fb.nseg = int(segs.size());
   l.fb.r = uint32_t(r);
   l.fb.nblk = nblk;
   l.fb.blk = blk;
-  l.fb.lo = lo;
-  l.fb.hi = hi;
-  l.fb.sub = sub;
-  l.fb.in_t = sa ? sa->in_t : MICS_F32;
-  l.fb.zero_accum = sa ? uint32_t(sa->zero_accum) : 0;
-  l.ndesc = int(rs.size() + ad.size() + aj.size());
+  l.ndesc = int(rs.size() + ad.size());
   // grid: one resident wave (MICS_FB_CTAS, experiments: CTAs per SM, at most the
   // resident count, or 0: one CTA per item)
   const char* ce = std::getenv("MICS_FB_CTAS");
@@ -447,34 +405,25 @@ Launch build_boundary_fused_range(mics_sync* st, const mics_adam* adam, uint64_t
   // lag: Adam items of block t are taken two waves of CTAs after the fold of block t
   // (MICS_FB_LAG overrides), so they rarely wait (C3, 4 GPUs: 1 wave 3.29 ms, 2 waves
   // 3.18 ms, 8 rounds 3.64 ms)
-  const uint32_t per_round = uint32_t(rs.size() + (ad.size() + aj.size()) * size_t(r));
+  const uint32_t per_round = uint32_t(rs.size() + ad.size() * size_t(r));
   const char* le = std::getenv("MICS_FB_LAG");
   l.fb.lag = le ? uint32_t(std::max(0, std::atoi(le))) : uint32_t(ceil_div(2 * wave, std::max<uint32_t>(per_round, 1))) + 1;
-  // rounds t = 0 .. nblk + lag - 1: the fold of block t, then Adam of block t - lag (K10: stage A
-  // of block t, the fold of block t - lag, Adam of block t - 2 lag)
-  l.ntiles = l.ndesc ? (nblk + (sa ? 2 : 1) * l.fb.lag) * per_round : 0;
+  // rounds t = 0 .. nblk + lag - 1: the fold of block t, then Adam of block t - lag
+  l.ntiles = l.ndesc ? (nblk + l.fb.lag) * per_round : 0;
   l.grid = int(std::max<uint64_t>(per_sm <= 0 ? l.ntiles : std::min<uint64_t>(l.ntiles, wave), 1));
   l.hier_sys = sys ? 1 : 0;
   l.adam = make_adam_scalars(adam->lr, adam->beta1, adam->beta2, adam->eps, adam->weight_decay, adam->step,
                              adam->grad_scale);
   l.bar = ctx->barrier(rmask | pmask, 1, 1, chan);
-  if (l.ndesc) {  // one blob: fold jobs, Adam jobs, stage-A jobs, layer pieces
-    const uint64_t o1 = round_up(sizeof(FbRsJob) * rs.size(), 16);
-    const uint64_t o2 = o1 + round_up(sizeof(FbAdJob) * ad.size(), 16);
-    const uint64_t o3 = o2 + round_up(sizeof(FtAJob) * aj.size(), 16);
-    const uint64_t bytes = o3 + sizeof(FtSeg) * segs.size();
+  if (l.ndesc) {  // one blob: fold jobs, then Adam jobs
+    const uint64_t o1 = round_up(sizeof(FbRsJob) * rs.size(), 16), bytes = o1 + sizeof(FbAdJob) * ad.size();
     MICS_CUDA(cudaMalloc(&l.d_desc, bytes));
     std::vector<char> blob(bytes, 0);
     if (!rs.empty()) std::memcpy(blob.data(), rs.data(), sizeof(FbRsJob) * rs.size());
     if (!ad.empty()) std::memcpy(blob.data() + o1, ad.data(), sizeof(FbAdJob) * ad.size());
-    if (!aj.empty()) std::memcpy(blob.data() + o2, aj.data(), sizeof(FtAJob) * aj.size());
-    if (!segs.empty()) std::memcpy(blob.data() + o3, segs.data(), sizeof(FtSeg) * segs.size());
     MICS_CUDA(cudaMemcpy(l.d_desc, blob.data(), bytes, cudaMemcpyHostToDevice));
-    char* base = static_cast<char*>(l.d_desc);
-    l.fb.rs = reinterpret_cast<const FbRsJob*>(base);
-    l.fb.ad = reinterpret_cast<const FbAdJob*>(base + o1);
-    l.fb.aj = reinterpret_cast<const FtAJob*>(base + o2);
-    l.fb.segs = reinterpret_cast<const FtSeg*>(base + o3);
+    l.fb.rs = static_cast<const FbRsJob*>(l.d_desc);
+    l.fb.ad = reinterpret_cast<const FbAdJob*>(static_cast<const char*>(l.d_desc) + o1);
   }
   return l;
 }

@@ -43,16 +43,9 @@ Launch build_micro_launch(mics_sync* st, mics_buf grads, uint64_t goff, mics_dty
 BoundaryLaunches build_boundary(mics_sync* st, const mics_adam* adam, bool persistent, bool record);
 BoundaryLaunches build_boundary_range(mics_sync* st, const mics_adam* adam, mics_buf shard, uint64_t lo, uint64_t hi,
                                       int chan, int rs_chan = -1);
-// K9: layer group g of G; flags = per rank [G][r][nblk_max] u64 block flags (K10: then as many
-// stage-A flags), then G item tickets.  sa: K10's stage A (the last micro-step's reduce-scatter)
-struct FtStage {
-  mics_buf grads;         // the gradient slots
-  uint64_t goff_bytes;    // the last micro-step's slot
-  mics_dtype in_t;
-  int zero_accum;         // the last micro-step is the first (s = 1)
-};
+// K9: layer group g of G; flags = per rank [G][r][nblk_max] u64 block flags, then G item tickets
 Launch build_boundary_fused_range(mics_sync* st, const mics_adam* adam, uint64_t lo, uint64_t hi, mics_buf flags,
-                                  int g, int G, uint32_t nblk_max, int chan, const FtStage* sa = nullptr);
+                                  int g, int G, uint32_t nblk_max, int chan);
 void micro_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale, int mode);
 void boundary(mics_sync* st, const mics_adam* adam);
 void alt_step(mics_sync* st, mics_buf grads, uint64_t goff, mics_dtype grad_t, double scale);
@@ -111,7 +104,6 @@ struct mics_step {
   // Fused tail (every rank on this GPU, N=1; MICS_FUSED_TAIL=0 disables): the last
   // micro-step's reduce-scatter + the boundary all-reduce + Adam as one K8 launch
   bool fused_tail = false;
-  bool ftail_multi = false;  // K10 (k_fbnd with stage A) instead of K8
   mics::Launch ftail{};
   std::vector<mics::Launch> tail_rs;
   std::vector<mics::BoundaryLaunches> tail_bnd;

@@ -213,10 +213,9 @@ def main():
     # ---- overlapped tail (auto-on for multi-process jobs) vs in order; p=4 spans GPUs at world 4
     for pt in (2, 4):
         res = {}
-        for tail in ("0", "1", "1f", "k10"):
-            os.environ["MICS_TAIL_OVERLAP"] = "0" if tail == "k10" else tail[0]
+        for tail in ("0", "1", "1f"):
+            os.environ["MICS_TAIL_OVERLAP"] = tail[0]
             os.environ["MICS_TAIL_FUSED"] = "1" if tail == "1f" else "0"
-            os.environ["MICS_FTAIL"] = "1" if tail == "k10" else "0"
             e5 = Engine(n_ranks=n, world=world, world_rank=rank, device=local, arena_bytes=256 << 20)
             mdist.connect(e5)
             step = MicsStep(e5, Workload("tail", [1_500_000, 70_000, 12_345, 700_000, 40_000, 9_999, 33_333], p=pt, s=3),
@@ -231,8 +230,7 @@ def main():
             e5.close()
         os.environ.pop("MICS_TAIL_OVERLAP")
         os.environ.pop("MICS_TAIL_FUSED")
-        os.environ.pop("MICS_FTAIL")
-        for t in ("1", "1f", "k10"):
+        for t in ("1", "1f"):
             for x, y in zip(res["0"], res[t]):
                 expect(np.array_equal(x.view(np.uint32), y.view(np.uint32)),
                        f"overlapped tail ({t}) != in-order (p={pt})")
