@@ -679,8 +679,10 @@ def run_mics(args, wl, rank, world, local):
     # tables (this process, per step): pulled from peers over NVLink / local HBM r+w
     kernels = {"allgather": "k_copy (per-layer partition-group all-gather)",
                "reducescatter": "k_reduce (micro-step reduce-scatter + shard accumulate)",
-               "boundary": "k_reduce + k_adam (boundary all-reduce fused with Adam)" if world > 1 else
-                           "k_tail (K8: last micro-step reduce-scatter + boundary all-reduce + Adam, one pass)"}
+               "boundary": ("k_tail (K8: last micro-step reduce-scatter + boundary all-reduce + Adam, one pass)"
+                            if world == 1 else
+                            "k_fbnd (K9: per layer group boundary all-reduce + Adam in one launch, block flags)"
+                            if wl.n // wl.p > 1 else "k_adam (shards already reduced: Adam only)")}
     phases = {"allgather": (prof["allgather_ms"], stats.ag_launches, stats.ag_remote_bytes, stats.ag_hbm_bytes),
               "reducescatter": (prof["reducescatter_ms"], stats.rs_launches, stats.rs_remote_bytes,
                                 stats.rs_hbm_bytes),
