@@ -969,13 +969,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_fbnd(FbArg fa, AdamScalars sc, 
   const uint32_t r = fa.r, nrs = uint32_t(fa.nrs);
   const uint32_t per_round = nrs + uint32_t(fa.nad) * r;
   __shared__ uint32_t s_item;
-  // gridDim.x >= items: one item per CTA (CTAs retire, so the hardware can give freed
-  // slots to other streams' kernels); else persistent CTAs
-  const uint32_t items = fa.items;
-  const bool once = gridDim.x >= items;
-  const uint32_t last = once ? gridDim.x - 1 : items + gridDim.x - 1;
-  for (bool first = true;; first = false) {
-    if (once && !first) break;
+  const uint32_t items = fa.items, last = items + gridDim.x - 1;
+  for (;;) {
     __syncthreads();  // every thread read the previous item
     if (threadIdx.x == 0) {
       const uint32_t t = atomicAdd(fa.ticket, 1u);

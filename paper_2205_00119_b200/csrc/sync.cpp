@@ -397,11 +397,9 @@ Launch build_boundary_fused_range(mics_sync* st, const mics_adam* adam, uint64_t
   l.fb.nblk = nblk;
   l.fb.blk = blk;
   l.ndesc = int(rs.size() + ad.size());
-  // grid: one resident wave (MICS_FB_CTAS, experiments: CTAs per SM, at most the
-  // resident count, or 0: one CTA per item)
-  const char* ce = std::getenv("MICS_FB_CTAS");
-  const int per_sm = ce ? std::min(std::atoi(ce), ctx->occ_fbnd) : ctx->occ_fbnd;
-  const uint64_t wave = uint64_t(ctx->nsm) * uint64_t(per_sm > 0 ? per_sm : ctx->occ_fbnd);
+  // grid: one resident wave (measured: 1 CTA per SM 4.55 ms, one CTA per item 3.26 ms,
+  // the wave of 2 per SM 3.18 ms; C3 N=4 boundary)
+  const uint64_t wave = uint64_t(ctx->nsm) * uint64_t(ctx->occ_fbnd);
   // lag: Adam items of block t are taken two waves of CTAs after the fold of block t
   // (MICS_FB_LAG overrides), so they rarely wait (C3, 4 GPUs: 1 wave 3.29 ms, 2 waves
   // 3.18 ms, 8 rounds 3.64 ms)
@@ -410,7 +408,7 @@ Launch build_boundary_fused_range(mics_sync* st, const mics_adam* adam, uint64_t
   l.fb.lag = le ? uint32_t(std::max(0, std::atoi(le))) : uint32_t(ceil_div(2 * wave, std::max<uint32_t>(per_round, 1))) + 1;
   // rounds t = 0 .. nblk + lag - 1: the fold of block t, then Adam of block t - lag
   l.ntiles = l.ndesc ? (nblk + l.fb.lag) * per_round : 0;
-  l.grid = int(std::max<uint64_t>(per_sm <= 0 ? l.ntiles : std::min<uint64_t>(l.ntiles, wave), 1));
+  l.grid = int(std::max<uint64_t>(std::min<uint64_t>(l.ntiles, wave), 1));
   l.hier_sys = sys ? 1 : 0;
   l.adam = make_adam_scalars(adam->lr, adam->beta1, adam->beta2, adam->eps, adam->weight_decay, adam->step,
                              adam->grad_scale);

@@ -63,3 +63,37 @@ def test_relaxed_barriers_match_fenced_under_stress(m, monkeypatch):
     for x, y in zip(relaxed, fenced):
         assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
     assert all(np.isfinite(x).all() for x in relaxed)
+
+
+def _tail_run(m, monkeypatch, variant, steps):
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, Workload
+    monkeypatch.setenv("MICS_TAIL_OVERLAP", "0" if variant == "in_order" else "1")
+    monkeypatch.setenv("MICS_TAIL_FUSED", "1" if variant == "k9" else "0")
+    eng = m.Engine(n_ranks=8, arena_bytes=256 << 20, devices=[0, 1])
+    # p=2: each position's 4 replicas span both GPUs; the 300k / 131k layers give several
+    # K9 blocks per owner slice
+    step = MicsStep(eng, Workload("tail stress", [300_000, 9_000, 131_072, 4_099], p=2, s=2),
+                    StepOptions(seed=9, lr=1e-2))
+    for _ in range(steps // 100):
+        step.run(100)
+    eng.synchronize()
+    S = step.sync_info()[0].shard_elems
+    b = step.buffers()
+    out = [eng.d2h(b[k], r, S) for k in ("master", "exp_avg_sq") for r in range(8)]
+    out += [eng.d2h(b["param_bf16"], r, S, "bf16") for r in (0, 5)]
+    step.close()
+    eng.close()
+    return out
+
+
+def test_k9_block_flags_match_under_stress(m, monkeypatch):
+    """K9's relaxed per-block flags and item tickets (k_fbnd) over 500 back-to-back
+    replayed steps on two GPUs of one process: the same bits as the two-kernel boundary
+    and the in-order step.  A fold read before its owner's flag, or an Adam block before
+    the fold, would compound into different bits."""
+    ref = _tail_run(m, monkeypatch, "in_order", 500)
+    for v in ("two_kernel", "k9"):
+        got = _tail_run(m, monkeypatch, v, 500)
+        for x, y in zip(ref, got):
+            assert np.array_equal(x.view(np.uint16), y.view(np.uint16)), v
+    assert all(np.isfinite(x.astype(np.float32)).all() for x in ref[:16])
