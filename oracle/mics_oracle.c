@@ -3,6 +3,7 @@
 #include "mics_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -475,4 +476,83 @@ void ora_adam_f32(size_t count, float* param, float* m, float* v, const float* g
     param[i] = p;
     if (param_bf16) param_bf16[i] = ora_f32_to_bf16(p);
   }
+}
+
+/* ------------------------------------------------------------------------
+ * whole-shard expected step (see the header): test infrastructure for the
+ * full-size bit-exact check of the step driver
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  uint64_t seed;
+  int n, p, s, j;
+  const ora_seg_t* segs;
+  int nseg;
+  uint64_t lo, hi;
+  ora_adam_scalars_t sc;
+  float *master, *m, *v;
+  uint16_t* bf16;
+} step1_job_t;
+
+static float gen_one(uint64_t seed, int rank, int step, int layer, uint64_t idx) {
+  const uint64_t x = ora_splitmix64(gen_key(seed, rank, step, layer, idx));
+  return (float)((int32_t)(x >> 40) - (1 << 23)) * (1.0f / 8388608.0f);
+}
+
+static void* step1_worker(void* arg) {
+  const step1_job_t* J = (const step1_job_t*)arg;
+  const int r = J->n / J->p;
+  int q = 0;
+  while (q + 1 < J->nseg && J->segs[q + 1].so <= J->lo) ++q;
+  for (uint64_t x = J->lo; x < J->hi; ++x) {
+    while (q + 1 < J->nseg && J->segs[q + 1].so <= x) ++q;
+    const ora_seg_t* S = &J->segs[q];
+    const uint64_t pos = (uint64_t)J->j * S->c + (x - S->so), gi = S->go + pos;
+    const int valid = pos < S->len;
+    float red = 0.0f;
+    for (int gg = 0; gg < r; ++gg) { /* replica gg: partition group gg */
+      float acc = 0.0f;
+      for (int t = 0; t < J->s; ++t) {
+        float f = 0.0f;
+        if (valid) {
+          f = gen_one(J->seed, gg * J->p, t, 0, gi);
+          for (int i = 1; i < J->p; ++i) f = f + gen_one(J->seed, gg * J->p + i, t, 0, gi);
+        }
+        acc = t ? acc + f : 0.0f + f;
+      }
+      red = gg ? red + acc : acc;
+    }
+    float pm = gen_one(J->seed ^ 0x5EEDull, J->j, 0, 255, x), mm = 0.0f, vv = 0.0f;
+    uint16_t b;
+    ora_adam_f32(1, &pm, &mm, &vv, &red, &J->sc, &b);
+    J->master[x] = pm;
+    J->m[x] = mm;
+    J->v[x] = vv;
+    J->bf16[x] = b;
+  }
+  return NULL;
+}
+
+int ora_step1_shard(uint64_t seed, int n, int p, int s, int j, const ora_seg_t* segs, int nseg, uint64_t shard_elems,
+                    double lr, double b1, double b2, double eps, double wd, int threads, float* master, float* m,
+                    float* v, uint16_t* bf16) {
+  if (n <= 0 || p <= 0 || n % p || j < 0 || j >= p || nseg <= 0 || threads <= 0) return 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  step1_job_t jobs[256];
+  ora_adam_scalars_t sc;
+  ora_adam_scalars(lr, b1, b2, eps, wd, 1, 1.0 / ((double)n * s), &sc);
+  const uint64_t per = (shard_elems + threads - 1) / threads;
+  int started = 0;
+  for (int k = 0; k < threads; ++k) {
+    step1_job_t* J = &jobs[k];
+    J->seed = seed; J->n = n; J->p = p; J->s = s; J->j = j; J->segs = segs; J->nseg = nseg;
+    J->lo = (uint64_t)k * per;
+    J->hi = J->lo + per < shard_elems ? J->lo + per : shard_elems;
+    J->sc = sc; J->master = master; J->m = m; J->v = v; J->bf16 = bf16;
+    if (J->lo >= J->hi) break;
+    if (pthread_create(&th[k], NULL, step1_worker, J)) return 2;
+    ++started;
+  }
+  for (int k = 0; k < started; ++k) pthread_join(th[k], NULL);
+  return 0;
 }

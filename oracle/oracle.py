@@ -230,6 +230,21 @@ class Oracle:
                                   _I(step), C.c_double(grad_scale), C.byref(sc))
         return sc
 
+    def step1_shard(self, seed, n, p, s, j, segs, shard_elems, lr, b1=0.9, b2=0.999, eps=1e-8, wd=0.0,
+                    threads=None):
+        """Expected (master, m, v, bf16) of partition position j over its whole shard after
+        one step of a generated-gradient step-driver job (ora_step1_shard, see the header).
+        segs: (len, chunk, shard_off, grad_off) per layer."""
+        sg = np.array([tuple(int(t) for t in x) for x in segs], np.uint64).reshape(-1, 4)
+        out = [np.empty(shard_elems, np.float32) for _ in range(3)] + [np.empty(shard_elems, np.uint16)]
+        th = threads or min(64, os.cpu_count() or 1)
+        st = self.lib.ora_step1_shard(C.c_uint64(seed), _I(n), _I(p), _I(s), _I(j), _ptr(sg), _I(len(sg)),
+                                      C.c_uint64(shard_elems), C.c_double(lr), C.c_double(b1), C.c_double(b2),
+                                      C.c_double(eps), C.c_double(wd), _I(th), *[_ptr(a) for a in out])
+        if st:
+            raise OracleError(st, "step1_shard")
+        return tuple(out)
+
     def adam(self, param, m, v, grad, lr, b1, b2, eps, wd, step, grad_scale=1.0, want_bf16=False):
         """Returns updated copies (param, m, v, param_bf16_or_None)."""
         param = np.array(param, np.float32)

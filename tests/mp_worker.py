@@ -207,6 +207,21 @@ def main():
         check_sampled(ora, e6, step, wl3, opts3, e6.local_ranks, nsamples=150, seed=rank)
     except AssertionError as ex:
         expect(False, f"full-size C3 sampled check: {ex}")
+    # every element of every local rank's master and bf16 shard (the K9 boundary across
+    # processes) against the oracle's whole-shard step
+    info3, segs3 = step.sync_info()
+    S3 = info3.shard_elems
+    for j in sorted({r % wl3.p for r in e6.local_ranks}):
+        want, _, _, want_bf = ora.step1_shard(opts3.seed, wl3.n, wl3.p, wl3.s, j, segs3, S3, opts3.lr,
+                                              threads=max(1, (os.cpu_count() or 4) // world))
+        for r in e6.local_ranks:
+            if r % wl3.p != j:
+                continue
+            got = e6.d2h(step.buffers()["master"], r, S3)
+            nbad = int(np.count_nonzero(got.view(np.uint32) != want.view(np.uint32)))
+            expect(nbad == 0, f"full-size C3 master of rank {r}: {nbad} elements differ")
+            expect(np.array_equal(e6.d2h(step.buffers()["param_bf16"], r, S3, "bf16"), want_bf),
+                   f"full-size C3 bf16 of rank {r}")
     step.close()
     e6.close()
 

@@ -80,3 +80,42 @@ def test_c3_full_size_sampled_bitexact(oracle):
     check_sampled(oracle, eng, step, wl, opts, list(range(wl.n)))
     step.close()
     eng.close()
+
+
+@pytest.mark.parametrize("path", ["k8", "k9"])
+def test_c3_full_size_every_element_bitexact(oracle, monkeypatch, path):
+    """C3 at full size (334,088,192 parameters, n=8, p=2, s=4) on one GPU, EVERY shard
+    element of every rank: the device's master / bf16 (and m / v of two ranks) after one
+    step equal the oracle's whole-shard step (ora_step1_shard: the generator's
+    gradients folded in the reference's order, then Adam), bit for bit.  k8: the default
+    fused tail; k9: the overlapped tail with the fused layer-group boundary forced on one
+    GPU."""
+    from paper_2205_00119_b200.engine import Engine
+    from paper_2205_00119_b200.step import MicsStep, StepOptions, workloads
+    import bench
+    if path == "k9":
+        monkeypatch.setenv("MICS_FUSED_TAIL", "0")
+        monkeypatch.setenv("MICS_TAIL_OVERLAP", "1")
+        monkeypatch.setenv("MICS_TAIL_FUSED", "1")
+    wl = workloads()["C3"]
+    opts = StepOptions(seed=2205, lr=1e-4)
+    eng = Engine(n_ranks=wl.n, device=0, arena_bytes=bench.arena_bytes(wl, wl.n, True, wl.n))
+    step = MicsStep(eng, wl, opts)
+    info, segs = step.sync_info()
+    S = info.shard_elems
+    step.run(1)
+    eng.synchronize()
+    b = step.buffers()
+    for j in range(wl.p):
+        master, m, v, bf = oracle.step1_shard(opts.seed, wl.n, wl.p, wl.s, j, segs, S, opts.lr, opts.beta1,
+                                              opts.beta2, opts.eps, opts.weight_decay)
+        for r in range(j, wl.n, wl.p):
+            got = eng.d2h(b["master"], r, S)
+            bad = np.flatnonzero(got.view(np.uint32) != master.view(np.uint32))
+            assert bad.size == 0, (r, bad[:5], bad.size)
+            assert np.array_equal(eng.d2h(b["param_bf16"], r, S, "bf16"), bf), r
+        r = j  # the optimizer state of one replica per position
+        assert np.array_equal(eng.d2h(b["exp_avg"], r, S).view(np.uint32), m.view(np.uint32))
+        assert np.array_equal(eng.d2h(b["exp_avg_sq"], r, S).view(np.uint32), v.view(np.uint32))
+    step.close()
+    eng.close()
