@@ -189,7 +189,7 @@ struct FbAdJob {                      // one local rank (+ an optional second re
   float* v2;
   uint16_t* bf2;
   uint64_t elems, sub;                // group elements; slice length (multiple of the block)
-  uint32_t r, nblk, pad_, fstride;    // nblk = sub / block; fstride: flags per owner (the largest group's nblk)
+  uint32_t fstride, pad_;             // flags per owner (the largest group's blocks per slice)
 };
 struct FbArg {                        // one k_fbnd launch (device pointers into its descriptor blob)
   const FbRsJob* rs = nullptr;

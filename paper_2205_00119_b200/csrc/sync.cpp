@@ -386,8 +386,6 @@ Launch build_boundary_fused_range(mics_sync* st, const mics_adam* adam, uint64_t
       }
     J.elems = len;
     J.sub = sub;
-    J.r = uint32_t(r);
-    J.nblk = nblk;
     J.fstride = nblk_max;
     ad.push_back(J);
   }
