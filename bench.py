@@ -453,7 +453,6 @@ def nccl_compute_step(wl, rank, world, steps, warmup):
     side = torch.cuda.Stream()
     ev_g = [torch.cuda.Event() for _ in range(2)]
     ev_free = [torch.cuda.Event() for _ in range(2)]
-    main = torch.cuda.current_stream()
     L = len(ldy)
 
     def gather(l):
@@ -467,6 +466,10 @@ def nccl_compute_step(wl, rank, world, steps, warmup):
         return gathered[l % 2][:ldy[l] * h].view(ldy[l], h)
 
     def one():
+        main = torch.cuda.current_stream()  # a capture stream when graph-captured
+        side.wait_stream(main)  # the side stream joins this stream's work (and a capture)
+        for e in ev_free:
+            e.record(main)
         for t in range(s):
             g = grads[t % 2]
             gather(0)
@@ -498,6 +501,7 @@ def nccl_compute_step(wl, rank, world, steps, warmup):
             dist.all_reduce(acc, group=my_rg)
         opt.step()
         shard.copy_(master.detach().to(torch.bfloat16))
+        main.wait_stream(side)  # rejoin the side stream
 
     run, mode = graph_or_eager(one, warmup)
     torch.cuda.synchronize()
